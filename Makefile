@@ -1,0 +1,30 @@
+# Builds every native artefact in-tree (the .so files travel to the GPU box
+# with gpurun; they are git-ignored).
+#   make            -> paper_1303_4312_b200/lib/libcomerge_cuda.so + oracles
+NVCC ?= nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -Wall \
+           --expt-relaxed-constexpr -Iinclude
+PKG := paper_1303_4312_b200
+LIB := $(PKG)/lib/libcomerge_cuda.so
+SRCS := $(PKG)/csrc/comerge_cuda.cu $(PKG)/csrc/testkit.cu
+HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/comerge_cuda.h include/comerge_cuda_testkit.h
+OBJS := $(patsubst $(PKG)/csrc/%.cu,$(PKG)/lib/%.o,$(SRCS))
+
+all: $(LIB) oracle
+
+$(PKG)/lib/%.o: $(PKG)/csrc/%.cu $(HDRS)
+	@mkdir -p $(PKG)/lib
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(@:.o=.ptxas.txt) || (cat $(@:.o=.ptxas.txt); false)
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -f $(PKG)/lib/*.o $(PKG)/lib/*.so $(PKG)/lib/*.ptxas.txt
+	$(MAKE) -C oracle clean
+
+.PHONY: all oracle clean

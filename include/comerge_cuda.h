@@ -1,0 +1,204 @@
+/*
+ * comerge_cuda.h -- C ABI of the B200 (sm_100a) stable parallel merge.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj/include/comerge/{corank,merge,parallel}.hpp).  The
+ * reference is header-only C++ with no C ABI of its own; every entry point
+ * below names the reference interface it replaces.  All indices are size_t
+ * / uint64_t, all memory is caller-owned, and nothing here takes a torch or
+ * CUDA-runtime type: the stream argument is a `struct CUstream_st*`, which is
+ * exactly `cudaStream_t`.
+ *
+ * Two tiers:
+ *   comerge_cuda_*   asynchronous, DEVICE pointers, enqueued on `stream`,
+ *                    scratch from a caller workspace (or NULL: stream-ordered
+ *                    allocation inside the call).
+ *   comerge_merge_parallel_* / comerge_co_rank_*
+ *                    synchronous mirrors of the reference's templates taking
+ *                    HOST or DEVICE pointers (detected per call), filling a
+ *                    merge report like comerge::merge_report.
+ *
+ * Error behaviour mirrors the reference's exceptions as status codes; the
+ * message (same substrings as the reference's what()) is available from
+ * comerge_cuda_last_error() on the calling thread.
+ */
+#ifndef COMERGE_CUDA_H
+#define COMERGE_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+struct CUstream_st;
+typedef struct CUstream_st* comerge_stream_t; /* == cudaStream_t */
+
+typedef enum comerge_status {
+    COMERGE_OK = 0,
+    COMERGE_E_INVALID = 1, /* std::invalid_argument: length, alias, null, workers==0 */
+    COMERGE_E_RANGE = 2,   /* std::out_of_range: "rank out of range (exceeds m+n)"   */
+    COMERGE_E_LENGTH = 3,  /* std::length_error: m+n beyond the index range          */
+    COMERGE_E_CUDA = 4     /* launch / runtime failure (detail in last_error)         */
+} comerge_status;
+
+typedef enum comerge_key_kind {
+    COMERGE_KEY_I32 = 0,
+    COMERGE_KEY_U32 = 1,
+    COMERGE_KEY_U64 = 2
+} comerge_key_kind;
+
+/* Thread-local message of the last failing call ("" if none). */
+const char* comerge_cuda_last_error(void);
+/* ABI version (major*10000 + minor*100 + patch). */
+int comerge_cuda_abi_version(void);
+
+/* Instrumentation (bench / profiling): when set on the calling thread, every
+ * comerge_cuda_merge_* call records `before` on its stream right before the
+ * dominant merge kernel and `after` right after it, so a caller can time that
+ * kernel alone with cudaEventElapsedTime.  Pass NULLs to disable.  The
+ * arguments are cudaEvent_t handles. */
+void comerge_cuda_set_kernel_events(void* before, void* after);
+
+/* ------------------------------------------------------------ workspace */
+
+/* Bytes of scratch the merge entry points need for (m, n): the tile
+ * boundary co-ranks.  Replaces nothing in the reference (which allocates
+ * per-worker slots itself, parallel.hpp:189); CUB-style query. */
+size_t comerge_cuda_merge_workspace_bytes(size_t m, size_t n, int key_kind, int has_payload);
+size_t comerge_cuda_segmented_workspace_bytes(size_t total, size_t nseg, int key_kind);
+
+/* ------------------------------------------- asynchronous, device memory */
+
+/* Stable merge of sorted a[0,m) and b[0,n) into out[0,m+n), ties A-first.
+ * Replaces comerge::merge_parallel / merge_parallel_synced /
+ * stable_merge for keys with std::less<> (parallel.hpp:304-336,
+ * merge.hpp:52-68).  `out` must not overlap a or b (E_INVALID). */
+int comerge_cuda_merge_keys_i32(const int32_t* a, size_t m, const int32_t* b, size_t n,
+                                int32_t* out, void* ws, size_t ws_bytes, comerge_stream_t stream);
+int comerge_cuda_merge_keys_u32(const uint32_t* a, size_t m, const uint32_t* b, size_t n,
+                                uint32_t* out, void* ws, size_t ws_bytes,
+                                comerge_stream_t stream);
+int comerge_cuda_merge_keys_u64(const uint64_t* a, size_t m, const uint64_t* b, size_t n,
+                                uint64_t* out, void* ws, size_t ws_bytes,
+                                comerge_stream_t stream);
+
+/* Key-value merge (SoA keys + uint32 payload): the same decisions as the
+ * keys-only merge, payload moved with its key.  Replaces merge_parallel over
+ * a {key, val} struct with a key-only less (the reference's
+ * tagged<K>/tagged_key_less pattern, oracle.hpp:22-37). */
+int comerge_cuda_merge_pairs_i32(const int32_t* a_keys, const uint32_t* a_vals, size_t m,
+                                 const int32_t* b_keys, const uint32_t* b_vals, size_t n,
+                                 int32_t* out_keys, uint32_t* out_vals, void* ws, size_t ws_bytes,
+                                 comerge_stream_t stream);
+int comerge_cuda_merge_pairs_u32(const uint32_t* a_keys, const uint32_t* a_vals, size_t m,
+                                 const uint32_t* b_keys, const uint32_t* b_vals, size_t n,
+                                 uint32_t* out_keys, uint32_t* out_vals, void* ws,
+                                 size_t ws_bytes, comerge_stream_t stream);
+int comerge_cuda_merge_pairs_u64(const uint64_t* a_keys, const uint32_t* a_vals, size_t m,
+                                 const uint64_t* b_keys, const uint32_t* b_vals, size_t n,
+                                 uint64_t* out_keys, uint32_t* out_vals, void* ws,
+                                 size_t ws_bytes, comerge_stream_t stream);
+
+/* Segmented batch: pair s merges a[a_off[s], a_off[s+1]) with
+ * b[b_off[s], b_off[s+1]) into out[a_off[s]+b_off[s], ...).  a_off / b_off
+ * hold nseg+1 nondecreasing offsets (device memory) with a_off[0] =
+ * b_off[0] = 0, a_off[nseg] = m and b_off[nseg] = n (the caller passes m and
+ * n so the call never synchronises).  One launch for all pairs.  The reference has no batched
+ * API; this replaces a loop of comerge::stable_merge (merge.hpp:52-68). */
+int comerge_cuda_merge_segmented_i32(const int32_t* a, const uint64_t* a_off, size_t m,
+                                     const int32_t* b, const uint64_t* b_off, size_t n,
+                                     size_t nseg, int32_t* out, void* ws, size_t ws_bytes,
+                                     comerge_stream_t stream);
+int comerge_cuda_merge_segmented_u32(const uint32_t* a, const uint64_t* a_off, size_t m,
+                                     const uint32_t* b, const uint64_t* b_off, size_t n,
+                                     size_t nseg, uint32_t* out, void* ws, size_t ws_bytes,
+                                     comerge_stream_t stream);
+
+/* Batched co-rank (Algorithm 1 exactly, corank.hpp:72-121): for each
+ * ranks[q] (device array) writes j (k = ranks[q] - j) and, if the pointers
+ * are non-NULL, the reference's co_rank_stats {iterations, comparisons}.
+ * A rank > m+n yields out_j = UINT64_MAX (the reference throws
+ * std::out_of_range there; the synchronous comerge_co_rank_* below returns
+ * COMERGE_E_RANGE). */
+int comerge_cuda_co_rank_batch_i32(const uint64_t* ranks, size_t count, const int32_t* a,
+                                   size_t m, const int32_t* b, size_t n, uint64_t* out_j,
+                                   uint32_t* out_iterations, uint32_t* out_comparisons,
+                                   comerge_stream_t stream);
+int comerge_cuda_co_rank_batch_u32(const uint64_t* ranks, size_t count, const uint32_t* a,
+                                   size_t m, const uint32_t* b, size_t n, uint64_t* out_j,
+                                   uint32_t* out_iterations, uint32_t* out_comparisons,
+                                   comerge_stream_t stream);
+int comerge_cuda_co_rank_batch_u64(const uint64_t* ranks, size_t count, const uint64_t* a,
+                                   size_t m, const uint64_t* b, size_t n, uint64_t* out_j,
+                                   uint32_t* out_iterations, uint32_t* out_comparisons,
+                                   comerge_stream_t stream);
+
+/* -------------------------------- synchronous mirrors of the templates */
+
+/* comerge::merge_report (parallel.hpp:44-55) in C: the vectors are
+ * caller-provided arrays (block_sizes: `workers` entries, corank_iterations:
+ * 2*workers, or `workers` when synced), either may be NULL. */
+typedef struct comerge_merge_report {
+    uint64_t m;
+    uint64_t n;
+    uint64_t workers;
+    uint64_t wall_ns;     /* merge region on the device (CUDA events)        */
+    uint64_t e2e_ns;      /* whole call incl. host<->device copies           */
+    uint64_t h2d_bytes;   /* bytes copied host->device by this call          */
+    uint64_t d2h_bytes;   /* bytes copied device->host by this call          */
+    uint64_t tiles;       /* device output tiles (the GPU's unit of work)    */
+} comerge_merge_report;
+
+/* comerge::merge_parallel(a, b, out, workers) / merge_parallel_synced
+ * (parallel.hpp:304-336).  Pointers may be host or device memory (mixed is
+ * allowed); host data is staged through the device inside the call.
+ * `workers` >= 1 defines the reported block partition (partition_output,
+ * parallel.hpp:60-67) exactly as in the reference; the device always
+ * merges in its own fixed-size tiles, so the output is worker-independent
+ * (acceptance criterion 6). */
+int comerge_merge_parallel_i32(const int32_t* a, size_t m, const int32_t* b, size_t n,
+                               int32_t* out, size_t out_len, size_t workers, int synced,
+                               comerge_merge_report* report, uint64_t* block_sizes,
+                               uint32_t* corank_iterations);
+int comerge_merge_parallel_u32(const uint32_t* a, size_t m, const uint32_t* b, size_t n,
+                               uint32_t* out, size_t out_len, size_t workers, int synced,
+                               comerge_merge_report* report, uint64_t* block_sizes,
+                               uint32_t* corank_iterations);
+int comerge_merge_parallel_u64(const uint64_t* a, size_t m, const uint64_t* b, size_t n,
+                               uint64_t* out, size_t out_len, size_t workers, int synced,
+                               comerge_merge_report* report, uint64_t* block_sizes,
+                               uint32_t* corank_iterations);
+int comerge_merge_parallel_pairs_i32(const int32_t* a_keys, const uint32_t* a_vals, size_t m,
+                                     const int32_t* b_keys, const uint32_t* b_vals, size_t n,
+                                     int32_t* out_keys, uint32_t* out_vals, size_t out_len,
+                                     size_t workers, comerge_merge_report* report);
+int comerge_merge_parallel_pairs_u32(const uint32_t* a_keys, const uint32_t* a_vals, size_t m,
+                                     const uint32_t* b_keys, const uint32_t* b_vals, size_t n,
+                                     uint32_t* out_keys, uint32_t* out_vals, size_t out_len,
+                                     size_t workers, comerge_merge_report* report);
+int comerge_merge_parallel_pairs_u64(const uint64_t* a_keys, const uint32_t* a_vals, size_t m,
+                                     const uint64_t* b_keys, const uint32_t* b_vals, size_t n,
+                                     uint64_t* out_keys, uint32_t* out_vals, size_t out_len,
+                                     size_t workers, comerge_merge_report* report);
+
+/* comerge::co_rank(target, a, b, less, stats) (corank.hpp:128-133); host or
+ * device pointers; iterations / comparisons may be NULL. */
+int comerge_co_rank_i32(uint64_t target, const int32_t* a, size_t m, const int32_t* b, size_t n,
+                        uint64_t* j, uint64_t* k, uint32_t* iterations, uint32_t* comparisons);
+int comerge_co_rank_u32(uint64_t target, const uint32_t* a, size_t m, const uint32_t* b,
+                        size_t n, uint64_t* j, uint64_t* k, uint32_t* iterations,
+                        uint32_t* comparisons);
+int comerge_co_rank_u64(uint64_t target, const uint64_t* a, size_t m, const uint64_t* b,
+                        size_t n, uint64_t* j, uint64_t* k, uint32_t* iterations,
+                        uint32_t* comparisons);
+
+/* comerge::partition_output(total, workers, r) (parallel.hpp:60-67). */
+int comerge_partition_output(uint64_t total, uint64_t workers, uint64_t r, uint64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* COMERGE_CUDA_H */

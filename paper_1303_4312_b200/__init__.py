@@ -1,0 +1,14 @@
+"""B200-native (sm_100a) stable parallel merge of arXiv 1303.4312.
+
+The product is ``lib/libcomerge_cuda.so`` (C ABI: include/comerge_cuda.h,
+C++ shim: include/comerge/cuda.hpp).  This package is its Python mirror of
+the reference API (see ``comerge``).
+"""
+from .comerge import (BlockAssignment, ComparisonCounter, CoRankStats, MergeOptions,  # noqa: F401
+                      MergeReport, co_rank, co_rank_batch, co_rank_counted, merge_pairs,
+                      merge_parallel, merge_parallel_synced, merge_segmented, partition_output,
+                      plan, stable_merge)
+
+__all__ = ["co_rank", "co_rank_counted", "co_rank_batch", "stable_merge", "partition_output",
+           "plan", "merge_parallel", "merge_parallel_synced", "merge_pairs", "merge_segmented",
+           "MergeReport", "MergeOptions", "CoRankStats", "ComparisonCounter", "BlockAssignment"]

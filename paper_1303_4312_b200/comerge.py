@@ -1,0 +1,329 @@
+"""Python mirror of the reference's co-rank / merge API, backed by sm_100a kernels.
+
+Names, argument meaning and error behaviour follow the reference library
+(/root/reference/proj/include/comerge/):
+
+===========================  ==============================================
+this module                  reference
+===========================  ==============================================
+``co_rank``                  ``comerge::co_rank``            corank.hpp:128-133
+``co_rank_counted``          ``comerge::co_rank_counted``    corank.hpp:138-147
+``stable_merge``             ``comerge::stable_merge``       merge.hpp:52-68
+``partition_output``         ``comerge::partition_output``   parallel.hpp:60-67
+``plan``                     ``comerge::plan``               parallel.hpp:94-115
+``merge_parallel``           ``comerge::merge_parallel``     parallel.hpp:304-317
+``merge_parallel_synced``    ``comerge::merge_parallel_synced`` :323-336
+``MergeReport``              ``comerge::merge_report``       parallel.hpp:44-55
+===========================  ==============================================
+
+Exceptions: ``ValueError`` = std::invalid_argument, ``IndexError`` =
+std::out_of_range, ``OverflowError`` = std::length_error (same message
+substrings as the reference).  Arrays may be numpy (host) or torch CUDA
+tensors (device); every merge runs on the GPU through the C ABI in
+``include/comerge_cuda.h`` -- there is no CPU fallback.
+
+Extensions beyond the reference (the B200 hot path's other shapes):
+``merge_pairs`` (key + uint32 payload), ``merge_segmented`` (batched
+independent pairs) and ``co_rank_batch``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _native as N
+
+try:  # torch is plumbing only (device memory + streams)
+    import torch
+except Exception:  # pragma: no cover
+    torch = None
+
+_SUFFIX = {"int32": "i32", "uint32": "u32", "uint64": "u64"}
+_KIND = {"i32": N.KEY_I32, "u32": N.KEY_U32, "u64": N.KEY_U64}
+
+
+def _is_torch(x) -> bool:
+    return torch is not None and isinstance(x, torch.Tensor)
+
+
+def _dtype_name(x) -> str:
+    if _is_torch(x):
+        return str(x.dtype).replace("torch.", "")
+    return np.dtype(x.dtype).name
+
+
+def _suffix(x) -> str:
+    name = _dtype_name(x)
+    if name not in _SUFFIX:
+        raise TypeError(f"comerge: unsupported key dtype {name} (int32, uint32, uint64)")
+    return _SUFFIX[name]
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if _is_torch(x):
+        if not x.is_contiguous():
+            raise ValueError("comerge: arrays must be contiguous")
+        return C.c_void_p(x.data_ptr()) if x.numel() else None
+    if not x.flags["C_CONTIGUOUS"]:
+        raise ValueError("comerge: arrays must be contiguous")
+    return C.c_void_p(x.ctypes.data) if x.size else None
+
+
+def _len(x) -> int:
+    return int(x.numel()) if _is_torch(x) else int(x.size)
+
+
+def _stream(x=None):
+    if x is not None and _is_torch(x) and x.is_cuda:
+        return C.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)
+    return None
+
+
+def _empty_like_merge(a, total):
+    if _is_torch(a):
+        return torch.empty(total, dtype=a.dtype, device=a.device)
+    return np.empty(total, dtype=a.dtype)
+
+
+# ----------------------------------------------------------------- co_rank
+
+@dataclass
+class CoRankStats:
+    """comerge::co_rank_stats (corank.hpp:44-47)."""
+    iterations: int = 0
+    comparisons: int = 0
+
+
+@dataclass
+class ComparisonCounter:
+    """comerge::comparison_counter (corank.hpp:50-52)."""
+    count: int = 0
+
+
+def co_rank(target: int, a, b, stats: Optional[CoRankStats] = None):
+    """Unique split (j, k), j + k = target, of the stable merge of a and b.
+
+    Runs Algorithm 1 (corank.hpp:72-121) on the device; raises IndexError
+    ("rank out of range") when target > m + n, like the reference.
+    """
+    suf = _suffix(a)
+    if _suffix(b) != suf:
+        raise TypeError("co_rank: a and b must have the same dtype")
+    if target < 0:
+        raise IndexError("co_rank: rank out of range (exceeds m+n)")
+    j, k, it, cmp = C.c_uint64(), C.c_uint64(), C.c_uint32(), C.c_uint32()
+    N.check(getattr(N.lib, f"comerge_co_rank_{suf}")(
+        int(target), _ptr(a), _len(a), _ptr(b), _len(b), C.byref(j), C.byref(k), C.byref(it),
+        C.byref(cmp)))
+    if stats is not None:
+        stats.iterations, stats.comparisons = it.value, cmp.value
+    return (j.value, k.value)
+
+
+def co_rank_counted(target: int, a, b, counter: ComparisonCounter):
+    st = CoRankStats()
+    res = co_rank(target, a, b, st)
+    counter.count += st.comparisons
+    return res
+
+
+def co_rank_batch(ranks, a, b, with_stats: bool = False):
+    """Device batch of co-ranks: returns j (uint64 tensor) [, iterations, comparisons]."""
+    suf = _suffix(a)
+    dev = a.device
+    q = int(ranks.numel())
+    j = torch.empty(q, dtype=torch.uint64, device=dev)
+    it = torch.empty(q, dtype=torch.uint32, device=dev) if with_stats else None
+    cmp = torch.empty(q, dtype=torch.uint32, device=dev) if with_stats else None
+    N.check(getattr(N.lib, f"comerge_cuda_co_rank_batch_{suf}")(
+        _ptr(ranks), q, _ptr(a), _len(a), _ptr(b), _len(b), _ptr(j), _ptr(it), _ptr(cmp),
+        _stream(a)))
+    return (j, it, cmp) if with_stats else j
+
+
+# ------------------------------------------------------------------- merges
+
+def partition_output(total: int, workers: int, r: int) -> int:
+    """floor(r * total / workers) without overflow (parallel.hpp:60-67)."""
+    if workers < 0 or r < 0:
+        raise ValueError("partition_output: worker count must be positive")
+    out = C.c_uint64()
+    N.check(N.lib.comerge_partition_output(total, workers, r, C.byref(out)))
+    return out.value
+
+
+def _check_out(who, a, b, out):
+    if _len(out) != _len(a) + _len(b):
+        raise ValueError(f"{who}: output length must equal |a| + |b|")
+
+
+def stable_merge(a, b, out=None):
+    """Stable two-way merge into out (merge.hpp:52-68).  Device tensors run
+    asynchronously on the current stream; host arrays synchronously."""
+    suf = _suffix(a)
+    if out is None:
+        out = _empty_like_merge(a, _len(a) + _len(b))
+    _check_out("stable_merge", a, b, out)
+    if _is_torch(a) and a.is_cuda:
+        N.check(getattr(N.lib, f"comerge_cuda_merge_keys_{suf}")(
+            _ptr(a), _len(a), _ptr(b), _len(b), _ptr(out), None, 0, _stream(a)))
+    else:
+        rep = N.MergeReport()
+        rc = getattr(N.lib, f"comerge_merge_parallel_{suf}")(
+            _ptr(a), _len(a), _ptr(b), _len(b), _ptr(out), _len(out), 1, 0, C.byref(rep),
+            None, None)
+        if rc == N.E_INVALID:
+            raise ValueError(N.last_error().replace("merge_parallel", "stable_merge"))
+        N.check(rc)
+    return out
+
+
+@dataclass
+class MergeReport:
+    """comerge::merge_report (parallel.hpp:44-55) plus device-side fields."""
+    m: int = 0
+    n: int = 0
+    workers: int = 0
+    wall_ns: int = 0
+    block_sizes: List[int] = field(default_factory=list)
+    corank_iterations: List[int] = field(default_factory=list)
+    comparisons: Optional[int] = None
+    verified: Optional[bool] = None
+    speedup_vs_p1: Optional[float] = None
+    note: str = ""
+    # B200 extras
+    e2e_ns: int = 0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+    tiles: int = 0
+
+
+@dataclass
+class MergeOptions:
+    """comerge::merge_options (parallel.hpp:39-42).  `mode` is accepted for
+    API compatibility; the device schedule does not depend on it.
+    `count_comparisons` is not supported on the device (raises)."""
+    mode: str = "threads"
+    count_comparisons: bool = False
+
+
+def _merge_parallel(who, a, b, out, workers, opts, synced):
+    suf = _suffix(a)
+    if _suffix(b) != suf or _suffix(out) != suf:
+        raise TypeError(f"{who}: a, b and out must share one dtype")
+    if opts is not None and opts.count_comparisons:
+        raise ValueError(f"{who}: comparison counting is not available on the device")
+    if workers < 0:
+        raise ValueError("merge_parallel: worker count must be positive")
+    rep = N.MergeReport()
+    bs = np.zeros(max(workers, 1), np.uint64)
+    its = np.zeros(2 * max(workers, 1), np.uint32)
+    if _is_torch(out) and out.is_cuda:
+        torch.cuda.current_stream(out.device).synchronize()
+    N.check(getattr(N.lib, f"comerge_merge_parallel_{suf}")(
+        _ptr(a), _len(a), _ptr(b), _len(b), _ptr(out), _len(out), workers, int(synced),
+        C.byref(rep), C.c_void_p(bs.ctypes.data), C.c_void_p(its.ctypes.data)))
+    return MergeReport(
+        m=rep.m, n=rep.n, workers=rep.workers, wall_ns=rep.wall_ns,
+        block_sizes=[int(x) for x in bs[:workers]],
+        corank_iterations=[int(x) for x in its[:(workers if synced else 2 * workers)]],
+        e2e_ns=rep.e2e_ns, h2d_bytes=rep.h2d_bytes, d2h_bytes=rep.d2h_bytes, tiles=rep.tiles)
+
+
+def merge_parallel(a, b, out, workers: int, less=None, opts: Optional[MergeOptions] = None):
+    """comerge::merge_parallel (parallel.hpp:304-317): merges a and b stably
+    into out and reports per-worker block sizes and co-rank iterations for
+    the reference's `workers`-way output partition.  Only the default
+    ordering is supported (`less` must be None)."""
+    if less is not None:
+        raise TypeError("merge_parallel: only the default std::less<> ordering runs on the device")
+    return _merge_parallel("merge_parallel", a, b, out, workers, opts, False)
+
+
+def merge_parallel_synced(a, b, out, workers: int, less=None,
+                          opts: Optional[MergeOptions] = None):
+    """comerge::merge_parallel_synced (parallel.hpp:323-336)."""
+    if less is not None:
+        raise TypeError("merge_parallel_synced: only the default ordering runs on the device")
+    return _merge_parallel("merge_parallel_synced", a, b, out, workers, opts, True)
+
+
+@dataclass
+class BlockAssignment:
+    """comerge::block_assignment (parallel.hpp:70-84)."""
+    worker: int = 0
+    out_begin: int = 0
+    out_end: int = 0
+    a_begin: int = 0
+    a_end: int = 0
+    b_begin: int = 0
+    b_end: int = 0
+
+    def as_tuple(self):
+        return (self.worker, self.out_begin, self.out_end, self.a_begin, self.a_end,
+                self.b_begin, self.b_end)
+
+
+def plan(a, b, workers: int):
+    """comerge::plan (parallel.hpp:94-115): per-worker assignments from two
+    independent co-ranks per block, computed in one device batch."""
+    if workers <= 0:
+        raise ValueError("plan: worker count must be positive")
+    total = _len(a) + _len(b)
+    bounds = [partition_output(total, workers, r) for r in range(workers + 1)]
+    if _is_torch(a) and a.is_cuda:
+        ranks = torch.tensor(bounds, dtype=torch.uint64, device=a.device)
+        js = co_rank_batch(ranks, a, b).cpu().numpy().astype(np.uint64)
+    else:
+        js = [co_rank(i, a, b)[0] for i in bounds]
+    blocks = []
+    for r in range(workers):
+        lo, hi = bounds[r], bounds[r + 1]
+        ja, jb = int(js[r]), int(js[r + 1])
+        blocks.append(BlockAssignment(r, lo, hi, ja, jb, lo - ja, hi - jb))
+    return blocks
+
+
+def merge_pairs(a_keys, a_vals, b_keys, b_vals, out_keys=None, out_vals=None):
+    """Key-value stable merge on the device (uint32 payload moves with its key)."""
+    suf = _suffix(a_keys)
+    total = _len(a_keys) + _len(b_keys)
+    if out_keys is None:
+        out_keys = _empty_like_merge(a_keys, total)
+    if out_vals is None:
+        out_vals = _empty_like_merge(a_vals, total)
+    if _len(a_vals) != _len(a_keys) or _len(b_vals) != _len(b_keys):
+        raise ValueError("merge_pairs: payload length must equal key length")
+    _check_out("merge_pairs", a_keys, b_keys, out_keys)
+    _check_out("merge_pairs", a_vals, b_vals, out_vals)
+    if _is_torch(a_keys) and a_keys.is_cuda:
+        N.check(getattr(N.lib, f"comerge_cuda_merge_pairs_{suf}")(
+            _ptr(a_keys), _ptr(a_vals), _len(a_keys), _ptr(b_keys), _ptr(b_vals), _len(b_keys),
+            _ptr(out_keys), _ptr(out_vals), None, 0, _stream(a_keys)))
+    else:
+        rep = N.MergeReport()
+        N.check(getattr(N.lib, f"comerge_merge_parallel_pairs_{suf}")(
+            _ptr(a_keys), _ptr(a_vals), _len(a_keys), _ptr(b_keys), _ptr(b_vals), _len(b_keys),
+            _ptr(out_keys), _ptr(out_vals), total, 1, C.byref(rep)))
+    return out_keys, out_vals
+
+
+def merge_segmented(a, a_off, b, b_off, out=None):
+    """Merge every pair s (a[a_off[s]:a_off[s+1]], b[b_off[s]:b_off[s+1]]) into
+    out[a_off[s]+b_off[s]:...] in one device launch (device tensors)."""
+    suf = _suffix(a)
+    if suf == "u64":
+        raise TypeError("merge_segmented: int32 / uint32 keys")
+    nseg = int(a_off.numel()) - 1
+    if out is None:
+        out = _empty_like_merge(a, _len(a) + _len(b))
+    _check_out("merge_segmented", a, b, out)
+    N.check(getattr(N.lib, f"comerge_cuda_merge_segmented_{suf}")(
+        _ptr(a), _ptr(a_off), _len(a), _ptr(b), _ptr(b_off), _len(b), max(nseg, 0), _ptr(out),
+        None, 0, _stream(a)))
+    return out

@@ -1,0 +1,510 @@
+// comerge_cuda.cu -- C ABI (include/comerge_cuda.h) over the sm_100a merge
+// kernels.  Host-side contract checks mirror the reference's exceptions
+// (corank.hpp:67-79, merge.hpp:61-66, parallel.hpp:61-64, :185-186,
+// :284-295) as status codes with the same message substrings.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/comerge_cuda.h"
+#include "merge_tile.cuh"
+
+using namespace comerge_b200;
+
+namespace {
+
+thread_local std::string g_error;
+thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;
+
+void mark_before(cudaStream_t s) {
+    if (g_ev_before) cudaEventRecord(g_ev_before, s);
+}
+void mark_after(cudaStream_t s) {
+    if (g_ev_after) cudaEventRecord(g_ev_after, s);
+}
+
+int fail(int code, const std::string& msg) {
+    g_error = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    g_error = std::string(where) + ": " + cudaGetErrorString(e);
+    return COMERGE_E_CUDA;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// merge.hpp:35-45 on byte ranges
+bool overlaps(const void* x, size_t xbytes, const void* y, size_t ybytes) {
+    if (xbytes == 0 || ybytes == 0) return false;
+    const auto xb = reinterpret_cast<uintptr_t>(x), yb = reinterpret_cast<uintptr_t>(y);
+    return xb < yb + ybytes && yb < xb + xbytes;
+}
+
+constexpr uint64_t kMaxTotal = uint64_t(1) << 40;  // tile ids fit a 1-D grid
+
+uint64_t div_up(uint64_t x, uint64_t y) { return (x + y - 1) / y; }
+size_t round256(size_t x) { return (x + 255) / 256 * 256; }
+
+// Stream-ordered scratch: caller workspace, or cudaMallocAsync when ws == NULL.
+struct scratch {
+    void* ptr = nullptr;
+    bool owned = false;
+    cudaStream_t stream = nullptr;
+    int acquire(void* ws, size_t ws_bytes, size_t need, cudaStream_t s) {
+        stream = s;
+        if (need == 0) return COMERGE_OK;
+        if (ws) {
+            if (ws_bytes < need)
+                return fail(COMERGE_E_INVALID, "comerge: workspace too small (need " +
+                                                   std::to_string(need) + " bytes)");
+            ptr = ws;
+            return COMERGE_OK;
+        }
+        const cudaError_t e = cudaMallocAsync(&ptr, need, s);
+        if (e != cudaSuccess) return cuda_fail(e, "comerge: workspace allocation");
+        owned = true;
+        return COMERGE_OK;
+    }
+    ~scratch() {
+        if (owned) cudaFreeAsync(ptr, stream);
+    }
+};
+
+int check_launch(const char* where) {
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? COMERGE_OK : cuda_fail(e, where);
+}
+
+template <typename K>
+size_t merge_ws_bytes(size_t m, size_t n) {
+    if (m > SIZE_MAX - n) return 0;
+    const uint64_t total = m + n;
+    if (total == 0) return 0;
+    return round256((div_up(total, tile_cfg<K>::kTile) + 1) * sizeof(uint64_t));
+}
+
+template <typename K>
+size_t seg_ws_bytes(size_t total) {
+    if (total == 0) return 0;
+    return 2 * round256((div_up(total, seg_cfg<K>::kTile) + 1) * sizeof(uint64_t));
+}
+
+// Common contract of every merge entry (corank.hpp:67-70, merge.hpp:61-66).
+template <typename K>
+int check_merge_args(const char* who, const K* a, size_t m, const K* b, size_t n, const K* out,
+                     const uint32_t* av, const uint32_t* bv, const uint32_t* outv, bool has_v) {
+    if (m > SIZE_MAX - n)
+        return fail(COMERGE_E_LENGTH, "comerge: combined input length exceeds index range");
+    const uint64_t total = m + n;
+    if (total > kMaxTotal)
+        return fail(COMERGE_E_LENGTH, std::string(who) +
+                                          ": combined input length exceeds the device index range");
+    if ((m && !a) || (n && !b) || (total && !out))
+        return fail(COMERGE_E_INVALID, std::string(who) + ": null data pointer");
+    if (has_v && ((m && !av) || (n && !bv) || (total && !outv)))
+        return fail(COMERGE_E_INVALID, std::string(who) + ": null payload pointer");
+    const size_t ob = total * sizeof(K);
+    if (overlaps(a, m * sizeof(K), out, ob) || overlaps(b, n * sizeof(K), out, ob))
+        return fail(COMERGE_E_INVALID, std::string(who) + ": output must not alias an input");
+    if (has_v) {
+        const size_t vb = total * sizeof(uint32_t);
+        if (overlaps(av, m * 4, outv, vb) || overlaps(bv, n * 4, outv, vb) ||
+            overlaps(a, m * sizeof(K), outv, vb) || overlaps(b, n * sizeof(K), outv, vb) ||
+            overlaps(av, m * 4, out, ob) || overlaps(bv, n * 4, out, ob) ||
+            overlaps(out, ob, outv, vb))
+            return fail(COMERGE_E_INVALID, std::string(who) + ": output must not alias an input");
+    }
+    return COMERGE_OK;
+}
+
+template <typename K, bool HAS_V>
+int merge_device(const K* a, const uint32_t* av, size_t m, const K* b, const uint32_t* bv,
+                 size_t n, K* out, uint32_t* outv, void* ws, size_t ws_bytes, cudaStream_t s) {
+    const char* who = HAS_V ? "merge_pairs" : "merge_keys";
+    if (int rc = check_merge_args<K>(who, a, m, b, n, out, av, bv, outv, HAS_V)) return rc;
+    const uint64_t total = uint64_t(m) + n;
+    if (total == 0) return COMERGE_OK;
+    constexpr int T = tile_cfg<K>::kTile;
+    const uint64_t ntiles = div_up(total, T);
+    const uint64_t nbound = ntiles + 1;
+    scratch sc;
+    if (int rc = sc.acquire(ws, ws_bytes, merge_ws_bytes<K>(m, n), s)) return rc;
+    uint64_t* bj = static_cast<uint64_t*>(sc.ptr);
+    partition_kernel<K><<<unsigned(div_up(nbound, 256)), 256, 0, s>>>(a, m, b, n, T, nbound, bj);
+    if (int rc = check_launch("comerge: partition launch")) return rc;
+    int flags = 0;
+    flags |= aligned16(a) ? kAAligned : 0;
+    flags |= aligned16(b) ? kBAligned : 0;
+    flags |= aligned16(out) ? kOutAligned : 0;
+    flags |= aligned16(av) ? kAVAligned : 0;
+    flags |= aligned16(bv) ? kBVAligned : 0;
+    flags |= aligned16(outv) ? kOutVAligned : 0;
+    mark_before(s);
+    merge_tile_kernel<K, HAS_V><<<unsigned(ntiles), tile_cfg<K>::kThreads, 0, s>>>(
+        a, av, m, b, bv, n, out, outv, bj, flags);
+    mark_after(s);
+    return check_launch("comerge: merge launch");
+}
+
+template <typename K>
+int merge_segmented_device(const K* a, const uint64_t* a_off, size_t m, const K* b,
+                           const uint64_t* b_off, size_t n, size_t nseg, K* out, void* ws,
+                           size_t ws_bytes, cudaStream_t s) {
+    if (nseg == 0) {
+        if (m || n) return fail(COMERGE_E_INVALID, "merge_segmented: no segments for nonempty input");
+        return COMERGE_OK;
+    }
+    if (!a_off || !b_off) return fail(COMERGE_E_INVALID, "merge_segmented: null offsets");
+    if (int rc = check_merge_args<K>("merge_segmented", a, m, b, n, out, nullptr, nullptr,
+                                     nullptr, false))
+        return rc;
+    const uint64_t total = m + n;
+    if (total == 0) return COMERGE_OK;
+    constexpr int T = seg_cfg<K>::kTile;
+    const uint64_t ntiles = div_up(total, T);
+    const uint64_t nbound = ntiles + 1;
+    scratch sc;
+    if (int rc = sc.acquire(ws, ws_bytes, seg_ws_bytes<K>(total), s)) return rc;
+    uint64_t* bj = static_cast<uint64_t*>(sc.ptr);
+    uint64_t* bseg = bj + round256(nbound * sizeof(uint64_t)) / sizeof(uint64_t);
+    seg_partition_kernel<K><<<unsigned(div_up(nbound, 256)), 256, 0, s>>>(
+        a, a_off, b, b_off, nseg, total, T, nbound, bj, bseg);
+    if (int rc = check_launch("comerge: segmented partition launch")) return rc;
+    int flags = 0;
+    flags |= aligned16(a) ? kAAligned : 0;
+    flags |= aligned16(b) ? kBAligned : 0;
+    flags |= aligned16(out) ? kOutAligned : 0;
+    mark_before(s);
+    seg_merge_tile_kernel<K><<<unsigned(ntiles), seg_cfg<K>::kThreads, 0, s>>>(
+        a, a_off, m, b, b_off, n, out, bj, bseg, flags);
+    mark_after(s);
+    return check_launch("comerge: segmented merge launch");
+}
+
+template <typename K>
+int co_rank_batch_device(const uint64_t* ranks, size_t count, const K* a, size_t m, const K* b,
+                         size_t n, uint64_t* out_j, uint32_t* out_it, uint32_t* out_cmp,
+                         cudaStream_t s) {
+    if (m > SIZE_MAX - n)
+        return fail(COMERGE_E_LENGTH, "comerge: combined input length exceeds index range");
+    if (count == 0) return COMERGE_OK;
+    if (!ranks || !out_j || (m && !a) || (n && !b))
+        return fail(COMERGE_E_INVALID, "co_rank: null pointer");
+    co_rank_batch_kernel<K><<<unsigned(div_up(count, 128)), 128, 0, s>>>(ranks, count, a, m, b, n,
+                                                                       out_j, out_it, out_cmp);
+    return check_launch("comerge: co_rank launch");
+}
+
+// ------------------------------------------------ synchronous mirrors
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+cudaStream_t sync_stream() {
+    thread_local cudaStream_t s = [] {
+        cudaStream_t st = nullptr;
+        cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+        return st;
+    }();
+    return s;
+}
+
+// Device view of a possibly-host array (copied in on `s` when host).
+struct staged {
+    void* dev = nullptr;
+    bool owned = false;
+    cudaStream_t s = nullptr;
+    int in(const void* src, size_t bytes, cudaStream_t st, uint64_t* h2d) {
+        s = st;
+        if (bytes == 0 || src == nullptr) return COMERGE_OK;
+        if (is_device_ptr(src)) {
+            dev = const_cast<void*>(src);
+            return COMERGE_OK;
+        }
+        cudaError_t e = cudaMallocAsync(&dev, bytes, st);
+        if (e != cudaSuccess) return cuda_fail(e, "comerge: device staging allocation");
+        owned = true;
+        e = cudaMemcpyAsync(dev, src, bytes, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return cuda_fail(e, "comerge: host->device copy");
+        if (h2d) *h2d += bytes;
+        return COMERGE_OK;
+    }
+    int out_alloc(void* dst, size_t bytes, cudaStream_t st) {
+        s = st;
+        if (bytes == 0 || dst == nullptr) return COMERGE_OK;
+        if (is_device_ptr(dst)) {
+            dev = dst;
+            return COMERGE_OK;
+        }
+        const cudaError_t e = cudaMallocAsync(&dev, bytes, st);
+        if (e != cudaSuccess) return cuda_fail(e, "comerge: device staging allocation");
+        owned = true;
+        return COMERGE_OK;
+    }
+    int back(void* dst, size_t bytes, uint64_t* d2h) {
+        if (!owned || bytes == 0) return COMERGE_OK;
+        const cudaError_t e = cudaMemcpyAsync(dst, dev, bytes, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) return cuda_fail(e, "comerge: device->host copy");
+        if (d2h) *d2h += bytes;
+        return COMERGE_OK;
+    }
+    ~staged() {
+        if (owned) cudaFreeAsync(dev, s);
+    }
+};
+
+// parallel.hpp:60-67
+int partition_output_impl(uint64_t total, uint64_t workers, uint64_t r, uint64_t* out) {
+    if (workers == 0)
+        return fail(COMERGE_E_INVALID, "partition_output: worker count must be positive");
+    if (r > workers) return fail(COMERGE_E_INVALID, "partition_output: worker id out of range");
+    *out = uint64_t((unsigned __int128)r * total / workers);
+    return COMERGE_OK;
+}
+
+struct event_pair {
+    cudaEvent_t a = nullptr, b = nullptr;
+    event_pair() {
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+    }
+    ~event_pair() {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    }
+    uint64_t ns() const {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        return uint64_t(double(ms) * 1e6);
+    }
+};
+
+template <typename K, bool HAS_V>
+int merge_parallel_sync(const K* a, const uint32_t* av, size_t m, const K* b, const uint32_t* bv,
+                        size_t n, K* out, uint32_t* outv, size_t out_len, size_t workers,
+                        int synced, comerge_merge_report* rep, uint64_t* block_sizes,
+                        uint32_t* corank_iterations) {
+    const char* who = synced ? "merge_parallel_synced" : "merge_parallel";
+    // checked_output (parallel.hpp:284-295), then workers (:185-186)
+    if (m > SIZE_MAX - n)
+        return fail(COMERGE_E_LENGTH, "comerge: combined input length exceeds index range");
+    if (out_len != m + n)
+        return fail(COMERGE_E_INVALID, std::string(who) + ": output length must equal |a| + |b|");
+    if (overlaps(a, m * sizeof(K), out, out_len * sizeof(K)) ||
+        overlaps(b, n * sizeof(K), out, out_len * sizeof(K)))
+        return fail(COMERGE_E_INVALID, std::string(who) + ": output must not alias an input");
+    if (workers == 0)
+        return fail(COMERGE_E_INVALID, "merge_parallel: worker count must be positive");
+    const uint64_t total = m + n;
+    cudaStream_t s = sync_stream();
+    event_pair e2e, dev;
+    uint64_t h2d = 0, d2h = 0;
+    cudaEventRecord(e2e.a, s);
+    int rc = COMERGE_OK;
+    {
+        staged da, db, dav, dbv, dout, doutv;
+        if ((rc = da.in(a, m * sizeof(K), s, &h2d))) return rc;
+        if ((rc = db.in(b, n * sizeof(K), s, &h2d))) return rc;
+        if (HAS_V) {
+            if ((rc = dav.in(av, m * 4, s, &h2d))) return rc;
+            if ((rc = dbv.in(bv, n * 4, s, &h2d))) return rc;
+            if ((rc = doutv.out_alloc(outv, total * 4, s))) return rc;
+        }
+        if ((rc = dout.out_alloc(out, total * sizeof(K), s))) return rc;
+        cudaEventRecord(dev.a, s);
+        rc = merge_device<K, HAS_V>(static_cast<const K*>(da.dev),
+                                    static_cast<const uint32_t*>(dav.dev), m,
+                                    static_cast<const K*>(db.dev),
+                                    static_cast<const uint32_t*>(dbv.dev), n,
+                                    static_cast<K*>(dout.dev), static_cast<uint32_t*>(doutv.dev),
+                                    nullptr, 0, s);
+        if (rc) return rc;
+        cudaEventRecord(dev.b, s);
+        // report: co-rank both ends of every reference worker block with
+        // Algorithm 1 on the device (parallel.hpp:201-207, :273-275)
+        const size_t nq = workers + 1;
+        std::vector<uint64_t> ranks(nq), js(nq);
+        std::vector<uint32_t> its(nq);
+        for (size_t r = 0; r <= workers; ++r) partition_output_impl(total, workers, r, &ranks[r]);
+        const bool want_iters = corank_iterations != nullptr;
+        if (want_iters) {
+            staged dr, dj, dit;
+            if ((rc = dr.in(ranks.data(), nq * 8, s, nullptr))) return rc;
+            if ((rc = dj.out_alloc(js.data(), nq * 8, s))) return rc;
+            if ((rc = dit.out_alloc(its.data(), nq * 4, s))) return rc;
+            if ((rc = co_rank_batch_device<K>(static_cast<const uint64_t*>(dr.dev), nq,
+                                              static_cast<const K*>(da.dev), m,
+                                              static_cast<const K*>(db.dev), n,
+                                              static_cast<uint64_t*>(dj.dev),
+                                              static_cast<uint32_t*>(dit.dev), nullptr, s)))
+                return rc;
+            if ((rc = dit.back(its.data(), nq * 4, nullptr))) return rc;
+        }
+        if ((rc = dout.back(out, total * sizeof(K), &d2h))) return rc;
+        if (HAS_V && (rc = doutv.back(outv, total * 4, &d2h))) return rc;
+        cudaEventRecord(e2e.b, s);
+        const cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return cuda_fail(e, "comerge: merge_parallel");
+        if (block_sizes)
+            for (size_t r = 0; r < workers; ++r) block_sizes[r] = ranks[r + 1] - ranks[r];
+        if (want_iters) {
+            // unsynced: begin/end per worker; synced: begin only (:269-275)
+            for (size_t r = 0; r < workers; ++r) {
+                if (synced) {
+                    corank_iterations[r] = its[r];
+                } else {
+                    corank_iterations[2 * r] = its[r];
+                    corank_iterations[2 * r + 1] = its[r + 1];
+                }
+            }
+        }
+    }
+    if (rep) {
+        rep->m = m;
+        rep->n = n;
+        rep->workers = workers;
+        rep->wall_ns = total ? dev.ns() : 0;
+        rep->e2e_ns = e2e.ns();
+        rep->h2d_bytes = h2d;
+        rep->d2h_bytes = d2h;
+        rep->tiles = div_up(total, tile_cfg<K>::kTile);
+    }
+    return COMERGE_OK;
+}
+
+template <typename K>
+int co_rank_sync(uint64_t target, const K* a, size_t m, const K* b, size_t n, uint64_t* j,
+                 uint64_t* k, uint32_t* iterations, uint32_t* comparisons) {
+    if (m > SIZE_MAX - n)
+        return fail(COMERGE_E_LENGTH, "comerge: combined input length exceeds index range");
+    if (target > m + n)  // corank.hpp:78-79
+        return fail(COMERGE_E_RANGE, "co_rank: rank out of range (exceeds m+n)");
+    if (!j || !k) return fail(COMERGE_E_INVALID, "co_rank: null result pointer");
+    cudaStream_t s = sync_stream();
+    int rc;
+    uint64_t hj = 0;
+    uint32_t hit = 0, hcmp = 0;
+    {
+        staged da, db, dr, dj, dit, dcmp;
+        if ((rc = da.in(a, m * sizeof(K), s, nullptr))) return rc;
+        if ((rc = db.in(b, n * sizeof(K), s, nullptr))) return rc;
+        if ((rc = dr.in(&target, 8, s, nullptr))) return rc;
+        if ((rc = dj.out_alloc(&hj, 8, s))) return rc;
+        if ((rc = dit.out_alloc(&hit, 4, s))) return rc;
+        if ((rc = dcmp.out_alloc(&hcmp, 4, s))) return rc;
+        if ((rc = co_rank_batch_device<K>(
+                 static_cast<const uint64_t*>(dr.dev), 1, static_cast<const K*>(da.dev), m,
+                 static_cast<const K*>(db.dev), n, static_cast<uint64_t*>(dj.dev),
+                 static_cast<uint32_t*>(dit.dev), static_cast<uint32_t*>(dcmp.dev), s)))
+            return rc;
+        if ((rc = dj.back(&hj, 8, nullptr)) || (rc = dit.back(&hit, 4, nullptr)) ||
+            (rc = dcmp.back(&hcmp, 4, nullptr)))
+            return rc;
+        const cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return cuda_fail(e, "comerge: co_rank");
+    }
+    *j = hj;
+    *k = target - hj;
+    if (iterations) *iterations = hit;
+    if (comparisons) *comparisons = hcmp;
+    return COMERGE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* comerge_cuda_last_error(void) { return g_error.c_str(); }
+
+void comerge_cuda_set_kernel_events(void* before, void* after) {
+    g_ev_before = static_cast<cudaEvent_t>(before);
+    g_ev_after = static_cast<cudaEvent_t>(after);
+}
+int comerge_cuda_abi_version(void) { return 10000; }
+
+size_t comerge_cuda_merge_workspace_bytes(size_t m, size_t n, int key_kind, int) {
+    return key_kind == COMERGE_KEY_U64 ? merge_ws_bytes<uint64_t>(m, n)
+                                       : merge_ws_bytes<uint32_t>(m, n);
+}
+size_t comerge_cuda_segmented_workspace_bytes(size_t total, size_t, int key_kind) {
+    return key_kind == COMERGE_KEY_U64 ? seg_ws_bytes<uint64_t>(total)
+                                       : seg_ws_bytes<uint32_t>(total);
+}
+
+#define COMERGE_KEYS(SUF, K)                                                                     \
+    int comerge_cuda_merge_keys_##SUF(const K* a, size_t m, const K* b, size_t n, K* out,       \
+                                      void* ws, size_t ws_bytes, comerge_stream_t stream) {      \
+        return merge_device<K, false>(a, nullptr, m, b, nullptr, n, out, nullptr, ws, ws_bytes,  \
+                                      stream);                                                   \
+    }                                                                                            \
+    int comerge_cuda_merge_pairs_##SUF(const K* ak, const uint32_t* av, size_t m, const K* bk,   \
+                                       const uint32_t* bv, size_t n, K* ok, uint32_t* ov,        \
+                                       void* ws, size_t ws_bytes, comerge_stream_t stream) {     \
+        return merge_device<K, true>(ak, av, m, bk, bv, n, ok, ov, ws, ws_bytes, stream);        \
+    }                                                                                            \
+    int comerge_cuda_co_rank_batch_##SUF(const uint64_t* ranks, size_t count, const K* a,       \
+                                         size_t m, const K* b, size_t n, uint64_t* out_j,        \
+                                         uint32_t* out_it, uint32_t* out_cmp,                    \
+                                         comerge_stream_t stream) {                              \
+        return co_rank_batch_device<K>(ranks, count, a, m, b, n, out_j, out_it, out_cmp,         \
+                                       stream);                                                  \
+    }                                                                                            \
+    int comerge_merge_parallel_##SUF(const K* a, size_t m, const K* b, size_t n, K* out,        \
+                                     size_t out_len, size_t workers, int synced,                 \
+                                     comerge_merge_report* report, uint64_t* block_sizes,        \
+                                     uint32_t* corank_iterations) {                              \
+        return merge_parallel_sync<K, false>(a, nullptr, m, b, nullptr, n, out, nullptr,         \
+                                             out_len, workers, synced, report, block_sizes,      \
+                                             corank_iterations);                                 \
+    }                                                                                            \
+    int comerge_merge_parallel_pairs_##SUF(const K* ak, const uint32_t* av, size_t m,            \
+                                           const K* bk, const uint32_t* bv, size_t n, K* ok,     \
+                                           uint32_t* ov, size_t out_len, size_t workers,         \
+                                           comerge_merge_report* report) {                       \
+        return merge_parallel_sync<K, true>(ak, av, m, bk, bv, n, ok, ov, out_len, workers, 0,   \
+                                            report, nullptr, nullptr);                           \
+    }                                                                                            \
+    int comerge_co_rank_##SUF(uint64_t target, const K* a, size_t m, const K* b, size_t n,       \
+                              uint64_t* j, uint64_t* k, uint32_t* iterations,                    \
+                              uint32_t* comparisons) {                                           \
+        return co_rank_sync<K>(target, a, m, b, n, j, k, iterations, comparisons);               \
+    }
+
+COMERGE_KEYS(i32, int32_t)
+COMERGE_KEYS(u32, uint32_t)
+COMERGE_KEYS(u64, uint64_t)
+
+int comerge_cuda_merge_segmented_i32(const int32_t* a, const uint64_t* a_off, size_t m,
+                                     const int32_t* b, const uint64_t* b_off, size_t n,
+                                     size_t nseg, int32_t* out, void* ws, size_t ws_bytes,
+                                     comerge_stream_t stream) {
+    return merge_segmented_device<int32_t>(a, a_off, m, b, b_off, n, nseg, out, ws, ws_bytes,
+                                           stream);
+}
+int comerge_cuda_merge_segmented_u32(const uint32_t* a, const uint64_t* a_off, size_t m,
+                                     const uint32_t* b, const uint64_t* b_off, size_t n,
+                                     size_t nseg, uint32_t* out, void* ws, size_t ws_bytes,
+                                     comerge_stream_t stream) {
+    return merge_segmented_device<uint32_t>(a, a_off, m, b, b_off, n, nseg, out, ws, ws_bytes,
+                                            stream);
+}
+
+int comerge_partition_output(uint64_t total, uint64_t workers, uint64_t r, uint64_t* out) {
+    if (!out) return fail(COMERGE_E_INVALID, "partition_output: null result pointer");
+    return partition_output_impl(total, workers, r, out);
+}
+
+}  // extern "C"

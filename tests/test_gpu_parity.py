@@ -1,0 +1,328 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference.
+
+Every check is bit-exact (integer work):
+  * the reference's KATs (tests/golden/kat.json),
+  * vectors produced by the unmodified reference (tests/golden/ref_vectors.npz),
+  * seeded random sweeps against the C oracle (oracle/comerge_oracle.c) over
+    ragged / empty / tile-boundary / misaligned shapes and duplicate-heavy keys,
+  * the five BASELINE configs at full size: exact comparison with the oracle
+    where the host finishes in seconds, and size-independent properties
+    (sortedness, multiset checksum, tagged stability) everywhere.
+"""
+import numpy as np
+import pytest
+
+from conftest import KEY_DTYPES
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+TDT = {np.dtype(np.int32): torch.int32, np.dtype(np.uint32): torch.uint32,
+       np.dtype(np.uint64): torch.uint64}
+
+
+def dev(x, cuda):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(cuda)
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def P():
+    import paper_1303_4312_b200 as mod
+    return mod
+
+
+def tagged(m, n):
+    return (np.arange(m, dtype=np.uint32),
+            np.arange(n, dtype=np.uint32) | np.uint32(1 << 31))
+
+
+# ------------------------------------------------------------------ KATs
+
+def test_kat_co_rank(cuda, kat):
+    from test_oracle import kinds_for
+    for case in kat["co_rank"]:
+        for k in kinds_for(case["a"] + case["b"]):
+            dt = KEY_DTYPES[k]
+            a, b = dev(np.array(case["a"], dt), cuda), dev(np.array(case["b"], dt), cuda)
+            st = P().CoRankStats()
+            assert list(P().co_rank(case["i"], a, b, st)) == case["expect"], case["src"]
+            if "iterations" in case:
+                assert st.iterations == case["iterations"]
+            if "comparisons" in case:
+                assert st.comparisons == case["comparisons"]
+            if "max_comparisons" in case:
+                assert st.comparisons <= case["max_comparisons"]
+    for case in kat["co_rank_errors"]:
+        a = dev(np.array(case["a"], np.uint64), cuda)
+        b = dev(np.array(case["b"], np.uint64), cuda)
+        with pytest.raises(IndexError, match=case["message"]):
+            P().co_rank(case["i"], a, b)
+
+
+def test_kat_merge(cuda, kat):
+    from test_oracle import kinds_for
+    for case in kat["merge"]:
+        for k in kinds_for(case["a"] + case["b"]):
+            dt = KEY_DTYPES[k]
+            out = P().stable_merge(dev(np.array(case["a"], dt), cuda),
+                                   dev(np.array(case["b"], dt), cuda))
+            torch.cuda.synchronize()
+            assert host(out).tolist() == case["expect"], case["src"]
+    for case in kat["merge_tagged"]:
+        for k in ("i32", "u32", "u64"):
+            dt = KEY_DTYPES[k]
+            av, bv = tagged(len(case["a"]), len(case["b"]))
+            _, vals = P().merge_pairs(dev(np.array(case["a"], dt), cuda), dev(av, cuda),
+                                      dev(np.array(case["b"], dt), cuda), dev(bv, cuda))
+            vals = host(vals)
+            assert [int(v >> 31) for v in vals] == case["expect_origin"], case["src"]
+            assert [int(v & 0x7FFFFFFF) for v in vals] == case["expect_index"], case["src"]
+    for case in kat["merge_errors"]:
+        a = dev(np.array(case["a"], np.uint64), cuda)
+        b = dev(np.array(case["b"], np.uint64), cuda)
+        with pytest.raises(ValueError, match=case["message"]):
+            P().stable_merge(a, b, torch.zeros(case["out_len"], dtype=torch.uint64, device=cuda))
+
+
+def test_kat_plan_and_merge_parallel(cuda, kat):
+    for case in kat["plan"]:
+        a = dev(np.array(case["a"], np.uint64), cuda)
+        b = dev(np.array(case["b"], np.uint64), cuda)
+        got = [list(x.as_tuple()) for x in P().plan(a, b, case["workers"])]
+        assert got == case["expect"], case["src"]
+    for case in kat["merge_parallel"]:
+        a, b = np.array(case["a"], np.uint64), np.array(case["b"], np.uint64)
+        out = np.zeros(len(a) + len(b), np.uint64)
+        rep = P().merge_parallel(a, b, out, case["workers"])
+        assert out.tolist() == case["expect"], case["src"]
+        if "block_sizes" in case:
+            assert rep.block_sizes == case["block_sizes"]
+    for case in kat["merge_parallel_errors"]:
+        a, b = np.array(case["a"], np.uint64), np.array(case["b"], np.uint64)
+        with pytest.raises(ValueError, match=case["message"]):
+            P().merge_parallel(a, b, np.zeros(case["out_len"], np.uint64), case["workers"])
+
+
+# ------------------------------------------------- reference-made vectors
+
+def _cases(golden, prefix):
+    from test_oracle import _cases as c
+    return c(golden, prefix)
+
+
+def test_golden_co_rank_batch_exact_stats(cuda, golden):
+    """Device Algorithm 1 reproduces the reference's j, iterations and comparisons."""
+    for name, c in _cases(golden, "corank"):
+        a, b = dev(c["a"], cuda), dev(c["b"], cuda)
+        ranks = torch.arange(len(c["a"]) + len(c["b"]) + 1, device=cuda).to(torch.uint64)
+        j, it, cmp = P().co_rank_batch(ranks, a, b, with_stats=True)
+        assert np.array_equal(host(j), c["j"]), name
+        assert np.array_equal(host(it), c["it"]), name
+        assert np.array_equal(host(cmp), c["cmp"]), name
+
+
+def test_golden_merges_device_and_host_paths(cuda, golden):
+    for name, c in _cases(golden, "merge"):
+        out = P().stable_merge(dev(c["a"], cuda), dev(c["b"], cuda))
+        torch.cuda.synchronize()
+        assert np.array_equal(host(out), c["out"]), name
+        hout = np.full(len(c["out"]), 0x5A, dtype=c["out"].dtype)  # poisoned output
+        rep = P().merge_parallel(c["a"], c["b"], hout, 7)
+        assert np.array_equal(hout, c["out"]), name
+        assert rep.block_sizes == c["bs7"].tolist(), name
+        assert rep.corank_iterations == c["it7"].tolist(), name
+        rep_s = P().merge_parallel_synced(c["a"], c["b"], hout, 7)
+        assert np.array_equal(hout, c["out"]) and len(rep_s.corank_iterations) == 7
+
+
+def test_golden_key_value(cuda, golden):
+    for name, c in _cases(golden, "kv"):
+        av, bv = tagged(len(c["a"]), len(c["b"]))
+        ok, ov = P().merge_pairs(dev(c["a"], cuda), dev(av, cuda), dev(c["b"], cuda), dev(bv, cuda))
+        torch.cuda.synchronize()
+        assert np.array_equal(host(ok), c["outk"]) and np.array_equal(host(ov), c["outv"]), name
+        hk = np.empty_like(c["outk"])
+        hv = np.empty_like(c["outv"])
+        P().merge_pairs(c["a"], av, c["b"], bv, hk, hv)  # host buffers through the C ABI
+        assert np.array_equal(hk, c["outk"]) and np.array_equal(hv, c["outv"]), name
+
+
+def test_golden_segmented(cuda, golden):
+    for name, c in _cases(golden, "seg"):
+        out = P().merge_segmented(dev(c["a"], cuda), dev(c["aoff"], cuda), dev(c["b"], cuda),
+                                  dev(c["boff"], cuda))
+        torch.cuda.synchronize()
+        assert np.array_equal(host(out), c["out"]), name
+
+
+def test_golden_plan(cuda, golden):
+    for name, c in _cases(golden, "plan"):
+        got = [list(x.as_tuple()) for x in P().plan(dev(c["a"], cuda), dev(c["b"], cuda),
+                                                    len(c["blocks"]))]
+        assert got == c["blocks"].tolist(), name
+
+
+# ------------------------------------------------------ random sweeps
+
+def _draw(rng, dt, size, alphabet):
+    if alphabet == 0:
+        hi = 2**64 if dt == np.uint64 else 2**31
+        v = rng.integers(0, hi, size, dtype=np.uint64 if dt == np.uint64 else np.int64)
+        if dt == np.int32:
+            v = v - 2**30
+    else:
+        v = rng.integers(0, alphabet, size) - (alphabet // 2 if dt == np.int32 else 0)
+    return np.sort(v.astype(dt))
+
+
+TILES = {np.int32: 256 * 15, np.uint32: 256 * 15, np.uint64: 256 * 11}
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.uint32, np.uint64])
+def test_random_sweep_keys_and_pairs(cuda, port, dt):
+    rng = np.random.default_rng(int(np.dtype(dt).itemsize) * 7 + (dt == np.int32))
+    T = TILES[dt]
+    shapes = [(0, 0), (0, 1), (1, 0), (T - 1, 0), (0, T + 1), (T, T), (T - 1, 1), (1, T - 1),
+              (2 * T + 3, 5), (5, 3 * T - 2), (3, 50000), (50000, 3), (70001, 69999)]
+    shapes += [(int(rng.integers(0, 20000)), int(rng.integers(0, 20000))) for _ in range(12)]
+    for idx, (m, n) in enumerate(shapes):
+        alphabet = [0, 1, 2, 16, 1000][idx % 5]
+        a, b = _draw(rng, dt, m, alphabet), _draw(rng, dt, n, alphabet)
+        expect = port.merge(a, b)
+        out = P().stable_merge(dev(a, cuda), dev(b, cuda))
+        torch.cuda.synchronize()
+        assert np.array_equal(host(out), expect), (m, n, alphabet)
+        av, bv = tagged(m, n)
+        ek, ev = port.merge(a, b, av, bv)
+        ok, ov = P().merge_pairs(dev(a, cuda), dev(av, cuda), dev(b, cuda), dev(bv, cuda))
+        torch.cuda.synchronize()
+        assert np.array_equal(host(ok), ek) and np.array_equal(host(ov), ev), (m, n, alphabet)
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.uint64])
+def test_misaligned_views(cuda, port, dt):
+    """Inputs / outputs that are not 16-byte aligned take the scalar edges."""
+    rng = np.random.default_rng(5)
+    for shift_a, shift_b, shift_o in [(1, 0, 0), (0, 3, 1), (2, 1, 3), (3, 3, 2)]:
+        m, n = 9001 + shift_a, 7777 + shift_b
+        a, b = _draw(rng, dt, m, 64), _draw(rng, dt, n, 64)
+        ta = torch.zeros(m + 8, dtype=TDT[np.dtype(dt)], device=cuda)
+        tb = torch.zeros(n + 8, dtype=TDT[np.dtype(dt)], device=cuda)
+        to = torch.zeros(m + n + 8, dtype=TDT[np.dtype(dt)], device=cuda)
+        va, vb = ta[shift_a:shift_a + m], tb[shift_b:shift_b + n]
+        va.copy_(dev(a, cuda))
+        vb.copy_(dev(b, cuda))
+        vo = to[shift_o:shift_o + m + n]
+        P().stable_merge(va, vb, vo)
+        torch.cuda.synchronize()
+        assert np.array_equal(host(vo), port.merge(a, b)), (shift_a, shift_b, shift_o)
+
+
+def test_random_segmented(cuda, port):
+    rng = np.random.default_rng(99)
+    for dt in (np.int32, np.uint32):
+        for nseg, maxlen in [(1, 10000), (3000, 8), (500, 600), (64, 4096)]:
+            ma = rng.integers(0, maxlen + 1, nseg)
+            nb = rng.integers(0, maxlen + 1, nseg)
+            ma[rng.integers(0, nseg, nseg // 4)] = 0
+            a = np.concatenate([_draw(rng, dt, int(x), 100) for x in ma] + [np.empty(0, dt)])
+            b = np.concatenate([_draw(rng, dt, int(x), 100) for x in nb] + [np.empty(0, dt)])
+            ao = np.concatenate([[0], np.cumsum(ma)]).astype(np.uint64)
+            bo = np.concatenate([[0], np.cumsum(nb)]).astype(np.uint64)
+            out = P().merge_segmented(dev(a, cuda), dev(ao, cuda), dev(b, cuda), dev(bo, cuda))
+            torch.cuda.synchronize()
+            assert np.array_equal(host(out), port.merge_segmented(a, ao, b, bo)), (nseg, maxlen)
+
+
+def test_co_rank_split_equals_reference_search(cuda, port):
+    """The partition's one-sided search returns Algorithm 1's split (Lemma 1)."""
+    rng = np.random.default_rng(3)
+    for dt in (np.int32, np.uint64):
+        a, b = _draw(rng, dt, 100000, 7), _draw(rng, dt, 80000, 7)
+        ranks = np.unique(rng.integers(0, 180001, 2000)).astype(np.uint64)
+        j = host(P().co_rank_batch(dev(ranks, cuda), dev(a, cuda), dev(b, cuda)))
+        for i, jj in zip(ranks[:200], j[:200]):
+            assert port.co_rank(int(i), a, b)[0] == int(jj)
+        out = host(P().stable_merge(dev(a, cuda), dev(b, cuda)))
+        assert np.array_equal(out, port.merge(a, b))
+
+
+def test_worker_count_independence(cuda, port):
+    """Acceptance criterion 6 at GPU scale: outputs identical for any p."""
+    rng = np.random.default_rng(2026)
+    a, b = _draw(rng, np.uint64, 300000, 0), _draw(rng, np.uint64, 300000, 0)
+    expect = port.merge(a, b)
+    for p in (1, 2, 4, 8, 33):
+        out = np.zeros(600000, np.uint64)
+        rep = P().merge_parallel(a, b, out, p)
+        assert np.array_equal(out, expect) and len(rep.block_sizes) == p
+        assert max(rep.block_sizes) - min(rep.block_sizes) <= 1
+
+
+# ------------------------------------------------------ generator pin
+
+def test_gpu_generator_matches_reference_recipe(cuda, port, golden):
+    from paper_1303_4312_b200 import testkit as tk
+    for dist, width in ((0, 0), (2, 16)):
+        seed = int(golden[f"gen__{dist}__seed"][0])
+        a = golden[f"gen__{dist}__a"]
+        got = tk.generate_sorted(torch.uint64, seed, 0, len(a), width)
+        assert np.array_equal(host(got), a)
+    for dt, width in ((torch.int32, 2**31), (torch.int32, 16), (torch.uint32, 2**20),
+                      (torch.uint64, 0), (torch.uint64, 3 * 2**62)):
+        for seed, length in ((5, 1), (5, 1000), (77, 123457)):
+            got = tk.generate_sorted(dt, seed, 1, length, width)
+            npdt = {torch.int32: np.int32, torch.uint32: np.uint32, torch.uint64: np.uint64}[dt]
+            assert np.array_equal(host(got), port.generate_sorted(npdt, seed, 1, length, width))
+
+
+# ------------------------------------------- BASELINE configs, full size
+
+def _config_inputs(cfg, cuda):
+    import bench
+    return bench.make_inputs(cfg, seed=5, device=cuda)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C3s", "C4", "C5"])
+def test_baseline_config_full_size(cuda, port, cfg):
+    import bench
+    from paper_1303_4312_b200 import testkit as tk
+    inp = _config_inputs(cfg, cuda)
+    out = bench.run_config(cfg, inp)
+    torch.cuda.synchronize()
+    a, b = inp["a"], inp["b"]
+    total = a.numel() + b.numel()
+    # size-independent properties at full size
+    assert tk.count_unsorted(out["keys"]) == 0
+    assert tk.checksum(out["keys"]) == (tk.checksum(a) + tk.checksum(b)) % 2**64
+    if "vals" in out:
+        assert tk.verify_pairs(a, b, out["keys"], out["vals"]) == [0, 0, 0, 0]
+    # exact comparison with the oracle where the host finishes in seconds
+    if total <= 2**26 + 2**25:
+        ha, hb = host(a), host(b)
+        if cfg == "C5":
+            expect = port.merge_segmented(ha, host(inp["a_off"]), hb, host(inp["b_off"]),
+                                          threads=8)
+            assert np.array_equal(host(out["keys"]), expect)
+        elif "vals" in out:
+            ek, ev, _, _ = port.merge_parallel(ha, hb, 64, host(inp["av"]), host(inp["bv"]),
+                                               threads=8)
+            assert np.array_equal(host(out["keys"]), ek) and np.array_equal(host(out["vals"]), ev)
+        else:
+            ek, _, _, _ = port.merge_parallel(ha, hb, 64, threads=8)
+            assert np.array_equal(host(out["keys"]), ek)
+    else:
+        # spot-check tile boundaries of the huge configs against Algorithm 1
+        ha, hb = host(a), host(b)
+        rng = np.random.default_rng(1)
+        hk = out["keys"]
+        for i in rng.integers(0, total + 1, 16):
+            j, k = port.co_rank(int(i), ha, hb)
+            lo = max(0, int(i) - 64)
+            window = host(hk[lo:int(i)])
+            pref = np.sort(np.concatenate([ha[max(0, j - 64):j], hb[max(0, k - 64):k]]))
+            assert np.array_equal(window, pref[len(pref) - len(window):])
