@@ -296,8 +296,9 @@ def test_baseline_config_full_size(cuda, port, cfg):
     torch.cuda.synchronize()
     a, b = inp["a"], inp["b"]
     total = a.numel() + b.numel()
-    # size-independent properties at full size
-    assert tk.count_unsorted(out["keys"]) == 0
+    # size-independent properties at full size (C5 is sorted per pair only)
+    if cfg != "C5":
+        assert tk.count_unsorted(out["keys"]) == 0
     assert tk.checksum(out["keys"]) == (tk.checksum(a) + tk.checksum(b)) % 2**64
     if "vals" in out:
         assert tk.verify_pairs(a, b, out["keys"], out["vals"]) == [0, 0, 0, 0]
