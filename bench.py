@@ -120,8 +120,12 @@ def run_config(cfg, inp, out=None):
     return out
 
 
-def launches_per_step(cfg):
-    return 2  # partition kernel + merge kernel
+KERNEL_NAMES = {1: "merge_tile_kernel (+ partition_kernel)", 2: "merge_stream_kernel",
+                3: "seg_merge_tile_kernel (+ seg_partition_kernel)"}
+
+
+def launches_per_step(path):
+    return 1 if path == 2 else 2  # streaming: one launch; tile paths: partition + merge
 
 
 # ------------------------------------------------------------------ clocks
@@ -237,9 +241,10 @@ def time_config(cfg, steps, warmup, device, seed=SEED, dist_ctx=None, clocks=Fal
         dist_ctx.barrier()
     if sampler:
         sampler.__exit__()
+    path = N.lib.comerge_cuda_last_path()
     step_ms = [e[0].elapsed_time(e[1]) for e in ev]
     kern_ms = [e[2].elapsed_time(e[3]) for e in ev]
-    res = dict(total=total, step_ms=step_ms, kern_ms=kern_ms,
+    res = dict(total=total, step_ms=step_ms, kern_ms=kern_ms, path=path,
                clocks=sampler.summary() if sampler else None, inp=inp, out=out)
     return res
 
@@ -259,7 +264,8 @@ def summarize(cfg, res, peak, n_gpus=1, max_step_total_ms=None):
         merge_kernel_ms=kern, merge_kernel_gbs=balg / (kern * 1e-3) / 1e9,
         frac_of_peak=balg / (kern * 1e-3) / 1e9 / peak,
         step_frac_of_peak=balg / (ms_step * 1e-3) / 1e9 / peak,
-        frac_of_8tbs=balg / (kern * 1e-3) / 8e12, algorithmic_bytes=balg)
+        frac_of_8tbs=balg / (kern * 1e-3) / 8e12, algorithmic_bytes=balg,
+        kernel=KERNEL_NAMES.get(res["path"], "?"), launches_per_step=launches_per_step(res["path"]))
 
 
 # ------------------------------------------------------------- CPU legs
@@ -493,11 +499,11 @@ def main():
                         l2="flushed between steps (512 MiB write, outside the events)"),
             roofline=dict(bound="hbm", achieved=head["merge_kernel_gbs"], peak=peak,
                           unit="GB/s", frac=head["frac_of_peak"], traffic=traffic_for(cfg),
-                          kernel="merge_tile_kernel", peak_source=peak_src,
+                          kernel=head["kernel"], peak_source=peak_src,
                           algorithmic_bytes_per_launch=head["algorithmic_bytes"],
                           step_gbs=head["step_gbs"], frac_of_8tbs=head["frac_of_8tbs"]),
             cpu_baseline=cpu, e2e=e2e, clocks=res["clocks"],
-            gpu_launches=args.steps * launches_per_step(cfg),
+            gpu_launches=args.steps * head["launches_per_step"],
             configs=per_config)
         print(json.dumps(line), flush=True)
     if dist:

@@ -61,6 +61,16 @@ int comerge_cuda_abi_version(void);
  * arguments are cudaEvent_t handles. */
 void comerge_cuda_set_kernel_events(void* before, void* after);
 
+/* Kernel selection on the calling thread (testing / benchmarking both
+ * device paths): 0 = automatic (default), 1 = tile kernel (partition +
+ * one CTA per tile, handles any alignment), 2 = persistent streaming kernel
+ * whenever all buffers are 16-byte aligned. */
+void comerge_cuda_set_path(int path);
+/* Kernel family used by the last merge on this thread: 1 = tile kernel
+ * (partition + merge launches), 2 = streaming kernel (one launch),
+ * 3 = segmented tile kernel (partition + merge launches), 0 = none yet. */
+int comerge_cuda_last_path(void);
+
 /* ------------------------------------------------------------ workspace */
 
 /* Bytes of scratch the merge entry points need for (m, n): the tile

@@ -62,6 +62,9 @@ def _load():
             _p, _p, _sz, _p, _p, _sz, _sz, _p, _p, _sz, _p]
     lib.comerge_cuda_set_kernel_events.argtypes = [_p, _p]
     lib.comerge_cuda_set_kernel_events.restype = None
+    lib.comerge_cuda_set_path.argtypes = [_i]
+    lib.comerge_cuda_set_path.restype = None
+    lib.comerge_cuda_last_path.restype = _i
     lib.comerge_testkit_generate_raw.argtypes = [_u64, _u64, _sz, _u64, _p, _p]
     lib.comerge_testkit_generate_runs.argtypes = [_i, _u64, _u64, _p, _sz, _sz, _u64, _p, _p]
     lib.comerge_partition_output.argtypes = [_u64, _u64, _u64, C.POINTER(_u64)]

@@ -148,6 +148,16 @@ def co_rank_batch(ranks, a, b, with_stats: bool = False):
 
 # ------------------------------------------------------------------- merges
 
+KERNEL_PATHS = {"auto": 0, "tile": 1, "stream": 2}
+
+
+def set_kernel_path(path: str = "auto") -> None:
+    """Select the device kernel for merges issued from this thread: "auto",
+    "tile" (partition + one CTA per tile; any alignment) or "stream" (the
+    persistent TMA streaming kernel whenever buffers are 16-byte aligned)."""
+    N.lib.comerge_cuda_set_path(KERNEL_PATHS[path])
+
+
 def partition_output(total: int, workers: int, r: int) -> int:
     """floor(r * total / workers) without overflow (parallel.hpp:60-67)."""
     if workers < 0 or r < 0:

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../../include/comerge_cuda.h"
+#include "merge_stream.cuh"
 #include "merge_tile.cuh"
 
 using namespace comerge_b200;
@@ -19,6 +20,37 @@ namespace {
 
 thread_local std::string g_error;
 thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;
+thread_local int g_path = 0;  // 0 auto, 1 tile kernel (v1), 2 streaming kernel (v2)
+thread_local int g_last_path = 0;  // kernel family of the last merge: 1, 2, 3 = segmented
+
+int sm_count() {
+    static const int n = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v > 0 ? v : 148;
+    }();
+    return n;
+}
+
+// Persistent grid size for the streaming kernel (resident CTAs, cached).
+template <typename K, bool HAS_V>
+int stream_grid_limit() {
+    static const int limit = [] {
+        using L = stream_layout<K, HAS_V>;
+        auto kern = merge_stream_kernel<K, HAS_V>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::kSmem));
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::kThreads,
+                                                          L::kSmem) != cudaSuccess ||
+            per_sm < 1) {
+            cudaGetLastError();
+            per_sm = 1;
+        }
+        return per_sm * sm_count();
+    }();
+    return limit;
+}
 
 void mark_before(cudaStream_t s) {
     if (g_ev_before) cudaEventRecord(g_ev_before, s);
@@ -130,6 +162,22 @@ int merge_device(const K* a, const uint32_t* av, size_t m, const K* b, const uin
     if (int rc = check_merge_args<K>(who, a, m, b, n, out, av, bv, outv, HAS_V)) return rc;
     const uint64_t total = uint64_t(m) + n;
     if (total == 0) return COMERGE_OK;
+    // v2: persistent streaming kernel (TMA rings) when every buffer is
+    // 16-byte aligned and there is more than one tile per resident CTA slot.
+    using SL = stream_layout<K, HAS_V>;
+    const bool aligned_all = aligned16(a) && aligned16(b) && aligned16(out) &&
+                             (!HAS_V || (aligned16(av) && aligned16(bv) && aligned16(outv)));
+    const uint64_t stiles = div_up(total, SL::T);
+    if (g_path != 1 && aligned_all && (g_path == 2 || stiles >= 64)) {
+        const int limit = stream_grid_limit<K, HAS_V>();
+        const unsigned grid = unsigned(stiles < uint64_t(limit) ? stiles : uint64_t(limit));
+        stream_args args{a, av, m, b, bv, n, out, outv, stiles};
+        g_last_path = 2;
+        mark_before(s);
+        merge_stream_kernel<K, HAS_V><<<grid, SL::kThreads, SL::kSmem, s>>>(args);
+        mark_after(s);
+        return check_launch("comerge: streaming merge launch");
+    }
     constexpr int T = tile_cfg<K>::kTile;
     const uint64_t ntiles = div_up(total, T);
     const uint64_t nbound = ntiles + 1;
@@ -145,6 +193,7 @@ int merge_device(const K* a, const uint32_t* av, size_t m, const K* b, const uin
     flags |= aligned16(av) ? kAVAligned : 0;
     flags |= aligned16(bv) ? kBVAligned : 0;
     flags |= aligned16(outv) ? kOutVAligned : 0;
+    g_last_path = 1;
     mark_before(s);
     merge_tile_kernel<K, HAS_V><<<unsigned(ntiles), tile_cfg<K>::kThreads, 0, s>>>(
         a, av, m, b, bv, n, out, outv, bj, flags);
@@ -180,6 +229,7 @@ int merge_segmented_device(const K* a, const uint64_t* a_off, size_t m, const K*
     flags |= aligned16(a) ? kAAligned : 0;
     flags |= aligned16(b) ? kBAligned : 0;
     flags |= aligned16(out) ? kOutAligned : 0;
+    g_last_path = 3;
     mark_before(s);
     seg_merge_tile_kernel<K><<<unsigned(ntiles), seg_cfg<K>::kThreads, 0, s>>>(
         a, a_off, m, b, b_off, n, out, bj, bseg, flags);
@@ -428,6 +478,9 @@ int co_rank_sync(uint64_t target, const K* a, size_t m, const K* b, size_t n, ui
 extern "C" {
 
 const char* comerge_cuda_last_error(void) { return g_error.c_str(); }
+
+void comerge_cuda_set_path(int path) { g_path = path; }
+int comerge_cuda_last_path(void) { return g_last_path; }
 
 void comerge_cuda_set_kernel_events(void* before, void* after) {
     g_ev_before = static_cast<cudaEvent_t>(before);

@@ -35,6 +35,14 @@ def P():
     return mod
 
 
+@pytest.fixture(params=["tile", "stream"])
+def path(request):
+    """Run a test through each device kernel (v1 tile, v2 streaming)."""
+    P().set_kernel_path(request.param)
+    yield request.param
+    P().set_kernel_path("auto")
+
+
 def tagged(m, n):
     return (np.arange(m, dtype=np.uint32),
             np.arange(n, dtype=np.uint32) | np.uint32(1 << 31))
@@ -125,7 +133,7 @@ def test_golden_co_rank_batch_exact_stats(cuda, golden):
         assert np.array_equal(host(cmp), c["cmp"]), name
 
 
-def test_golden_merges_device_and_host_paths(cuda, golden):
+def test_golden_merges_device_and_host_paths(cuda, path, golden):
     for name, c in _cases(golden, "merge"):
         out = P().stable_merge(dev(c["a"], cuda), dev(c["b"], cuda))
         torch.cuda.synchronize()
@@ -139,7 +147,7 @@ def test_golden_merges_device_and_host_paths(cuda, golden):
         assert np.array_equal(hout, c["out"]) and len(rep_s.corank_iterations) == 7
 
 
-def test_golden_key_value(cuda, golden):
+def test_golden_key_value(cuda, path, golden):
     for name, c in _cases(golden, "kv"):
         av, bv = tagged(len(c["a"]), len(c["b"]))
         ok, ov = P().merge_pairs(dev(c["a"], cuda), dev(av, cuda), dev(c["b"], cuda), dev(bv, cuda))
@@ -183,7 +191,7 @@ TILES = {np.int32: 256 * 15, np.uint32: 256 * 15, np.uint64: 256 * 11}
 
 
 @pytest.mark.parametrize("dt", [np.int32, np.uint32, np.uint64])
-def test_random_sweep_keys_and_pairs(cuda, port, dt):
+def test_random_sweep_keys_and_pairs(cuda, path, port, dt):
     rng = np.random.default_rng(int(np.dtype(dt).itemsize) * 7 + (dt == np.int32))
     T = TILES[dt]
     shapes = [(0, 0), (0, 1), (1, 0), (T - 1, 0), (0, T + 1), (T, T), (T - 1, 1), (1, T - 1),
@@ -204,7 +212,7 @@ def test_random_sweep_keys_and_pairs(cuda, port, dt):
 
 
 @pytest.mark.parametrize("dt", [np.int32, np.uint64])
-def test_misaligned_views(cuda, port, dt):
+def test_misaligned_views(cuda, path, port, dt):
     """Inputs / outputs that are not 16-byte aligned take the scalar edges."""
     rng = np.random.default_rng(5)
     for shift_a, shift_b, shift_o in [(1, 0, 0), (0, 3, 1), (2, 1, 3), (3, 3, 2)]:
@@ -238,7 +246,7 @@ def test_random_segmented(cuda, port):
             assert np.array_equal(host(out), port.merge_segmented(a, ao, b, bo)), (nseg, maxlen)
 
 
-def test_co_rank_split_equals_reference_search(cuda, port):
+def test_co_rank_split_equals_reference_search(cuda, path, port):
     """The partition's one-sided search returns Algorithm 1's split (Lemma 1)."""
     rng = np.random.default_rng(3)
     for dt in (np.int32, np.uint64):
@@ -251,7 +259,7 @@ def test_co_rank_split_equals_reference_search(cuda, port):
         assert np.array_equal(out, port.merge(a, b))
 
 
-def test_worker_count_independence(cuda, port):
+def test_worker_count_independence(cuda, path, port):
     """Acceptance criterion 6 at GPU scale: outputs identical for any p."""
     rng = np.random.default_rng(2026)
     a, b = _draw(rng, np.uint64, 300000, 0), _draw(rng, np.uint64, 300000, 0)
@@ -289,6 +297,7 @@ def _config_inputs(cfg, cuda):
 
 @pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C3s", "C4", "C5"])
 def test_baseline_config_full_size(cuda, port, cfg):
+    P().set_kernel_path("auto")
     import bench
     from paper_1303_4312_b200 import testkit as tk
     inp = _config_inputs(cfg, cuda)
