@@ -121,11 +121,11 @@ def run_config(cfg, inp, out=None):
 
 
 KERNEL_NAMES = {1: "merge_tile_kernel (+ partition_kernel)", 2: "merge_stream_kernel",
-                3: "seg_merge_tile_kernel (+ seg_partition_kernel)"}
+                3: "merge_pipe_kernel", 4: "seg_merge_tile_kernel (+ seg_partition_kernel)"}
 
 
 def launches_per_step(path):
-    return 1 if path == 2 else 2  # streaming: one launch; tile paths: partition + merge
+    return 1 if path in (2, 3) else 2  # persistent kernels: one launch; tile paths: two
 
 
 # ------------------------------------------------------------------ clocks

@@ -61,15 +61,27 @@ int comerge_cuda_abi_version(void);
  * arguments are cudaEvent_t handles. */
 void comerge_cuda_set_kernel_events(void* before, void* after);
 
-/* Kernel selection on the calling thread (testing / benchmarking both
- * device paths): 0 = automatic (default), 1 = tile kernel (partition +
- * one CTA per tile, handles any alignment), 2 = persistent streaming kernel
- * whenever all buffers are 16-byte aligned. */
+/* Kernel selection on the calling thread (testing / benchmarking every
+ * device path): 0 = automatic (default: 3 when all buffers are 16-byte
+ * aligned and there are >= 16 tiles, else 1), 1 = tile kernel (partition +
+ * one CTA per tile, any alignment), 2 = ring-streaming kernel, 3 = persistent
+ * tile-pipeline kernel (2 and 3 need 16-byte aligned buffers, else 1 runs). */
 void comerge_cuda_set_path(int path);
-/* Kernel family used by the last merge on this thread: 1 = tile kernel
- * (partition + merge launches), 2 = streaming kernel (one launch),
- * 3 = segmented tile kernel (partition + merge launches), 0 = none yet. */
+/* Kernel used by the last merge on this thread: 1 = tile kernel (partition
+ * + merge launches), 2 = ring-streaming kernel (one launch), 3 = tile
+ * pipeline (one launch), 4 = segmented tile kernel (partition + merge),
+ * 0 = none yet. */
 int comerge_cuda_last_path(void);
+/* Debug tracing of the persistent kernels: when non-NULL, CTA c writes
+ * %globaltimer stamps (start, block co-ranked, first tile done, end) to
+ * device_buffer[8c .. 8c+3] and its SM id to device_buffer[8c+4].  NULL
+ * disables. */
+void comerge_cuda_set_trace(unsigned long long* device_buffer);
+/* Tuning knobs of the tile pipeline (benchmarking only; 0 = default): the
+ * statically assigned share of tiles in percent (default 100), the minimum
+ * claimed chunk in tiles (default 2) and the claim look-ahead (queued tiles
+ * below which the next chunk is claimed, default 4). */
+void comerge_cuda_set_tuning(int static_pct, int min_chunk, int lookahead);
 
 /* ------------------------------------------------------------ workspace */
 

@@ -65,6 +65,10 @@ def _load():
     lib.comerge_cuda_set_path.argtypes = [_i]
     lib.comerge_cuda_set_path.restype = None
     lib.comerge_cuda_last_path.restype = _i
+    lib.comerge_cuda_set_trace.argtypes = [_p]
+    lib.comerge_cuda_set_trace.restype = None
+    lib.comerge_cuda_set_tuning.argtypes = [_i, _i, _i]
+    lib.comerge_cuda_set_tuning.restype = None
     lib.comerge_testkit_generate_raw.argtypes = [_u64, _u64, _sz, _u64, _p, _p]
     lib.comerge_testkit_generate_runs.argtypes = [_i, _u64, _u64, _p, _sz, _sz, _u64, _p, _p]
     lib.comerge_partition_output.argtypes = [_u64, _u64, _u64, C.POINTER(_u64)]

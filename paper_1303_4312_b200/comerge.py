@@ -148,13 +148,14 @@ def co_rank_batch(ranks, a, b, with_stats: bool = False):
 
 # ------------------------------------------------------------------- merges
 
-KERNEL_PATHS = {"auto": 0, "tile": 1, "stream": 2}
+KERNEL_PATHS = {"auto": 0, "tile": 1, "stream": 2, "pipe": 3}
 
 
 def set_kernel_path(path: str = "auto") -> None:
     """Select the device kernel for merges issued from this thread: "auto",
-    "tile" (partition + one CTA per tile; any alignment) or "stream" (the
-    persistent TMA streaming kernel whenever buffers are 16-byte aligned)."""
+    "tile" (partition + one CTA per tile; any alignment), "stream" (ring
+    streaming kernel) or "pipe" (persistent tile pipeline; the default for
+    aligned buffers).  "stream" / "pipe" need 16-byte aligned buffers."""
     N.lib.comerge_cuda_set_path(KERNEL_PATHS[path])
 
 

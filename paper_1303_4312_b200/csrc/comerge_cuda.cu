@@ -7,10 +7,12 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
 #include "../../include/comerge_cuda.h"
+#include "merge_pipe.cuh"
 #include "merge_stream.cuh"
 #include "merge_tile.cuh"
 
@@ -20,8 +22,11 @@ namespace {
 
 thread_local std::string g_error;
 thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;
-thread_local int g_path = 0;  // 0 auto, 1 tile kernel (v1), 2 streaming kernel (v2)
-thread_local int g_last_path = 0;  // kernel family of the last merge: 1, 2, 3 = segmented
+thread_local int g_path = 0;  // 0 auto, 1 tile (v1), 2 ring streaming (v2), 3 tile pipeline (v3)
+thread_local int g_last_path = 0;
+thread_local unsigned long long* g_trace = nullptr;  // debug: per-CTA timestamps
+thread_local int g_search_mode = 0;                  // tuning knob (ring kernel search)
+thread_local int g_tune_min_chunk = 0, g_tune_lookahead = 0, g_tune_static_pct = 0;  // kernel family of the last merge: 1, 2, 3 = segmented
 
 int sm_count() {
     static const int n = [] {
@@ -31,6 +36,129 @@ int sm_count() {
         return v > 0 ? v : 148;
     }();
     return n;
+}
+
+// Self-calibrating static partition of the tile pipeline.  Every launch
+// reports per CTA {SM id, streaming ns, tiles} into host-mapped pinned memory;
+// the next launch folds the streaming rates into a per-SM speed table
+// (exponential moving average, shared by every kernel instantiation on the
+// device) and gives CTA c a share of the tiles proportional to the speed of
+// the SM it last ran on (placement of a persistent grid is deterministic).
+// The weights are hints only: any weights give a valid partition, so a stale
+// or concurrent update never affects the output.
+struct balance_state {
+    std::mutex mu;
+    double sm_speed[256];
+    uint32_t sm_seen[256];
+    int32_t cta_sm[kMaxPipeGrid];
+    unsigned long long* perf_host = nullptr;  // 4 * kMaxPipeGrid entries (mapped)
+    unsigned long long* perf_dev = nullptr;
+    uint32_t last_grid = 0;
+    balance_state() {
+        for (int i = 0; i < 256; ++i) {
+            sm_speed[i] = 1.0;
+            sm_seen[i] = 0;
+        }
+        for (int c = 0; c < kMaxPipeGrid; ++c) cta_sm[c] = -1;
+    }
+
+    void fold() {  // consume the last report
+        if (!perf_host || last_grid == 0) return;
+        const uint32_t G = last_grid;
+        double rate[kMaxPipeGrid];
+        double sum = 0;
+        uint64_t tiles = 0;
+        for (uint32_t c = 0; c < G; ++c) {
+            const unsigned long long* p = perf_host + 4 * c;
+            if (p[3] != 1 || p[1] == 0 || p[0] >= 256) return;  // incomplete report
+            rate[c] = double(p[2]) / double(p[1]);
+            sum += rate[c];
+            tiles += p[2];
+        }
+        for (uint32_t c = 0; c < G; ++c) cta_sm[c] = int32_t(perf_host[4 * c]);
+        if (tiles >= 16ull * G && sum > 0) {
+            // the per-SM rate is the sum over its CTAs, normalised by the mean SM
+            double sm_rate[256] = {0};
+            uint32_t sm_ctas[256] = {0};
+            for (uint32_t c = 0; c < G; ++c) {
+                sm_rate[cta_sm[c]] += rate[c];
+                sm_ctas[cta_sm[c]]++;
+            }
+            double mean = 0;
+            int nsm = 0;
+            for (int x = 0; x < 256; ++x)
+                if (sm_ctas[x]) {
+                    mean += sm_rate[x];
+                    ++nsm;
+                }
+            mean /= nsm;
+            for (int x = 0; x < 256; ++x)
+                if (sm_ctas[x]) {
+                    double r = sm_rate[x] / mean;
+                    r = r < 0.5 ? 0.5 : (r > 2.0 ? 2.0 : r);
+                    sm_speed[x] = sm_seen[x] ? 0.5 * sm_speed[x] + 0.5 * r : r;
+                    sm_seen[x]++;
+                }
+        }
+        std::memset(perf_host, 0, 4 * kMaxPipeGrid * sizeof(unsigned long long));
+    }
+
+    void prepare(pipe_args& args, uint32_t G, uint64_t ntiles) {
+        args.nweights = 0;
+        args.perf = nullptr;
+        if (G > uint32_t(kMaxPipeGrid)) return;
+        std::lock_guard<std::mutex> lock(mu);
+        if (!perf_host) {
+            void* h = nullptr;
+            if (cudaHostAlloc(&h, 4 * kMaxPipeGrid * sizeof(unsigned long long),
+                              cudaHostAllocMapped) != cudaSuccess) {
+                cudaGetLastError();
+                return;
+            }
+            perf_host = static_cast<unsigned long long*>(h);
+            std::memset(perf_host, 0, 4 * kMaxPipeGrid * sizeof(unsigned long long));
+            void* d = nullptr;
+            if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) {
+                cudaGetLastError();
+                return;
+            }
+            perf_dev = static_cast<unsigned long long*>(d);
+        }
+        fold();
+        if (ntiles < 8ull * G) return;  // small merges: uniform split, no report
+        for (uint32_t c = 0; c < G; ++c) {
+            const double w = cta_sm[c] >= 0 ? sm_speed[cta_sm[c]] : 1.0;
+            const double q = w * 1024.0;
+            args.weights[c] = uint16_t(q < 256 ? 256 : (q > 4096 ? 4096 : q + 0.5));
+        }
+        args.nweights = G;
+        args.perf = perf_dev;
+        last_grid = G;
+    }
+};
+
+balance_state& balance() {
+    static balance_state st;  // per process (one device in practice)
+    return st;
+}
+
+// Persistent grid size for the tile-pipeline kernel (resident CTAs, cached).
+template <typename K, bool HAS_V>
+int pipe_grid_limit() {
+    static const int limit = [] {
+        using L = pipe_layout<K, HAS_V>;
+        auto kern = merge_pipe_kernel<K, HAS_V>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::kSmem));
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::kThreads,
+                                                          L::kSmem) != cudaSuccess ||
+            per_sm < 1) {
+            cudaGetLastError();
+            per_sm = 1;
+        }
+        return per_sm * sm_count();
+    }();
+    return limit;
 }
 
 // Persistent grid size for the streaming kernel (resident CTAs, cached).
@@ -83,7 +211,38 @@ constexpr uint64_t kMaxTotal = uint64_t(1) << 40;  // tile ids fit a 1-D grid
 uint64_t div_up(uint64_t x, uint64_t y) { return (x + y - 1) / y; }
 size_t round256(size_t x) { return (x + 255) / 256 * 256; }
 
-// Stream-ordered scratch: caller workspace, or cudaMallocAsync when ws == NULL.
+// Library-private stream-ordered pool (one per device) that keeps its memory
+// across synchronisations, so per-call scratch costs no OS mapping.
+cudaMemPool_t private_pool() {
+    static cudaMemPool_t pools[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return nullptr;
+    static std::once_flag once[64];
+    std::call_once(once[dev], [dev] {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t p = nullptr;
+        if (cudaMemPoolCreate(&p, &props) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+            pools[dev] = p;
+        } else {
+            cudaGetLastError();
+        }
+    });
+    return pools[dev];
+}
+
+cudaError_t pool_alloc(void** ptr, size_t bytes, cudaStream_t s) {
+    cudaMemPool_t p = private_pool();
+    return p ? cudaMallocFromPoolAsync(ptr, bytes, p, s) : cudaMallocAsync(ptr, bytes, s);
+}
+
+// Stream-ordered scratch: caller workspace, or the private pool when ws == NULL.
 struct scratch {
     void* ptr = nullptr;
     bool owned = false;
@@ -98,7 +257,7 @@ struct scratch {
             ptr = ws;
             return COMERGE_OK;
         }
-        const cudaError_t e = cudaMallocAsync(&ptr, need, s);
+        const cudaError_t e = pool_alloc(&ptr, need, s);
         if (e != cudaSuccess) return cuda_fail(e, "comerge: workspace allocation");
         owned = true;
         return COMERGE_OK;
@@ -118,7 +277,9 @@ size_t merge_ws_bytes(size_t m, size_t n) {
     if (m > SIZE_MAX - n) return 0;
     const uint64_t total = m + n;
     if (total == 0) return 0;
-    return round256((div_up(total, tile_cfg<K>::kTile) + 1) * sizeof(uint64_t));
+    // tile kernel: one co-rank per tile boundary; pipeline: a claim counter
+    const size_t tile_ws = round256((div_up(total, tile_cfg<K>::kTile) + 1) * sizeof(uint64_t));
+    return tile_ws > 256 ? tile_ws : 256;
 }
 
 template <typename K>
@@ -168,10 +329,47 @@ int merge_device(const K* a, const uint32_t* av, size_t m, const K* b, const uin
     const bool aligned_all = aligned16(a) && aligned16(b) && aligned16(out) &&
                              (!HAS_V || (aligned16(av) && aligned16(bv) && aligned16(outv)));
     const uint64_t stiles = div_up(total, SL::T);
-    if (g_path != 1 && aligned_all && (g_path == 2 || stiles >= 64)) {
+    using PL = pipe_layout<K, HAS_V>;
+    const uint64_t ptiles = div_up(total, PL::T);
+    if (aligned_all && (g_path == 3 || (g_path == 0 && ptiles >= 16))) {
+        int limit = pipe_grid_limit<K, HAS_V>();
+        if (limit > kMaxPipeGrid) limit = kMaxPipeGrid;
+        const uint32_t grid = uint32_t(ptiles < uint64_t(limit) ? ptiles : uint64_t(limit));
+        pipe_args args{};
+        // static share of the tiles (default all); a dynamic tail needs a
+        // zeroed claim counter from the workspace
+        const uint64_t static_pct = g_tune_static_pct > 0 ? uint64_t(g_tune_static_pct) : 100;
+        args.static_tiles = ptiles * (static_pct > 100 ? 100 : static_pct) / 100;
+        scratch sc;
+        if (args.static_tiles < ptiles) {
+            if (int rc = sc.acquire(ws, ws_bytes, 256, s)) return rc;
+            const cudaError_t e = cudaMemsetAsync(sc.ptr, 0, sizeof(unsigned int), s);
+            if (e != cudaSuccess) return cuda_fail(e, "comerge: work counter reset");
+        }
+        args.a = a;
+        args.av = av;
+        args.m = m;
+        args.b = b;
+        args.bv = bv;
+        args.n = n;
+        args.out = out;
+        args.outv = outv;
+        args.ntiles = ptiles;
+        args.work = static_cast<unsigned int*>(sc.ptr);
+        args.trace = g_trace;
+        args.min_chunk = g_tune_min_chunk > 0 ? uint32_t(g_tune_min_chunk) : 2u;
+        args.lookahead = g_tune_lookahead > 0 ? uint32_t(g_tune_lookahead) : 4u;
+        balance().prepare(args, grid, ptiles);
+        g_last_path = 3;
+        mark_before(s);
+        merge_pipe_kernel<K, HAS_V><<<grid, PL::kThreads, PL::kSmem, s>>>(args);
+        mark_after(s);
+        return check_launch("comerge: pipeline merge launch");
+    }
+    if (aligned_all && g_path == 2) {
         const int limit = stream_grid_limit<K, HAS_V>();
         const unsigned grid = unsigned(stiles < uint64_t(limit) ? stiles : uint64_t(limit));
-        stream_args args{a, av, m, b, bv, n, out, outv, stiles};
+        stream_args args{a, av, m, b, bv, n, out, outv, stiles, g_trace, 0};
         g_last_path = 2;
         mark_before(s);
         merge_stream_kernel<K, HAS_V><<<grid, SL::kThreads, SL::kSmem, s>>>(args);
@@ -229,7 +427,7 @@ int merge_segmented_device(const K* a, const uint64_t* a_off, size_t m, const K*
     flags |= aligned16(a) ? kAAligned : 0;
     flags |= aligned16(b) ? kBAligned : 0;
     flags |= aligned16(out) ? kOutAligned : 0;
-    g_last_path = 3;
+    g_last_path = 4;
     mark_before(s);
     seg_merge_tile_kernel<K><<<unsigned(ntiles), seg_cfg<K>::kThreads, 0, s>>>(
         a, a_off, m, b, b_off, n, out, bj, bseg, flags);
@@ -284,7 +482,7 @@ struct staged {
             dev = const_cast<void*>(src);
             return COMERGE_OK;
         }
-        cudaError_t e = cudaMallocAsync(&dev, bytes, st);
+        cudaError_t e = pool_alloc(&dev, bytes, st);
         if (e != cudaSuccess) return cuda_fail(e, "comerge: device staging allocation");
         owned = true;
         e = cudaMemcpyAsync(dev, src, bytes, cudaMemcpyHostToDevice, st);
@@ -299,7 +497,7 @@ struct staged {
             dev = dst;
             return COMERGE_OK;
         }
-        const cudaError_t e = cudaMallocAsync(&dev, bytes, st);
+        const cudaError_t e = pool_alloc(&dev, bytes, st);
         if (e != cudaSuccess) return cuda_fail(e, "comerge: device staging allocation");
         owned = true;
         return COMERGE_OK;
@@ -481,6 +679,12 @@ const char* comerge_cuda_last_error(void) { return g_error.c_str(); }
 
 void comerge_cuda_set_path(int path) { g_path = path; }
 int comerge_cuda_last_path(void) { return g_last_path; }
+void comerge_cuda_set_trace(unsigned long long* device_buffer) { g_trace = device_buffer; }
+void comerge_cuda_set_tuning(int static_pct, int min_chunk, int lookahead) {
+    g_tune_static_pct = static_pct;
+    g_tune_min_chunk = min_chunk;
+    g_tune_lookahead = lookahead;
+}
 
 void comerge_cuda_set_kernel_events(void* before, void* after) {
     g_ev_before = static_cast<cudaEvent_t>(before);

@@ -1,0 +1,527 @@
+// merge_pipe.cuh -- persistent, self-scheduling tile pipeline for sm_100a
+// (the default merge path).
+//
+// Algorithm 2 of arXiv 1303.4312 (reference
+// parallel.hpp:180-282) mapped onto a persistent grid:
+//
+//   * Work unit = an output tile of T = 256*VT elements.  Tiles are grouped in
+//     contiguous chunks; a chunk is what a reference worker does
+//     (parallel.hpp:201-207): co-rank its start and end, then merge.
+//     B200 SMs do not stream at equal rates (measured: ~25% spread between
+//     GPCs) and CTA->SM placement of a persistent grid is deterministic, so
+//     CTA c takes a contiguous static range of tiles proportional to a weight
+//     learned from the per-CTA throughput of earlier launches (reported through
+//     host-mapped memory); an optional dynamic tail is handed out by guided
+//     self-scheduling (chunks of max(MIN, remaining / (2*grid)) tiles claimed
+//     from one global atomic counter).
+//   * Scheduler warp: claims a chunk only when fewer than LOOKAHEAD tiles are
+//     queued, co-ranks its start (one 33-ary warp search over the whole
+//     diagonal) and then every later boundary of the chunk -- its end included
+//     -- bracketed by its predecessor (lane-group searches, 1, 4, 8, then 32
+//     boundaries per pass), and pushes tile descriptors (i0, j0, j1, i1) into a
+//     shared-memory ring.
+//   * Producer warp: per descriptor, waits for a free stage and TMA-loads
+//     exactly the tile's A window [j0, j1) and B window [i0-j0, i1-j1) (16-byte
+//     aligned supersets, payloads too): every input byte crosses HBM once.
+//   * Consumers (8 warps): tile-local co-rank per VT-slot diagonal and the
+//     branch-free serial merge (merge.hpp:22-31, ties to A) of merge_tile.cuh;
+//     the merged tile is written back into the stage and stored with one TMA
+//     bulk store, then the stage is released.
+#pragma once
+
+#include <cstdint>
+
+#include "corank.cuh"
+#include "merge_stream.cuh"
+#include "merge_tile.cuh"
+
+namespace comerge_b200 {
+
+template <typename K, bool HAS_V>
+struct pipe_cfg;
+// 32-bit keys only: tile 3840, 6 stages of ~15.5 KB.
+template <>
+struct pipe_cfg<int32_t, false> {
+    static constexpr int VT = 15, NST = 6;
+};
+template <>
+struct pipe_cfg<uint32_t, false> : pipe_cfg<int32_t, false> {};
+// 32-bit keys + payload: tile 3840, 3 stages of ~31 KB.
+template <>
+struct pipe_cfg<int32_t, true> {
+    static constexpr int VT = 15, NST = 3;
+};
+template <>
+struct pipe_cfg<uint32_t, true> : pipe_cfg<int32_t, true> {};
+// 64-bit keys only: tile 2816, 4 stages of ~23 KB.
+template <>
+struct pipe_cfg<uint64_t, false> {
+    static constexpr int VT = 11, NST = 4;
+};
+// 64-bit keys + payload: tile 2816, 3 stages of ~34 KB.
+template <>
+struct pipe_cfg<uint64_t, true> {
+    static constexpr int VT = 11, NST = 3;
+};
+
+template <typename K, bool HAS_V>
+struct pipe_layout {
+    using C = pipe_cfg<K, HAS_V>;
+    static constexpr int kConsumers = 256;
+    static constexpr int kThreads = kConsumers + 64;  // + producer warp + scheduler warp
+    static constexpr int VT = C::VT;
+    static constexpr int T = kConsumers * VT;
+    static constexpr int NST = C::NST;
+    static constexpr int VECE = 16 / sizeof(K);
+    static constexpr int NB = 64;  // tile-descriptor ring entries
+    static_assert((T * sizeof(K)) % 16 == 0 && T % 4 == 0, "tile must be 16B multiple");
+    static constexpr int KW = ((T + 4 * VECE + VT + 2) + VECE - 1) / VECE * VECE;
+    static constexpr int VW = HAS_V ? ((T + 16 + VT + 2) + 3) / 4 * 4 : 0;
+    static constexpr size_t kStageKeys = (size_t(KW) * sizeof(K) + 127) / 128 * 128;
+    static constexpr size_t kStageVals = (size_t(VW) * 4 + 127) / 128 * 128;
+    static constexpr size_t kStage = kStageKeys + kStageVals;
+    static constexpr size_t oStages = 0;
+    static constexpr size_t oBars = oStages + NST * kStage;
+    static constexpr size_t oMeta = oBars + size_t(2 * NST) * 8;  // NST x 4 x u64
+    static constexpr size_t oDesc = oMeta + size_t(NST) * 32;      // NB x {i0, j0, j1, i1}
+    static constexpr size_t oScratch = oDesc + size_t(NB) * 32;    // 40 x u64
+    static constexpr size_t oMisc = oScratch + 40 * 8;
+    static constexpr size_t kMisc = 64;
+    static constexpr size_t kSmem = oMisc + kMisc;
+};
+
+constexpr int kMaxPipeGrid = 512;
+
+struct pipe_args {
+    const void* a;
+    const uint32_t* av;
+    uint64_t m;
+    const void* b;
+    const uint32_t* bv;
+    uint64_t n;
+    void* out;
+    uint32_t* outv;
+    uint64_t ntiles;
+    unsigned int* work;          // chunk-claim counter, zero at launch
+    unsigned long long* trace;   // optional per-CTA timestamps (8 x u64 per CTA)
+    uint64_t static_tiles;       // tiles [0, static_tiles) are split statically by weight
+    uint32_t min_chunk;          // smallest dynamically claimed chunk (tiles)
+    uint32_t lookahead;          // claim when fewer tiles than this are queued
+    unsigned long long* perf;    // optional: per-CTA {smid, stream ns, tiles, 1} at exit (host-mapped)
+    uint32_t nweights;           // == gridDim.x when weights are given, else 0 (uniform)
+    uint16_t weights[kMaxPipeGrid];  // per-CTA share of the static tiles
+};
+
+// Lane-group (P+1)-ary search: the warp is split into 32/P groups of P lanes
+// (P a power of two); every group searches its own diagonal i for the
+// Lemma-1 split inside its bracket [lo, hi] (guard 1 of corank.hpp:93-94 is
+// the monotone predicate).  All 32 lanes must call it.
+template <typename K>
+__device__ __forceinline__ uint64_t group_search(uint64_t i, uint64_t lo, uint64_t hi, int P,
+                                                 const K* __restrict__ a,
+                                                 const K* __restrict__ b,
+                                                 uint32_t* rounds = nullptr) {
+    const int lane = threadIdx.x & 31;
+    const int g = lane / P, r = lane % P;
+    const unsigned gmask = P == 32 ? 0xffffffffu : ((1u << P) - 1u) << (g * P);
+    const uint64_t P1 = uint64_t(P) + 1;
+    while (__any_sync(0xffffffffu, hi > lo)) {
+        const bool active = hi > lo;
+        const uint64_t width = hi - lo;
+        const uint64_t q = lo + ((uint64_t(r) + 1) * width + P) / P1;  // in (lo, hi]
+        bool not_far = true;
+        if (active) not_far = !(ldg_elem(b + (i - q)) < ldg_elem(a + (q - 1)));
+        const int nfalse = __popc(__ballot_sync(0xffffffffu, not_far) & gmask);
+        if (active) {
+            const int f = nfalse - 1;
+            const uint64_t nlo = f >= 0 ? lo + ((uint64_t(f) + 1) * width + P) / P1 : lo;
+            const uint64_t nhi = f + 1 < P ? lo + ((uint64_t(f) + 2) * width + P) / P1 - 1 : hi;
+            lo = nlo;
+            hi = nhi;
+        }
+        if (rounds) ++*rounds;
+    }
+    return lo;
+}
+
+// Stage src[lo, hi) for a TMA copy whose destination `dst` corresponds to
+// element lo - lo % vece: returns the 16-byte-multiple body in bytes; the
+// elements past the array's last full 16 bytes are copied here (scalar).
+template <typename E>
+__device__ __forceinline__ uint32_t stage_copy_plan(const E* __restrict__ src, uint64_t len,
+                                                    uint64_t lo, uint64_t hi, E* dst, int vece) {
+    if (hi <= lo) return 0;
+    const uint64_t lo_al = lo - lo % vece;
+    uint64_t hi_al = (hi + vece - 1) / vece * vece;
+    const uint64_t len_al = len - len % vece;
+    if (hi_al > len) hi_al = len_al > lo_al ? len_al : lo_al;
+    for (uint64_t e = hi_al; e < hi; ++e) dst[e - lo_al] = src[e];
+    return uint32_t((hi_al - lo_al) * sizeof(E));
+}
+
+__device__ __forceinline__ int pow2_group(int k) {  // lanes per group for k searches
+    int p = 32;
+    while (p > 1 && (32 / p) < k) p >>= 1;
+    return p;
+}
+
+template <typename K, bool HAS_V>
+__global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, 2)
+    merge_pipe_kernel(const pipe_args args) {
+    using L = pipe_layout<K, HAS_V>;
+    constexpr int NC = L::kConsumers;
+    constexpr int VT = L::VT;
+    constexpr int T = L::T;
+    constexpr int NST = L::NST;
+    constexpr int VECE = L::VECE;
+    constexpr int NB = L::NB;
+
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::oBars);
+    uint64_t* empty = full + NST;
+    uint64_t* meta = reinterpret_cast<uint64_t*>(smem + L::oMeta);
+    uint64_t* desc = reinterpret_cast<uint64_t*>(smem + L::oDesc);
+    uint64_t* scratch = reinterpret_cast<uint64_t*>(smem + L::oScratch);
+    volatile uint32_t* pushed = reinterpret_cast<volatile uint32_t*>(smem + L::oMisc);
+    volatile uint32_t* issued = pushed + 1;
+
+    const K* __restrict__ a = static_cast<const K*>(args.a);
+    const K* __restrict__ b = static_cast<const K*>(args.b);
+    const uint64_t m = args.m, n = args.n, total = m + n;
+    const uint64_t NT = args.ntiles;
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const uint32_t G = gridDim.x, c = blockIdx.x;
+    const uint64_t NS = args.static_tiles;
+
+    auto diag_of = [=](uint64_t t) {  // output rank of tile boundary t
+        const uint64_t d = t * uint64_t(T);
+        return d < total ? d : total;
+    };
+    auto full_bracket = [=](uint64_t i, uint64_t& lo, uint64_t& hi) {
+        lo = i > n ? i - n : 0;
+        hi = i < m ? i : m;
+    };
+
+    const unsigned long long t_start = globaltimer_ns();
+    if (args.trace && tid == 0) {
+        args.trace[8 * c + 0] = t_start;
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        args.trace[8 * c + 4] = smid;
+    }
+    if (tid == 0) {
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        *pushed = 0;
+        *issued = 0;
+        mbar_fence_init();
+    }
+    // ---- start-up: this worker's static range [ts0, te0) of the first NS
+    // tiles, proportional to its weight (weights learned from the throughput
+    // of earlier launches; any weights give a valid partition), then co-rank
+    // its start with one warp (33-ary; few concurrent probes keep rounds short).
+    uint64_t ts0 = 0, te0 = 0;
+    if (warp == 9) {
+        uint64_t below = 0, all = 0;
+        if (args.nweights == G) {
+            for (uint32_t x = lane; x < G; x += 32) {
+                all += args.weights[x];
+                if (x < c) below += args.weights[x];
+            }
+            for (int o = 16; o; o >>= 1) {
+                all += __shfl_xor_sync(0xffffffffu, all, o);
+                below += __shfl_xor_sync(0xffffffffu, below, o);
+            }
+        } else {
+            below = c;
+            all = G;
+        }
+        ts0 = NS * below / all;
+        te0 = NS * (below + (args.nweights == G ? args.weights[c] : 1)) / all;
+        if (lane == 0) {
+            scratch[33] = ts0;
+            scratch[34] = te0;
+        }
+        if (te0 > ts0) {
+            uint64_t lo, hi;
+            full_bracket(diag_of(ts0), lo, hi);
+            const uint64_t j = group_search<K>(diag_of(ts0), lo, hi, 32, a, b);
+            if (lane == 0) scratch[0] = j;
+        }
+    }
+    __syncthreads();
+    ts0 = scratch[33];
+    te0 = scratch[34];
+    // the idle consumer warps co-rank boundaries ts0+1 .. ts0+8 (one warp each,
+    // 33-ary, bracketed by the start split) so the first tiles are ready fast
+    int known = 0;
+    if (te0 > ts0) {
+        known = te0 - ts0 - 1 < 8 ? int(te0 - ts0 - 1) : 8;
+        if (warp < known) {
+            const uint64_t t = ts0 + 1 + warp;
+            const uint64_t i = diag_of(t), i0 = diag_of(ts0), j0 = scratch[0];
+            uint64_t lo = j0, hi = j0 + (i - i0);
+            if (i > n && i - n > lo) lo = i - n;
+            if (i < hi) hi = i;
+            if (m < hi) hi = m;
+            const uint64_t j = group_search<K>(i, lo, hi, 32, a, b);
+            if (lane == 0) scratch[1 + warp] = j;
+        }
+    }
+    __syncthreads();
+    if (args.trace && tid == 0) args.trace[8 * c + 5] = globaltimer_ns();
+    if (warp == 9) {
+        // ------------------------------------------------------ scheduler
+        uint32_t n_rounds = 0, n_claims = 0;
+        unsigned long long t_search = 0;
+        // push tile descriptors for tiles [t, t+k): lane g supplies tile t+g's
+        // boundary splits (j0, j1); waits for ring space.
+        auto push = [&](uint64_t t, int k, uint64_t j0, uint64_t j1) {
+            const uint32_t p = *pushed;
+            while (p + uint32_t(k) > *issued + NB) __nanosleep(128);
+            if (lane < k) {
+                uint64_t* d = desc + 4 * ((p + lane) % NB);
+                d[0] = diag_of(t + lane);
+                d[1] = j0;
+                d[2] = j1;
+                d[3] = diag_of(t + lane + 1);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                *pushed = p + uint32_t(k);
+            }
+            __syncwarp();
+        };
+        // co-rank and push every tile of chunk [ts, te) given its start split
+        // js.  Each pass co-ranks the next k boundaries (k = 1, 4, 8, then 32:
+        // the first tiles are ready fast, later passes amortise latency) in
+        // 32/k lane groups, every one bracketed by the last known boundary:
+        // at least j_c and at most j_c + (i - i_c) elements come from A.
+        auto run_chunk = [&](uint64_t ts, uint64_t te, uint64_t js, int known_inner) {
+            uint64_t cur = ts, jc = js;
+            if (known_inner > 0) {  // boundaries ts+1 .. ts+known_inner are in scratch[1..]
+                const int k = known_inner;
+                const uint64_t jb = scratch[1 + (lane < k ? lane : k - 1)];
+                const uint64_t jprev = __shfl_up_sync(0xffffffffu, jb, 1);
+                push(cur, k, lane == 0 ? jc : jprev, jb);
+                jc = __shfl_sync(0xffffffffu, jb, k - 1);
+                cur += uint64_t(k);
+            }
+            int cap = known_inner > 0 ? 32 : 1;
+            while (cur < te) {
+                int k = int(te - cur < uint64_t(cap) ? te - cur : uint64_t(cap));
+                cap = cap == 1 ? 4 : (cap == 4 ? 8 : 32);
+                const int P = pow2_group(k);
+                const int g = lane / P;
+                const uint64_t tb = cur + 1 + uint64_t(g < k ? g : k - 1);
+                const uint64_t i = diag_of(tb);
+                const uint64_t ic = diag_of(cur);
+                uint64_t lo = jc, hi = jc + (i - ic);
+                if (i > n && i - n > lo) lo = i - n;
+                if (i < hi) hi = i;
+                if (m < hi) hi = m;
+                const unsigned long long t_s = args.trace ? globaltimer_ns() : 0;
+                const uint64_t j = group_search<K>(i, lo, hi, P, a, b, &n_rounds);
+                if (args.trace) t_search += globaltimer_ns() - t_s;
+                // lane g <- boundary cur + 1 + g (the result of group g)
+                const uint64_t jb = __shfl_sync(0xffffffffu, j, (lane < k ? lane : k - 1) * P);
+                const uint64_t jprev = __shfl_up_sync(0xffffffffu, jb, 1);
+                push(cur, k, lane == 0 ? jc : jprev, jb);
+                jc = __shfl_sync(0xffffffffu, jb, k - 1);
+                cur += uint64_t(k);
+            }
+        };
+
+        if (te0 > ts0) run_chunk(ts0, te0, scratch[0], known);
+        // guided self-scheduling of the dynamic region [NS, NT)
+        const uint64_t base = NS;
+        const uint64_t nd = NT - base;
+        for (; nd > 0;) {
+            while (*pushed - *issued >= args.lookahead) __nanosleep(256);
+            uint64_t ts = 0, sz = 0;
+            if (lane == 0) {
+                const uint64_t seen = *reinterpret_cast<volatile unsigned int*>(args.work);
+                const uint64_t rem = nd > seen ? nd - seen : 0;
+                sz = rem / (2 * uint64_t(G));
+                if (sz < args.min_chunk) sz = args.min_chunk;
+                ts = atomicAdd(args.work, unsigned(sz));
+            }
+            ts = __shfl_sync(0xffffffffu, ts, 0);
+            sz = __shfl_sync(0xffffffffu, sz, 0);
+            if (ts >= nd) break;
+            ts += base;
+            const uint64_t te = ts + sz < NT ? ts + sz : NT;
+            uint64_t lo, hi;
+            full_bracket(diag_of(ts), lo, hi);
+            const unsigned long long t_s = args.trace ? globaltimer_ns() : 0;
+            const uint64_t js = group_search<K>(diag_of(ts), lo, hi, 32, a, b, &n_rounds);
+            if (args.trace) t_search += globaltimer_ns() - t_s;
+            ++n_claims;
+            run_chunk(ts, te, js, 0);
+        }
+        if (args.trace && lane == 0) {
+            args.trace[8 * c + 1] = (uint64_t(n_claims) << 48) | (uint64_t(n_rounds) << 32) |
+                                    (t_search / 1000);  // claims | rounds | search us
+        }
+        // end marker
+        {
+            const uint32_t p = *pushed;
+            while (p + 1 > *issued + NB) __nanosleep(128);
+            if (lane == 0) {
+                desc[4 * (p % NB)] = ~uint64_t(0);
+                __threadfence_block();
+                *pushed = p + 1;
+            }
+        }
+        return;
+    }
+
+    if (warp == 8) {
+        // ------------------------------------------------------ producer
+        if (lane != 0) return;
+        const uint64_t policy = policy_evict_first();
+        unsigned long long starve = 0;  // ns spent waiting for descriptors
+        for (uint32_t s = 0;; ++s) {
+            const int st = int(s % NST);
+            if (s >= uint32_t(NST)) mbar_wait(&empty[st], uint32_t((s / NST - 1) & 1));
+            if (*pushed <= s) {
+                const unsigned long long w0 = args.trace ? globaltimer_ns() : 0;
+                while (*pushed <= s) __nanosleep(64);
+                if (args.trace) starve += globaltimer_ns() - w0;
+            }
+            __threadfence_block();
+            const uint64_t* d = desc + 4 * (s % NB);
+            const uint64_t i0 = d[0];
+            uint64_t* mt = meta + 4 * st;
+            if (i0 == ~uint64_t(0)) {
+                mt[3] = uint64_t(1) << 63;  // done
+                mbar_arrive(&full[st]);
+                if (args.trace) args.trace[8 * c + 6] = starve;
+                break;
+            }
+            const uint64_t j0 = d[1], j1 = d[2], i1 = d[3];
+            *issued = s + 1;
+            const uint64_t k0 = i0 - j0, k1 = i1 - j1;
+            const uint32_t a_len = uint32_t(j1 - j0), b_len = uint32_t(k1 - k0);
+            unsigned char* stage = smem + L::oStages + size_t(st) * L::kStage;
+            K* sk = reinterpret_cast<K*>(stage);
+            uint32_t* sv = reinterpret_cast<uint32_t*>(stage + L::kStageKeys);
+            const uint32_t a_off = uint32_t(j0 % VECE);
+            const uint32_t b_base = (a_off + a_len + VECE - 1) / VECE * VECE;
+            const uint32_t b_off = uint32_t(k0 % VECE);
+            const uint32_t ab = stage_copy_plan(a, m, j0, j1, sk, VECE);
+            const uint32_t bb = stage_copy_plan(b, n, k0, k1, sk + b_base, VECE);
+            uint32_t avb = 0, bvb = 0, av_off = 0, bv_base = 0;
+            if constexpr (HAS_V) {
+                av_off = uint32_t(j0 % 4);
+                bv_base = (av_off + a_len + 3) / 4 * 4;
+                avb = stage_copy_plan(args.av, m, j0, j1, sv, 4);
+                bvb = stage_copy_plan(args.bv, n, k0, k1, sv + bv_base, 4);
+            }
+            mt[0] = i0;
+            mt[1] = k0;
+            mt[2] = (uint64_t(a_len) << 32) | b_len;
+            mt[3] = (uint64_t(a_off) << 48) | (uint64_t(b_base) << 24) | (uint64_t(b_off) << 8) |
+                    uint64_t(av_off);
+            mbar_arrive_expect_tx(&full[st], ab + bb + avb + bvb);
+            if (ab) tma_load_1d(sk, a + (j0 - j0 % VECE), ab, &full[st], policy);
+            if (bb) tma_load_1d(sk + b_base, b + (k0 - k0 % VECE), bb, &full[st], policy);
+            if constexpr (HAS_V) {
+                if (avb) tma_load_1d(sv, args.av + (j0 - j0 % 4), avb, &full[st], policy);
+                if (bvb)
+                    tma_load_1d(sv + bv_base, args.bv + (k0 - k0 % 4), bvb, &full[st], policy);
+            }
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------- consumers
+    K* __restrict__ out = static_cast<K*>(args.out);
+    uint32_t* __restrict__ outv = args.outv;
+    unsigned long long data_wait = 0;  // ns consumers waited for stage data
+    uint32_t s_done = 0;
+    unsigned long long t_stream = 0;   // when the first tile's data arrived
+    for (uint32_t s = 0;; ++s) {
+        const int st = int(s % NST);
+        if (args.trace && tid == 0) {
+            const unsigned long long w0 = globaltimer_ns();
+            mbar_wait(&full[st], uint32_t((s / NST) & 1));
+            data_wait += globaltimer_ns() - w0;
+        }
+        mbar_wait(&full[st], uint32_t((s / NST) & 1));
+        if (s == 0) t_stream = globaltimer_ns();
+        const uint64_t* mt = meta + 4 * st;
+        const uint64_t packed = mt[3];
+        if (packed >> 63) {
+            s_done = s;
+            break;
+        }
+        const uint64_t i0 = mt[0];
+        const uint64_t lens = mt[2];
+        const int a_len = int(lens >> 32), b_len = int(lens & 0xffffffffu);
+        const int len = a_len + b_len;
+        const int a_off = int((packed >> 48) & 0xff), b_base = int((packed >> 24) & 0xffffff);
+        const int b_off = int((packed >> 8) & 0xff), av_off = int(packed & 0xff);
+        unsigned char* stage = smem + L::oStages + size_t(st) * L::kStage;
+        K* sk = reinterpret_cast<K*>(stage);
+        uint32_t* sv = reinterpret_cast<uint32_t*>(stage + L::kStageKeys);
+
+        const int diag = min(tid * VT, len);
+        K keys[VT];
+        uint32_t src[VT];
+        merge_thread<K, VT, HAS_V>(sk + a_off, a_len, sk + b_base + b_off, b_len, diag, keys, src);
+        if constexpr (HAS_V) {
+            const int bv_base = (av_off + a_len + 3) / 4 * 4;
+            const int bv_off = int(mt[1] & 3);
+            const uint32_t* sav = sv + av_off;
+            const uint32_t* sbv = sv + bv_base + bv_off;
+#pragma unroll
+            for (int v = 0; v < VT; ++v)
+                if (diag + v < len)
+                    src[v] = (src[v] & 0x80000000u) ? sbv[src[v] & 0x7fffffffu] : sav[src[v]];
+        }
+        named_bar_sync(1, NC);  // every thread is done reading the windows
+        const int cnt = len - diag < VT ? len - diag : VT;
+#pragma unroll
+        for (int v = 0; v < VT; ++v)
+            if (v < cnt) {
+                sk[tid * VT + v] = keys[v];
+                if constexpr (HAS_V) sv[tid * VT + v] = src[v];
+            }
+        fence_proxy_async_smem();
+        named_bar_sync(1, NC);
+        if (tid == 0) {
+            const uint32_t kb_bytes = uint32_t(len * sizeof(K)) & ~15u;
+            if (kb_bytes) tma_store_1d(out + i0, sk, kb_bytes);
+            for (int x = kb_bytes / sizeof(K); x < len; ++x) out[i0 + x] = sk[x];
+            if constexpr (HAS_V) {
+                const uint32_t vb_bytes = uint32_t(len * 4) & ~15u;
+                if (vb_bytes) tma_store_1d(outv + i0, sv, vb_bytes);
+                for (int x = vb_bytes / 4; x < len; ++x) outv[i0 + x] = sv[x];
+            }
+            tma_store_commit();
+            tma_store_wait_read<0>();  // the stage has been read by the store
+            mbar_arrive(&empty[st]);
+        }
+        if (args.trace && tid == 0 && s == 0) args.trace[8 * c + 2] = globaltimer_ns();
+    }
+    if (tid == 0) tma_store_wait_all();
+    if (args.perf && tid == 0) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        args.perf[4 * c] = smid;
+        args.perf[4 * c + 1] = globaltimer_ns() - t_stream;
+        args.perf[4 * c + 2] = s_done;
+        args.perf[4 * c + 3] = 1;  // valid
+    }
+    if (args.trace && tid == 0) {
+        args.trace[8 * c + 3] = globaltimer_ns();
+        args.trace[8 * c + 7] = data_wait;
+    }
+}
+
+}  // namespace comerge_b200

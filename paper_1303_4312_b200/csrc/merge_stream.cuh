@@ -128,33 +128,40 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 }
 
 // ------------------------------------------------------------ configuration
+//
+// Each tile of T outputs needs up to T elements of EACH input resident (the
+// merge path may take all of them from one side); what the rings hold beyond
+// that window is prefetch.  Rings are NS chunks of CH elements (NS need not be
+// a power of two: a ring index is wrapped with one conditional subtract).
+// Budgets target 2 CTAs per SM (<= ~110 KB each) with >= 24 KB of prefetch
+// per input per CTA.
 
 template <typename K, bool HAS_V>
 struct stream_cfg;
 
-// int32 / uint32 keys only: tile 3840, chunk 4 KB, ring 32 KB per input.
+// 32-bit keys only: tile 3840, chunk 4 KB, ring 12 chunks (48 KB) per input.
 template <>
 struct stream_cfg<int32_t, false> {
-    static constexpr int VT = 15, CH = 1024, NS = 8;
+    static constexpr int VT = 15, CH = 1024, NS = 12;
 };
 template <>
 struct stream_cfg<uint32_t, false> : stream_cfg<int32_t, false> {};
-// 32-bit keys + payload: tile 1792, ring 4096 elements per input.
+// 32-bit keys + payload: tile 1792, chunk 512, ring 6144 elements (48 KB).
 template <>
 struct stream_cfg<int32_t, true> {
-    static constexpr int VT = 7, CH = 512, NS = 8;
+    static constexpr int VT = 7, CH = 512, NS = 12;
 };
 template <>
 struct stream_cfg<uint32_t, true> : stream_cfg<int32_t, true> {};
-// 64-bit keys only: tile 1792.
+// 64-bit keys only: tile 1792, ring 6144 elements (48 KB).
 template <>
 struct stream_cfg<uint64_t, false> {
-    static constexpr int VT = 7, CH = 512, NS = 8;
+    static constexpr int VT = 7, CH = 512, NS = 12;
 };
-// 64-bit keys + payload: tile 1280, ring 2048 elements per input.
+// 64-bit keys + payload: tile 1280, chunk 256, ring 3584 elements (42 KB).
 template <>
 struct stream_cfg<uint64_t, true> {
-    static constexpr int VT = 5, CH = 256, NS = 8;
+    static constexpr int VT = 5, CH = 256, NS = 14;
 };
 
 template <typename K, bool HAS_V>
@@ -166,10 +173,10 @@ struct stream_layout {
     static constexpr int T = kConsumers * VT;
     static constexpr int CH = C::CH;
     static constexpr int NS = C::NS;
-    static constexpr int RING = CH * NS;  // elements per input ring (power of two)
-    static_assert((RING & (RING - 1)) == 0, "ring must be a power of two");
+    static constexpr int RING = CH * NS;  // elements per input ring
     static_assert(RING >= T + CH, "ring must hold a full tile window plus one chunk");
     static_assert((T * sizeof(K)) % 16 == 0 && (T * 4) % 16 == 0, "tile must be 16B multiple");
+    static_assert((CH * sizeof(K)) % 16 == 0 && CH % 4 == 0, "chunks must be 16B multiples");
     static constexpr int VECE = 16 / sizeof(K);  // elements per 16 bytes
     // byte offsets in dynamic shared memory
     static constexpr size_t kRingKeys = size_t(RING) * sizeof(K);
@@ -181,8 +188,7 @@ struct stream_layout {
     static constexpr size_t oStage = oRingBV + kRingVals;
     static constexpr size_t kStageKeys = size_t(T) * sizeof(K);
     static constexpr size_t kStageVals = HAS_V ? size_t(T) * 4 : 0;
-    static constexpr size_t kStage = kStageKeys + kStageVals;
-    static constexpr size_t oBars = oStage + 2 * kStage;
+    static constexpr size_t oBars = oStage + kStageKeys + kStageVals;
     static constexpr size_t kBars = size_t(4 * NS) * 8;
     static constexpr size_t oMisc = oBars + kBars;
     static constexpr size_t kMisc = 128;
@@ -235,7 +241,15 @@ struct stream_args {
     void* out;
     uint32_t* outv;
     uint64_t ntiles;
+    unsigned long long* trace;  // optional per-CTA phase timestamps (ns), 8 per CTA
+    int search_mode;            // unused (kept for layout)
 };
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 template <typename K, bool HAS_V>
 __global__ void __launch_bounds__(stream_layout<K, HAS_V>::kThreads, 2)
@@ -246,7 +260,8 @@ __global__ void __launch_bounds__(stream_layout<K, HAS_V>::kThreads, 2)
     constexpr int T = L::T;
     constexpr int CH = L::CH;
     constexpr int NS = L::NS;
-    constexpr int MASK = L::RING - 1;
+    constexpr int RING = L::RING;
+    auto wrap = [](uint32_t x) { return x >= uint32_t(RING) ? x - uint32_t(RING) : x; };
     constexpr int VECE = L::VECE;
 
     extern __shared__ __align__(128) unsigned char smem[];
@@ -273,6 +288,7 @@ __global__ void __launch_bounds__(stream_layout<K, HAS_V>::kThreads, 2)
     const uint64_t o_begin = t0 * T;
     const uint64_t o_end = t1 * T < total ? t1 * T : total;
 
+    if (args.trace && tid == 0) args.trace[8 * blockIdx.x + 0] = globaltimer_ns();
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
             mbar_init(&fullA[s], 1);
@@ -290,11 +306,13 @@ __global__ void __launch_bounds__(stream_layout<K, HAS_V>::kThreads, 2)
         if ((tid & 127) == 0) misc64[g] = j;
     }
     __syncthreads();
+    if (args.trace && tid == 0) args.trace[8 * blockIdx.x + 1] = globaltimer_ns();
     const uint64_t j_begin = misc64[0], j_end = misc64[1];
     const uint64_t k_begin = o_begin - j_begin, k_end = o_end - j_end;
 
-    // chunk q of an input covers absolute elements [q*CH, (q+1)*CH); the
-    // ring position of element e is (e - q0*CH) & MASK.
+    // chunk q of an input covers absolute elements [q*CH, (q+1)*CH); relative
+    // chunk r = q - q0 lives in slot r % NS, so element e sits at ring
+    // position (e - q0*CH) % RING.
     const uint64_t qa0 = j_begin / CH, qb0 = k_begin / CH;
     const uint64_t na = j_end > j_begin ? (j_end - 1) / CH + 1 - qa0 : 0;
     const uint64_t nb = k_end > k_begin ? (k_end - 1) / CH + 1 - qb0 : 0;
@@ -324,26 +342,28 @@ __global__ void __launch_bounds__(stream_layout<K, HAS_V>::kThreads, 2)
             uint64_t hi_vv = (hi + 3) & ~uint64_t(3);
             const uint64_t len_vv = len & ~uint64_t(3);
             if (hi_vv > len) hi_vv = len_vv > lo_v ? len_vv : lo_v;
-            const int slot = int(r & (NS - 1));
-            for (uint64_t e = hi_v; e < hi; ++e) ring[(e - q0 * CH) & MASK] = src[e];
+            const int slot = int(r % NS);
+            const uint64_t base = q * CH;                 // first element of chunk r
+            K* const dst = ring + size_t(slot) * CH;      // chunk r's slot
+            uint32_t* const dstv = ringv + size_t(slot) * CH;
+            for (uint64_t e = hi_v; e < hi; ++e) dst[e - base] = src[e];
             if (HAS_V)
-                for (uint64_t e = hi_vv; e < hi; ++e) ringv[(e - q0 * CH) & MASK] = srcv[e];
+                for (uint64_t e = hi_vv; e < hi; ++e) dstv[e - base] = srcv[e];
             const uint32_t kb = uint32_t((hi_v - lo) * sizeof(K));
             const uint32_t vb = HAS_V ? uint32_t((hi_vv - lo_v) * 4) : 0;
             mbar_arrive_expect_tx(&full[slot], kb + vb);
-            if (kb) tma_load_1d(ring + ((lo - q0 * CH) & MASK), src + lo, kb, &full[slot], policy);
+            if (kb) tma_load_1d(dst + (lo - base), src + lo, kb, &full[slot], policy);
             if (HAS_V && vb)
-                tma_load_1d(ringv + ((lo_v - q0 * CH) & MASK), srcv + lo_v, vb, &full[slot],
-                            policy);
+                tma_load_1d(dstv + (lo_v - base), srcv + lo_v, vb, &full[slot], policy);
         };
         while (ia < na || ib < nb) {
             bool progressed = false;
-            if (ia < na && (ia < NS || mbar_test(&emptyA[ia & (NS - 1)], uint32_t((ia / NS - 1) & 1)))) {
+            if (ia < na && (ia < NS || mbar_test(&emptyA[ia % NS], uint32_t((ia / NS - 1) & 1)))) {
                 issue(a, args.av, m, j_begin, j_end, qa0, ia, ringA, ringAV, fullA);
                 ++ia;
                 progressed = true;
             }
-            if (ib < nb && (ib < NS || mbar_test(&emptyB[ib & (NS - 1)], uint32_t((ib / NS - 1) & 1)))) {
+            if (ib < nb && (ib < NS || mbar_test(&emptyB[ib % NS], uint32_t((ib / NS - 1) & 1)))) {
                 issue(b, args.bv, n, k_begin, k_end, qb0, ib, ringB, ringBV, fullB);
                 ++ib;
                 progressed = true;
@@ -354,11 +374,8 @@ __global__ void __launch_bounds__(stream_layout<K, HAS_V>::kThreads, 2)
     }
 
     // ----------------------------------------------------------- consumers
-    K* stage_k[2] = {reinterpret_cast<K*>(smem + L::oStage),
-                     reinterpret_cast<K*>(smem + L::oStage + L::kStage)};
-    uint32_t* stage_v[2] = {reinterpret_cast<uint32_t*>(smem + L::oStage + L::kStageKeys),
-                            reinterpret_cast<uint32_t*>(smem + L::oStage + L::kStage +
-                                                        L::kStageKeys)};
+    K* const sk = reinterpret_cast<K*>(smem + L::oStage);
+    uint32_t* const sv = reinterpret_cast<uint32_t*>(smem + L::oStage + L::kStageKeys);
     K* __restrict__ out = static_cast<K*>(args.out);
     uint32_t* __restrict__ outv = args.outv;
     volatile int* used = misc32 + 16;
@@ -366,6 +383,8 @@ __global__ void __launch_bounds__(stream_layout<K, HAS_V>::kThreads, 2)
     uint64_t a_pos = j_begin, b_pos = k_begin, o = o_begin;
     uint64_t ready_a = 0, ready_b = 0;  // chunks known complete (relative)
     uint64_t rel_a = 0, rel_b = 0;      // chunks released (relative)
+    uint32_t a_base = uint32_t((a_pos - qa0 * CH) % RING);
+    uint32_t b_base = uint32_t((b_pos - qb0 * CH) % RING);
     int s = 0;
     while (o < o_end) {
         const int len = int(o_end - o < uint64_t(T) ? o_end - o : uint64_t(T));
@@ -375,31 +394,28 @@ __global__ void __launch_bounds__(stream_layout<K, HAS_V>::kThreads, 2)
         if (a_cnt > 0) {
             const uint64_t need = (a_pos + a_cnt - 1) / CH - qa0 + 1;
             for (; ready_a < need; ++ready_a)
-                mbar_wait(&fullA[ready_a & (NS - 1)], uint32_t((ready_a / NS) & 1));
+                mbar_wait(&fullA[ready_a % NS], uint32_t((ready_a / NS) & 1));
         }
         if (b_cnt > 0) {
             const uint64_t need = (b_pos + b_cnt - 1) / CH - qb0 + 1;
             for (; ready_b < need; ++ready_b)
-                mbar_wait(&fullB[ready_b & (NS - 1)], uint32_t((ready_b / NS) & 1));
+                mbar_wait(&fullB[ready_b % NS], uint32_t((ready_b / NS) & 1));
         }
-        const uint32_t a_base = uint32_t((a_pos - qa0 * CH) & MASK);
-        const uint32_t b_base = uint32_t((b_pos - qb0 * CH) & MASK);
-        auto ra = [&](int x) { return ringA[(a_base + uint32_t(x)) & MASK]; };
-        auto rb = [&](int x) { return ringB[(b_base + uint32_t(x)) & MASK]; };
-
+#define RA(x) ringA[wrap(a_base + uint32_t(x))]
+#define RB(x) ringB[wrap(b_base + uint32_t(x))]
         const int diag = min(tid * VT, len);
         // co-rank of the diagonal inside the tile (Lemma-1 split)
         int lo = diag > b_cnt ? diag - b_cnt : 0;
         int hi = diag < a_cnt ? diag : a_cnt;
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
-            if (rb(diag - mid) < ra(mid - 1))
+            if (RB(diag - mid) < RA(mid - 1))
                 hi = mid - 1;
             else
                 lo = mid;
         }
         int ia = lo, ib = diag - lo;
-        K ka = ra(ia), kb = rb(ib);
+        K ka = RA(ia), kb = RB(ib);
         K keys[VT];
         uint32_t src[VT];
         const int cnt = len - diag < VT ? len - diag : VT;
@@ -409,17 +425,19 @@ __global__ void __launch_bounds__(stream_layout<K, HAS_V>::kThreads, 2)
                 const bool take_b = ib < b_cnt && (ia >= a_cnt || kb < ka);
                 keys[v] = take_b ? kb : ka;
                 if constexpr (HAS_V)
-                    src[v] = take_b ? (((b_base + uint32_t(ib)) & MASK) | 0x80000000u)
-                                    : ((a_base + uint32_t(ia)) & MASK);
+                    src[v] = take_b ? (wrap(b_base + uint32_t(ib)) | 0x80000000u)
+                                    : wrap(a_base + uint32_t(ia));
                 if (take_b) {
                     ++ib;
-                    kb = rb(ib);
+                    kb = RB(ib);
                 } else {
                     ++ia;
-                    ka = ra(ia);
+                    ka = RA(ia);
                 }
             }
         }
+#undef RA
+#undef RB
         if constexpr (HAS_V) {
 #pragma unroll
             for (int v = 0; v < VT; ++v)
@@ -430,11 +448,9 @@ __global__ void __launch_bounds__(stream_layout<K, HAS_V>::kThreads, 2)
             used[0] = ia;
             used[1] = ib;
         }
-        if (tid == 0) tma_store_wait_read<1>();  // staging buffer s&1 is free again
+        if (tid == 0) tma_store_wait_read<0>();  // previous tile's store has read the stage
         named_bar_sync(1, NC);                     // ring reads done, `used` visible
         const int used_a = used[0], used_b = used[1];
-        K* sk = stage_k[s & 1];
-        uint32_t* sv = stage_v[s & 1];
 #pragma unroll
         for (int v = 0; v < VT; ++v)
             if (v < cnt) {
@@ -445,14 +461,16 @@ __global__ void __launch_bounds__(stream_layout<K, HAS_V>::kThreads, 2)
         named_bar_sync(1, NC);
         a_pos += used_a;
         b_pos += used_b;
+        a_base = wrap(a_base + uint32_t(used_a));
+        b_base = wrap(b_base + uint32_t(used_b));
         if (tid == 0) {
             // release chunks the merge front has passed
             while (rel_a < ready_a && (qa0 + rel_a + 1) * CH <= a_pos) {
-                mbar_arrive(&emptyA[rel_a & (NS - 1)]);
+                mbar_arrive(&emptyA[rel_a % NS]);
                 ++rel_a;
             }
             while (rel_b < ready_b && (qb0 + rel_b + 1) * CH <= b_pos) {
-                mbar_arrive(&emptyB[rel_b & (NS - 1)]);
+                mbar_arrive(&emptyB[rel_b % NS]);
                 ++rel_b;
             }
             // tile store: 16-byte body by TMA, a scalar tail at the very end
@@ -466,10 +484,12 @@ __global__ void __launch_bounds__(stream_layout<K, HAS_V>::kThreads, 2)
             }
             tma_store_commit();
         }
+        if (args.trace && tid == 0 && s == 0) args.trace[8 * blockIdx.x + 2] = globaltimer_ns();
         o += len;
         ++s;
     }
     if (tid == 0) tma_store_wait_all();
+    if (args.trace && tid == 0) args.trace[8 * blockIdx.x + 3] = globaltimer_ns();
 }
 
 }  // namespace comerge_b200

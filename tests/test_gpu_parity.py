@@ -35,7 +35,7 @@ def P():
     return mod
 
 
-@pytest.fixture(params=["tile", "stream"])
+@pytest.fixture(params=["tile", "stream", "pipe"])
 def path(request):
     """Run a test through each device kernel (v1 tile, v2 streaming)."""
     P().set_kernel_path(request.param)

@@ -1,0 +1,84 @@
+"""Run one BASELINE config a few times (for ncu / tracing on the GPU box).
+
+    python tools/run_config.py C2 [--path auto|tile|stream] [--reps 3] [--trace]
+"""
+import argparse
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_1303_4312_b200 as P  # noqa: E402
+from paper_1303_4312_b200 import _native as N  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("config")
+    ap.add_argument("--path", default="auto")
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--trace", action="store_true")
+    ap.add_argument("--static-pct", type=int, default=0)
+    ap.add_argument("--min-chunk", type=int, default=0)
+    ap.add_argument("--lookahead", type=int, default=0)
+    args = ap.parse_args()
+    dev = torch.device("cuda:0")
+    inp = bench.make_inputs(args.config, device=dev)
+    out = bench.alloc_outputs(args.config, inp)
+    P.set_kernel_path(args.path)
+    N.lib.comerge_cuda_set_tuning(args.static_pct, args.min_chunk, args.lookahead)
+    flush = torch.empty(512 * 2**20 // 4, dtype=torch.int32, device=dev)
+    trace = torch.zeros(8 * 4096, dtype=torch.int64, device=dev) if args.trace else None
+    for r in range(args.reps):
+        flush.fill_(r)
+        if trace is not None and r == args.reps - 1:
+            N.lib.comerge_cuda_set_trace(C.c_void_p(trace.data_ptr()))
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        bench.run_config(args.config, inp, out)
+        e.record()
+        torch.cuda.synchronize()
+        N.lib.comerge_cuda_set_trace(None)
+        print(f"{args.config} rep {r}: {s.elapsed_time(e) * 1e3:.1f} us "
+              f"(path {N.lib.comerge_cuda_last_path()})")
+    if trace is not None:
+        full = trace.view(-1, 8).cpu()
+        full = full[full[:, 0] > 0]
+        t = full[:, :4]
+        t0 = t[:, 0].min()
+        rel = (t - t0).double() / 1e3
+        q = lambda x: [round(float(x.quantile(p)), 2) for p in (0.0, 0.5, 0.9, 1.0)]  # noqa: E731
+        print(f"CTAs {t.shape[0]}; us from first CTA start [min, p50, p90, max]:")
+        print("  start      ", q(rel[:, 0]))
+        sched = full[:, 1]
+        print("  sched claims", q((sched >> 48).double()), "rounds", q(((sched >> 32) & 0xffff).double()),
+              "search us", q((sched & 0xffffffff).double()))
+        print("  first tile ", q(rel[:, 2]))
+        print("  end        ", q(rel[:, 3]))
+
+        dur = rel[:, 3] - rel[:, 2]
+        sm = full[:, 4]
+        order = torch.argsort(dur)
+        print("  stream dur ", q(dur))
+        print("  startup done", q((full[:, 5] - t0).double() / 1e3))
+        print("  producer starved us", q(full[:, 6].double() / 1e3))
+        print("  consumer data-wait us", q(full[:, 7].double() / 1e3))
+        print("  slowest 12 (cta, smid, us):",
+              [(int(i), int(sm[i]), round(float(dur[i]), 1)) for i in order[-12:]])
+        print("  fastest 6  (cta, smid, us):",
+              [(int(i), int(sm[i]), round(float(dur[i]), 1)) for i in order[:6]])
+        by_sm = {}
+        for i in range(len(sm)):
+            by_sm.setdefault(int(sm[i]), []).append(round(float(rel[i, 3]), 1))
+        ends = sorted(((max(v), k, v) for k, v in by_sm.items()))
+        print("  latest-finishing SMs:", [(k, v) for _, k, v in ends[-8:]])
+        print("  earliest-finishing SMs:", [(k, v) for _, k, v in ends[:4]])
+
+
+if __name__ == "__main__":
+    main()
