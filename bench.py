@@ -97,11 +97,21 @@ def make_inputs(cfg, seed=SEED, device="cuda"):
 
 
 def alloc_outputs(cfg, inp):
+    """Outputs plus the merge's scratch workspace (queried, CUB-style)."""
     import torch
+    import paper_1303_4312_b200._native as N
     total = inp["a"].numel() + inp["b"].numel()
-    out = dict(keys=torch.empty(total, dtype=inp["a"].dtype, device=inp["a"].device))
+    dev = inp["a"].device
+    out = dict(keys=torch.empty(total, dtype=inp["a"].dtype, device=dev))
+    kind = {"int32": N.KEY_I32, "uint64": N.KEY_U64}[CONFIGS[cfg]["dtype"]]
+    if CONFIGS[cfg]["kind"] == "segmented":
+        wsb = N.lib.comerge_cuda_segmented_workspace_bytes(total, inp["a_off"].numel() - 1, kind)
+    else:
+        wsb = N.lib.comerge_cuda_merge_workspace_bytes(inp["a"].numel(), inp["b"].numel(), kind,
+                                                       int(CONFIGS[cfg]["kind"] == "pairs"))
+    out["ws"] = torch.empty(max(int(wsb), 256), dtype=torch.uint8, device=dev)
     if CONFIGS[cfg]["kind"] == "pairs":
-        out["vals"] = torch.empty(total, dtype=torch.uint32, device=inp["a"].device)
+        out["vals"] = torch.empty(total, dtype=torch.uint32, device=dev)
     return out
 
 
@@ -111,12 +121,15 @@ def run_config(cfg, inp, out=None):
     if out is None:
         out = alloc_outputs(cfg, inp)
     kind = CONFIGS[cfg]["kind"]
+    ws = out.get("ws")
     if kind == "keys":
-        P.stable_merge(inp["a"], inp["b"], out["keys"])
+        P.stable_merge(inp["a"], inp["b"], out["keys"], workspace=ws)
     elif kind == "pairs":
-        P.merge_pairs(inp["a"], inp["av"], inp["b"], inp["bv"], out["keys"], out["vals"])
+        P.merge_pairs(inp["a"], inp["av"], inp["b"], inp["bv"], out["keys"], out["vals"],
+                      workspace=ws)
     else:
-        P.merge_segmented(inp["a"], inp["a_off"], inp["b"], inp["b_off"], out["keys"])
+        P.merge_segmented(inp["a"], inp["a_off"], inp["b"], inp["b_off"], out["keys"],
+                          workspace=ws)
     return out
 
 
@@ -189,6 +202,37 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ timing
 
+_CUDART = None
+
+
+def _cudart():
+    """The CUDA runtime the merge library itself uses (for raw event handles)."""
+    global _CUDART
+    if _CUDART is None:
+        import paper_1303_4312_b200._native  # noqa: F401  (loads libcudart first)
+        _CUDART = C.CDLL("libcudart.so.12")
+        _CUDART.cudaEventCreate.argtypes = [C.POINTER(C.c_void_p)]
+        _CUDART.cudaEventElapsedTime.argtypes = [C.POINTER(C.c_float), C.c_void_p, C.c_void_p]
+    return _CUDART
+
+
+def raw_events(k):
+    rt = _cudart()
+    out = []
+    for _ in range(k):
+        e = C.c_void_p()
+        assert rt.cudaEventCreate(C.byref(e)) == 0
+        out.append(e)
+    return out
+
+
+def raw_elapsed_ms(e0, e1):
+    ms = C.c_float()
+    rc = _cudart().cudaEventElapsedTime(C.byref(ms), e0, e1)
+    assert rc == 0, f"cudaEventElapsedTime failed ({rc})"
+    return float(ms.value)
+
+
 def peak_hbm():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -203,7 +247,8 @@ def traffic_for(cfg):
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(cfg)
+            v = json.load(f).get(cfg)
+        return v if isinstance(v, (int, float)) else None
     except Exception:
         return None
 
@@ -219,20 +264,22 @@ def time_config(cfg, steps, warmup, device, seed=SEED, dist_ctx=None, clocks=Fal
     for _ in range(max(warmup, 0)):
         run_config(cfg, inp, out)
     torch.cuda.synchronize(device)
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] + list(raw_events(2))
+          for _ in range(steps)]
     sampler = ClockSampler(device.index or 0) if clocks else None
     if dist_ctx:
         dist_ctx.barrier()
     torch.cuda.synchronize(device)
     if sampler:
         sampler.__enter__()
+    # hold the GPU behind a spin so the host enqueues every step before the
+    # device starts them: step events then time device work, not host enqueue
+    torch.cuda._sleep(int(2e8))
     for k in range(steps):
         flush.fill_(k)  # evict L2 (> 126 MB) outside the timed events
         s0, s1, k0, k1 = ev[k]
         s0.record(stream)
-        k0.record(stream)  # marks the torch events recorded; the library re-records
-        k1.record(stream)  # them around the merge kernel itself
-        N.lib.comerge_cuda_set_kernel_events(C.c_void_p(k0.cuda_event), C.c_void_p(k1.cuda_event))
+        N.lib.comerge_cuda_set_kernel_events(k0, k1)  # recorded around the merge kernel
         run_config(cfg, inp, out)
         N.lib.comerge_cuda_set_kernel_events(None, None)
         s1.record(stream)
@@ -243,7 +290,7 @@ def time_config(cfg, steps, warmup, device, seed=SEED, dist_ctx=None, clocks=Fal
         sampler.__exit__()
     path = N.lib.comerge_cuda_last_path()
     step_ms = [e[0].elapsed_time(e[1]) for e in ev]
-    kern_ms = [e[2].elapsed_time(e[3]) for e in ev]
+    kern_ms = [raw_elapsed_ms(e[2], e[3]) for e in ev]
     res = dict(total=total, step_ms=step_ms, kern_ms=kern_ms, path=path,
                clocks=sampler.summary() if sampler else None, inp=inp, out=out)
     return res

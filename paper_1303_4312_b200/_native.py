@@ -12,7 +12,7 @@ import re
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 REPO_DIR = os.path.dirname(PKG_DIR)
-LIB_PATH = os.path.join(PKG_DIR, "lib", "libcomerge_cuda.so")
+LIB_PATH = os.environ.get("COMERGE_LIB_PATH") or os.path.join(PKG_DIR, "lib", "libcomerge_cuda.so")
 HEADERS = [os.path.join(REPO_DIR, "include", "comerge_cuda.h"),
            os.path.join(REPO_DIR, "include", "comerge_cuda_testkit.h")]
 

@@ -173,16 +173,34 @@ def _check_out(who, a, b, out):
         raise ValueError(f"{who}: output length must equal |a| + |b|")
 
 
-def stable_merge(a, b, out=None):
+def _ws(workspace):
+    if workspace is None:
+        return None, 0
+    return C.c_void_p(workspace.data_ptr()), int(workspace.numel() * workspace.element_size())
+
+
+def workspace_bytes(m: int, n: int, dtype, has_payload: bool = False) -> int:
+    """Scratch bytes a device merge of (m, n) may use (CUB-style query);
+    dtype is a numpy or torch dtype of the keys."""
+    name = str(dtype).replace("torch.", "") if torch is not None and isinstance(dtype, torch.dtype) \
+        else np.dtype(dtype).name
+    kind = _KIND[_SUFFIX[name]]
+    return int(N.lib.comerge_cuda_merge_workspace_bytes(m, n, kind, int(has_payload)))
+
+
+def stable_merge(a, b, out=None, workspace=None):
     """Stable two-way merge into out (merge.hpp:52-68).  Device tensors run
-    asynchronously on the current stream; host arrays synchronously."""
+    asynchronously on the current stream (scratch from `workspace`, a device
+    tensor of >= workspace_bytes() bytes, else from a stream-ordered pool);
+    host arrays synchronously."""
     suf = _suffix(a)
     if out is None:
         out = _empty_like_merge(a, _len(a) + _len(b))
     _check_out("stable_merge", a, b, out)
     if _is_torch(a) and a.is_cuda:
+        wsp, wsb = _ws(workspace)
         N.check(getattr(N.lib, f"comerge_cuda_merge_keys_{suf}")(
-            _ptr(a), _len(a), _ptr(b), _len(b), _ptr(out), None, 0, _stream(a)))
+            _ptr(a), _len(a), _ptr(b), _len(b), _ptr(out), wsp, wsb, _stream(a)))
     else:
         rep = N.MergeReport()
         rc = getattr(N.lib, f"comerge_merge_parallel_{suf}")(
@@ -300,7 +318,7 @@ def plan(a, b, workers: int):
     return blocks
 
 
-def merge_pairs(a_keys, a_vals, b_keys, b_vals, out_keys=None, out_vals=None):
+def merge_pairs(a_keys, a_vals, b_keys, b_vals, out_keys=None, out_vals=None, workspace=None):
     """Key-value stable merge on the device (uint32 payload moves with its key)."""
     suf = _suffix(a_keys)
     total = _len(a_keys) + _len(b_keys)
@@ -313,9 +331,10 @@ def merge_pairs(a_keys, a_vals, b_keys, b_vals, out_keys=None, out_vals=None):
     _check_out("merge_pairs", a_keys, b_keys, out_keys)
     _check_out("merge_pairs", a_vals, b_vals, out_vals)
     if _is_torch(a_keys) and a_keys.is_cuda:
+        wsp, wsb = _ws(workspace)
         N.check(getattr(N.lib, f"comerge_cuda_merge_pairs_{suf}")(
             _ptr(a_keys), _ptr(a_vals), _len(a_keys), _ptr(b_keys), _ptr(b_vals), _len(b_keys),
-            _ptr(out_keys), _ptr(out_vals), None, 0, _stream(a_keys)))
+            _ptr(out_keys), _ptr(out_vals), wsp, wsb, _stream(a_keys)))
     else:
         rep = N.MergeReport()
         N.check(getattr(N.lib, f"comerge_merge_parallel_pairs_{suf}")(
@@ -324,7 +343,7 @@ def merge_pairs(a_keys, a_vals, b_keys, b_vals, out_keys=None, out_vals=None):
     return out_keys, out_vals
 
 
-def merge_segmented(a, a_off, b, b_off, out=None):
+def merge_segmented(a, a_off, b, b_off, out=None, workspace=None):
     """Merge every pair s (a[a_off[s]:a_off[s+1]], b[b_off[s]:b_off[s+1]]) into
     out[a_off[s]+b_off[s]:...] in one device launch (device tensors)."""
     suf = _suffix(a)
@@ -334,7 +353,8 @@ def merge_segmented(a, a_off, b, b_off, out=None):
     if out is None:
         out = _empty_like_merge(a, _len(a) + _len(b))
     _check_out("merge_segmented", a, b, out)
+    wsp, wsb = _ws(workspace)
     N.check(getattr(N.lib, f"comerge_cuda_merge_segmented_{suf}")(
         _ptr(a), _ptr(a_off), _len(a), _ptr(b), _ptr(b_off), _len(b), max(nseg, 0), _ptr(out),
-        None, 0, _stream(a)))
+        wsp, wsb, _stream(a)))
     return out

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -23,10 +24,10 @@ namespace {
 thread_local std::string g_error;
 thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;
 thread_local int g_path = 0;  // 0 auto, 1 tile (v1), 2 ring streaming (v2), 3 tile pipeline (v3)
-thread_local int g_last_path = 0;
+thread_local int g_last_path = 0;  // kernel of the last merge: 1 tile, 2 ring, 3 pipe, 4 segmented
 thread_local unsigned long long* g_trace = nullptr;  // debug: per-CTA timestamps
-thread_local int g_search_mode = 0;                  // tuning knob (ring kernel search)
-thread_local int g_tune_min_chunk = 0, g_tune_lookahead = 0, g_tune_static_pct = 0;  // kernel family of the last merge: 1, 2, 3 = segmented
+// tuning knobs of the tile pipeline (0 = default)
+thread_local int g_tune_min_chunk = 0, g_tune_lookahead = 0, g_tune_static_pct = 0;
 
 int sm_count() {
     static const int n = [] {
@@ -242,6 +243,17 @@ cudaError_t pool_alloc(void** ptr, size_t bytes, cudaStream_t s) {
     return p ? cudaMallocFromPoolAsync(ptr, bytes, p, s) : cudaMallocAsync(ptr, bytes, s);
 }
 
+// 64-bit launch tag of the pipeline's tail state: unique per launch across
+// every kernel instantiation of the process (never 0).
+std::atomic<uint64_t> g_launches{0x5eed};
+uint64_t next_tail_epoch() {
+    uint64_t x = g_launches.fetch_add(1) + 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    x ^= x >> 31;
+    return x ? x : 1;
+}
+
 // Stream-ordered scratch: caller workspace, or the private pool when ws == NULL.
 struct scratch {
     void* ptr = nullptr;
@@ -277,9 +289,10 @@ size_t merge_ws_bytes(size_t m, size_t n) {
     if (m > SIZE_MAX - n) return 0;
     const uint64_t total = m + n;
     if (total == 0) return 0;
-    // tile kernel: one co-rank per tile boundary; pipeline: a claim counter
+    // tile kernel: one co-rank per tile boundary; pipeline: tail counter + slots
     const size_t tile_ws = round256((div_up(total, tile_cfg<K>::kTile) + 1) * sizeof(uint64_t));
-    return tile_ws > 256 ? tile_ws : 256;
+    const size_t pipe_ws = round256(16 * (3 * size_t(kMaxPipeGrid) + 2));
+    return tile_ws > pipe_ws ? tile_ws : pipe_ws;
 }
 
 template <typename K>
@@ -336,16 +349,6 @@ int merge_device(const K* a, const uint32_t* av, size_t m, const K* b, const uin
         if (limit > kMaxPipeGrid) limit = kMaxPipeGrid;
         const uint32_t grid = uint32_t(ptiles < uint64_t(limit) ? ptiles : uint64_t(limit));
         pipe_args args{};
-        // static share of the tiles (default all); a dynamic tail needs a
-        // zeroed claim counter from the workspace
-        const uint64_t static_pct = g_tune_static_pct > 0 ? uint64_t(g_tune_static_pct) : 100;
-        args.static_tiles = ptiles * (static_pct > 100 ? 100 : static_pct) / 100;
-        scratch sc;
-        if (args.static_tiles < ptiles) {
-            if (int rc = sc.acquire(ws, ws_bytes, 256, s)) return rc;
-            const cudaError_t e = cudaMemsetAsync(sc.ptr, 0, sizeof(unsigned int), s);
-            if (e != cudaSuccess) return cuda_fail(e, "comerge: work counter reset");
-        }
         args.a = a;
         args.av = av;
         args.m = m;
@@ -355,8 +358,18 @@ int merge_device(const K* a, const uint32_t* av, size_t m, const K* b, const uin
         args.out = out;
         args.outv = outv;
         args.ntiles = ptiles;
-        args.work = static_cast<unsigned int*>(sc.ptr);
         args.trace = g_trace;
+        // static weighted split + dynamic tail of ~3 tiles per CTA (<= 15%)
+        uint64_t tail_tiles = 3ull * grid;
+        if (g_tune_static_pct > 0) tail_tiles = ptiles * uint64_t(100 - (g_tune_static_pct > 100 ? 100 : g_tune_static_pct)) / 100;
+        else if (tail_tiles > ptiles * 15 / 100) tail_tiles = ptiles * 15 / 100;
+        args.static_tiles = ptiles - tail_tiles;
+        scratch sc;
+        if (tail_tiles > 0) {
+            if (int rc = sc.acquire(ws, ws_bytes, 16 * (tail_tiles + 2), s)) return rc;
+            args.tail = static_cast<uint64_t*>(sc.ptr);
+            args.epoch = next_tail_epoch();
+        }
         args.min_chunk = g_tune_min_chunk > 0 ? uint32_t(g_tune_min_chunk) : 2u;
         args.lookahead = g_tune_lookahead > 0 ? uint32_t(g_tune_lookahead) : 4u;
         balance().prepare(args, grid, ptiles);

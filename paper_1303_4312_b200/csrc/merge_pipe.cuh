@@ -11,9 +11,10 @@
 //     GPCs) and CTA->SM placement of a persistent grid is deterministic, so
 //     CTA c takes a contiguous static range of tiles proportional to a weight
 //     learned from the per-CTA throughput of earlier launches (reported through
-//     host-mapped memory); an optional dynamic tail is handed out by guided
-//     self-scheduling (chunks of max(MIN, remaining / (2*grid)) tiles claimed
-//     from one global atomic counter).
+//     host-mapped memory).  The last few tiles per CTA form a dynamic tail:
+//     claimed one at a time from a global counter, their co-ranks computed in
+//     the background by a tail warp in every CTA -- this absorbs start-up
+//     jitter and any residual rate mismatch.
 //   * Scheduler warp: claims a chunk only when fewer than LOOKAHEAD tiles are
 //     queued, co-ranks its start (one 33-ary warp search over the whole
 //     diagonal) and then every later boundary of the chunk -- its end included
@@ -47,9 +48,14 @@ struct pipe_cfg<int32_t, false> {
 template <>
 struct pipe_cfg<uint32_t, false> : pipe_cfg<int32_t, false> {};
 // 32-bit keys + payload: tile 3840, 3 stages of ~31 KB.
+#ifndef PIPE_KV32_VT
+#define PIPE_KV32_VT 15
+#define PIPE_KV32_NST 3
+#define PIPE_KV32_MINB 2
+#endif
 template <>
 struct pipe_cfg<int32_t, true> {
-    static constexpr int VT = 15, NST = 3;
+    static constexpr int VT = PIPE_KV32_VT, NST = PIPE_KV32_NST;
 };
 template <>
 struct pipe_cfg<uint32_t, true> : pipe_cfg<int32_t, true> {};
@@ -68,7 +74,7 @@ template <typename K, bool HAS_V>
 struct pipe_layout {
     using C = pipe_cfg<K, HAS_V>;
     static constexpr int kConsumers = 256;
-    static constexpr int kThreads = kConsumers + 64;  // + producer warp + scheduler warp
+    static constexpr int kThreads = kConsumers + 96;  // + producer, scheduler, tail warps
     static constexpr int VT = C::VT;
     static constexpr int T = kConsumers * VT;
     static constexpr int NST = C::NST;
@@ -108,6 +114,8 @@ struct pipe_args {
     uint32_t min_chunk;          // smallest dynamically claimed chunk (tiles)
     uint32_t lookahead;          // claim when fewer tiles than this are queued
     unsigned long long* perf;    // optional: per-CTA {smid, stream ns, tiles, 1} at exit (host-mapped)
+    uint64_t* tail;              // dynamic tail workspace (16B aligned): {tag, count} + slots
+    uint64_t epoch;              // per-launch tag validating tail state (no memset needed)
     uint32_t nweights;           // == gridDim.x when weights are given, else 0 (uniform)
     uint16_t weights[kMaxPipeGrid];  // per-CTA share of the static tiles
 };
@@ -159,6 +167,48 @@ __device__ __forceinline__ uint32_t stage_copy_plan(const E* __restrict__ src, u
     return uint32_t((hi_al - lo_al) * sizeof(E));
 }
 
+// ---- dynamic tail state.  The workspace is not cleared between launches;
+// every word is validated against this launch's 64-bit epoch instead:
+//   tail[0..1] = {tag, count}: reset once per launch by a 128-bit CAS
+//   slot q     = {j, hash(epoch, q, j)} at tail + 2 + 2q (16-byte stores)
+__device__ __forceinline__ uint64_t tail_hash(uint64_t epoch, uint64_t q, uint64_t j) {
+    uint64_t x = epoch ^ (q * 0x9e3779b97f4a7c15ULL) ^ (j + 0x632be59bd9b4e019ULL);
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
+__device__ __forceinline__ void cas128(uint64_t* addr, uint64_t clo, uint64_t chi, uint64_t vlo,
+                                       uint64_t vhi, uint64_t& dlo, uint64_t& dhi) {
+    asm volatile(
+        "{\n .reg .b128 c, v, d;\n mov.b128 c, {%2, %3};\n mov.b128 v, {%4, %5};\n"
+        " atom.global.cas.b128 d, [%6], c, v;\n mov.b128 {%0, %1}, d;\n}\n"
+        : "=l"(dlo), "=l"(dhi)
+        : "l"(clo), "l"(chi), "l"(vlo), "l"(vhi), "l"(addr)
+        : "memory");
+}
+
+__device__ __forceinline__ void st_slot(uint64_t* p, uint64_t j, uint64_t tag) {
+    asm volatile("st.global.relaxed.gpu.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(j), "l"(tag)
+                 : "memory");
+}
+
+__device__ __forceinline__ void ld_slot(const uint64_t* p, uint64_t& j, uint64_t& tag) {
+    asm volatile("ld.global.relaxed.gpu.v2.u64 {%0, %1}, [%2];" : "=l"(j), "=l"(tag) : "l"(p)
+                 : "memory");
+}
+
+// Claim the next tail tile index (0-based) of this launch.
+__device__ __forceinline__ uint64_t tail_claim(uint64_t* tail, uint64_t epoch) {
+    uint64_t tag, cnt;
+    ld_slot(tail, tag, cnt);
+    if (tag != epoch) {
+        uint64_t dt, dc;
+        cas128(tail, tag, cnt, epoch, 0, dt, dc);  // first claimer of this launch resets
+    }
+    return atomicAdd(reinterpret_cast<unsigned long long*>(tail + 1), 1ull);
+}
+
 __device__ __forceinline__ int pow2_group(int k) {  // lanes per group for k searches
     int p = 32;
     while (p > 1 && (32 / p) < k) p >>= 1;
@@ -166,7 +216,16 @@ __device__ __forceinline__ int pow2_group(int k) {  // lanes per group for k sea
 }
 
 template <typename K, bool HAS_V>
-__global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, 2)
+struct pipe_min_blocks {
+    static constexpr int value = 2;
+};
+template <>
+struct pipe_min_blocks<int32_t, true> {
+    static constexpr int value = PIPE_KV32_MINB;
+};
+
+template <typename K, bool HAS_V>
+__global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_blocks<K, HAS_V>::value)
     merge_pipe_kernel(const pipe_args args) {
     using L = pipe_layout<K, HAS_V>;
     constexpr int NC = L::kConsumers;
@@ -273,6 +332,26 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, 2)
     }
     __syncthreads();
     if (args.trace && tid == 0) args.trace[8 * c + 5] = globaltimer_ns();
+    if (warp == 10) {
+        // ------------------------------------------------------ tail warp
+        // co-rank the tail boundaries q = c, c+G, ... (in passes of up to 32,
+        // lane groups, full-diagonal brackets) and publish them
+        const uint64_t nq = NT - NS;  // slots 0 .. nq-1 (boundary NT is trivial)
+        for (uint64_t q0 = c; q0 < nq; q0 += 32 * uint64_t(G)) {
+            uint64_t left = (nq - q0 + G - 1) / G;
+            const int k = int(left < 32 ? left : 32);
+            const int P = pow2_group(k);
+            const int g = lane / P;
+            const uint64_t q = q0 + uint64_t(g < k ? g : k - 1) * G;
+            const uint64_t i = diag_of(NS + q);
+            uint64_t lo, hi;
+            full_bracket(i, lo, hi);
+            const uint64_t j = group_search<K>(i, lo, hi, P, a, b);
+            if (lane % P == 0 && g < k) st_slot(args.tail + 2 + 2 * q, j, tail_hash(args.epoch, q, j));
+        }
+        return;
+    }
+
     if (warp == 9) {
         // ------------------------------------------------------ scheduler
         uint32_t n_rounds = 0, n_claims = 0;
@@ -337,31 +416,37 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, 2)
         };
 
         if (te0 > ts0) run_chunk(ts0, te0, scratch[0], known);
-        // guided self-scheduling of the dynamic region [NS, NT)
-        const uint64_t base = NS;
-        const uint64_t nd = NT - base;
-        for (; nd > 0;) {
-            while (*pushed - *issued >= args.lookahead) __nanosleep(256);
-            uint64_t ts = 0, sz = 0;
-            if (lane == 0) {
-                const uint64_t seen = *reinterpret_cast<volatile unsigned int*>(args.work);
-                const uint64_t rem = nd > seen ? nd - seen : 0;
-                sz = rem / (2 * uint64_t(G));
-                if (sz < args.min_chunk) sz = args.min_chunk;
-                ts = atomicAdd(args.work, unsigned(sz));
+        // dynamic tail [NS, NT): one tile per claim; its boundaries were
+        // co-ranked in the background by the tail warps (slot q = boundary
+        // NS + q), a slot not yet valid is co-ranked here instead.
+        if (NS < NT) {
+            for (;;) {
+                while (*pushed - *issued >= args.lookahead) __nanosleep(128);
+                uint64_t q = 0;
+                if (lane == 0) q = tail_claim(args.tail, args.epoch);
+                q = __shfl_sync(0xffffffffu, q, 0);
+                if (NS + q >= NT) break;
+                ++n_claims;
+                uint64_t jj[2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const uint64_t qq = q + e;
+                    const uint64_t i = diag_of(NS + qq);
+                    uint64_t j = m, tag = 0;
+                    bool ok = NS + qq == NT;  // the last boundary is (m, n)
+                    if (!ok) {
+                        ld_slot(args.tail + 2 + 2 * qq, j, tag);
+                        ok = tag == tail_hash(args.epoch, qq, j);
+                    }
+                    if (!__shfl_sync(0xffffffffu, ok, 0)) {
+                        uint64_t lo, hi;
+                        full_bracket(i, lo, hi);
+                        j = group_search<K>(i, lo, hi, 32, a, b, &n_rounds);
+                    }
+                    jj[e] = __shfl_sync(0xffffffffu, j, 0);
+                }
+                push(NS + q, 1, jj[0], jj[1]);
             }
-            ts = __shfl_sync(0xffffffffu, ts, 0);
-            sz = __shfl_sync(0xffffffffu, sz, 0);
-            if (ts >= nd) break;
-            ts += base;
-            const uint64_t te = ts + sz < NT ? ts + sz : NT;
-            uint64_t lo, hi;
-            full_bracket(diag_of(ts), lo, hi);
-            const unsigned long long t_s = args.trace ? globaltimer_ns() : 0;
-            const uint64_t js = group_search<K>(diag_of(ts), lo, hi, 32, a, b, &n_rounds);
-            if (args.trace) t_search += globaltimer_ns() - t_s;
-            ++n_claims;
-            run_chunk(ts, te, js, 0);
         }
         if (args.trace && lane == 0) {
             args.trace[8 * c + 1] = (uint64_t(n_claims) << 48) | (uint64_t(n_rounds) << 32) |
