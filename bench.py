@@ -51,6 +51,13 @@ CONFIGS = {
     "C5": dict(kind="segmented", dtype="int32", nseg=2**14, maxlen=4096, width=2**20,
                desc="segmented batch: 2^14 pairs, m_s,n_s in [1,4096], int32 keys in [0,2^20)"),
 }
+# diagnostic shapes (not BASELINE configs; run only when named explicitly)
+EXTRA = {
+    "X1": dict(kind="keys", dtype="int32", m=2**26, n=2**26, width=2**31,
+               desc="diagnostic: int32 keys only, m=n=2^26, uniform [0,2^31)"),
+    "X2": dict(kind="pairs", dtype="int32", m=2**26, n=2**26, width=2**31,
+               desc="diagnostic: int32 keys + payload, m=n=2^26, uniform [0,2^31)"),
+}
 HEADLINE = "C2"
 SEED = 5
 
@@ -134,11 +141,12 @@ def run_config(cfg, inp, out=None):
 
 
 KERNEL_NAMES = {1: "merge_tile_kernel (+ partition_kernel)", 2: "merge_stream_kernel",
-                3: "merge_pipe_kernel", 4: "seg_merge_tile_kernel (+ seg_partition_kernel)"}
+                3: "merge_pipe_kernel", 4: "seg_merge_tile_kernel (+ seg_partition_kernel)",
+                5: "merge_pipe_kernel (segmented)"}
 
 
 def launches_per_step(path):
-    return 1 if path in (2, 3) else 2  # persistent kernels: one launch; tile paths: two
+    return 1 if path in (2, 3, 5) else 2  # persistent kernels: one launch; tile paths: two
 
 
 # ------------------------------------------------------------------ clocks

@@ -70,7 +70,7 @@ void comerge_cuda_set_path(int path);
 /* Kernel used by the last merge on this thread: 1 = tile kernel (partition
  * + merge launches), 2 = ring-streaming kernel (one launch), 3 = tile
  * pipeline (one launch), 4 = segmented tile kernel (partition + merge),
- * 0 = none yet. */
+ * 5 = segmented tile pipeline (one launch), 0 = none yet. */
 int comerge_cuda_last_path(void);
 /* Debug tracing of the persistent kernels: when non-NULL, CTA c writes
  * %globaltimer stamps (start, block co-ranked, first tile done, end) to
@@ -78,10 +78,10 @@ int comerge_cuda_last_path(void);
  * disables. */
 void comerge_cuda_set_trace(unsigned long long* device_buffer);
 /* Tuning knobs of the tile pipeline (benchmarking only; 0 = default): the
- * statically assigned share of tiles in percent (default 100), the minimum
- * claimed chunk in tiles (default 2) and the claim look-ahead (queued tiles
- * below which the next chunk is claimed, default 4). */
-void comerge_cuda_set_tuning(int static_pct, int min_chunk, int lookahead);
+ * statically assigned share of tiles in percent (default: all but ~3 tiles per
+ * CTA, at most 15% dynamic), an unused slot, and the claim look-ahead (queued
+ * tiles below which the next tail tile is claimed, default 4). */
+void comerge_cuda_set_tuning(int static_pct, int reserved, int lookahead);
 
 /* ------------------------------------------------------------ workspace */
 

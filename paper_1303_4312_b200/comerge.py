@@ -155,7 +155,8 @@ def set_kernel_path(path: str = "auto") -> None:
     """Select the device kernel for merges issued from this thread: "auto",
     "tile" (partition + one CTA per tile; any alignment), "stream" (ring
     streaming kernel) or "pipe" (persistent tile pipeline; the default for
-    aligned buffers).  "stream" / "pipe" need 16-byte aligned buffers."""
+    aligned buffers, segmented batches included).  "stream" / "pipe" need
+    16-byte aligned buffers."""
     N.lib.comerge_cuda_set_path(KERNEL_PATHS[path])
 
 

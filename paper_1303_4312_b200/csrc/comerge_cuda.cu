@@ -27,7 +27,7 @@ thread_local int g_path = 0;  // 0 auto, 1 tile (v1), 2 ring streaming (v2), 3 t
 thread_local int g_last_path = 0;  // kernel of the last merge: 1 tile, 2 ring, 3 pipe, 4 segmented
 thread_local unsigned long long* g_trace = nullptr;  // debug: per-CTA timestamps
 // tuning knobs of the tile pipeline (0 = default)
-thread_local int g_tune_min_chunk = 0, g_tune_lookahead = 0, g_tune_static_pct = 0;
+thread_local int g_tune_lookahead = 0, g_tune_static_pct = 0;
 
 int sm_count() {
     static const int n = [] {
@@ -144,11 +144,11 @@ balance_state& balance() {
 }
 
 // Persistent grid size for the tile-pipeline kernel (resident CTAs, cached).
-template <typename K, bool HAS_V>
+template <typename K, bool HAS_V, bool SEG>
 int pipe_grid_limit() {
     static const int limit = [] {
-        using L = pipe_layout<K, HAS_V>;
-        auto kern = merge_pipe_kernel<K, HAS_V>;
+        using L = pipe_layout<K, HAS_V, SEG>;
+        auto kern = merge_pipe_kernel<K, HAS_V, SEG>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::kSmem));
         int per_sm = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::kThreads,
@@ -291,14 +291,16 @@ size_t merge_ws_bytes(size_t m, size_t n) {
     if (total == 0) return 0;
     // tile kernel: one co-rank per tile boundary; pipeline: tail counter + slots
     const size_t tile_ws = round256((div_up(total, tile_cfg<K>::kTile) + 1) * sizeof(uint64_t));
-    const size_t pipe_ws = round256(16 * (3 * size_t(kMaxPipeGrid) + 2));
+    const size_t pipe_ws = round256(32 * (3 * size_t(kMaxPipeGrid) + 2));
     return tile_ws > pipe_ws ? tile_ws : pipe_ws;
 }
 
 template <typename K>
 size_t seg_ws_bytes(size_t total) {
     if (total == 0) return 0;
-    return 2 * round256((div_up(total, seg_cfg<K>::kTile) + 1) * sizeof(uint64_t));
+    const size_t tile_ws = 2 * round256((div_up(total, seg_cfg<K>::kTile) + 1) * sizeof(uint64_t));
+    const size_t pipe_ws = round256(32 * (3 * size_t(kMaxPipeGrid) + 2));
+    return tile_ws > pipe_ws ? tile_ws : pipe_ws;
 }
 
 // Common contract of every merge entry (corank.hpp:67-70, merge.hpp:61-66).
@@ -329,6 +331,54 @@ int check_merge_args(const char* who, const K* a, size_t m, const K* b, size_t n
     return COMERGE_OK;
 }
 
+// Launch the persistent tile pipeline (merge_pipe.cuh) for a plain merge or a
+// segmented batch (aoff/boff/nseg).  Scratch: the dynamic-tail state.
+template <typename K, bool HAS_V, bool SEG>
+int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const uint32_t* bv,
+                uint64_t n, K* out, uint32_t* outv, const uint64_t* aoff, const uint64_t* boff,
+                uint64_t nseg, void* ws, size_t ws_bytes, cudaStream_t s) {
+    using PL = pipe_layout<K, HAS_V, SEG>;
+    const uint64_t total = m + n;
+    const uint64_t ptiles = div_up(total, PL::T);
+    int limit = pipe_grid_limit<K, HAS_V, SEG>();
+    if (limit > kMaxPipeGrid) limit = kMaxPipeGrid;
+    const uint32_t grid = uint32_t(ptiles < uint64_t(limit) ? ptiles : uint64_t(limit));
+    pipe_args args{};
+    args.a = a;
+    args.av = av;
+    args.m = m;
+    args.b = b;
+    args.bv = bv;
+    args.n = n;
+    args.out = out;
+    args.outv = outv;
+    args.ntiles = ptiles;
+    args.aoff = aoff;
+    args.boff = boff;
+    args.nseg = nseg;
+    args.trace = g_trace;
+    // static weighted split + dynamic tail of ~3 tiles per CTA (<= 15%)
+    uint64_t tail_tiles = 3ull * grid;
+    if (g_tune_static_pct > 0)
+        tail_tiles = ptiles * uint64_t(100 - (g_tune_static_pct > 100 ? 100 : g_tune_static_pct)) / 100;
+    else if (tail_tiles > ptiles * 15 / 100)
+        tail_tiles = ptiles * 15 / 100;
+    args.static_tiles = ptiles - tail_tiles;
+    scratch sc;
+    if (tail_tiles > 0) {
+        if (int rc = sc.acquire(ws, ws_bytes, 32 * (tail_tiles + 2), s)) return rc;
+        args.tail = static_cast<uint64_t*>(sc.ptr);
+        args.epoch = next_tail_epoch();
+    }
+    args.lookahead = g_tune_lookahead > 0 ? uint32_t(g_tune_lookahead) : 4u;
+    balance().prepare(args, grid, ptiles);
+    g_last_path = SEG ? 5 : 3;
+    mark_before(s);
+    merge_pipe_kernel<K, HAS_V, SEG><<<grid, PL::kThreads, PL::kSmem, s>>>(args);
+    mark_after(s);
+    return check_launch("comerge: pipeline merge launch");
+}
+
 template <typename K, bool HAS_V>
 int merge_device(const K* a, const uint32_t* av, size_t m, const K* b, const uint32_t* bv,
                  size_t n, K* out, uint32_t* outv, void* ws, size_t ws_bytes, cudaStream_t s) {
@@ -344,41 +394,9 @@ int merge_device(const K* a, const uint32_t* av, size_t m, const K* b, const uin
     const uint64_t stiles = div_up(total, SL::T);
     using PL = pipe_layout<K, HAS_V>;
     const uint64_t ptiles = div_up(total, PL::T);
-    if (aligned_all && (g_path == 3 || (g_path == 0 && ptiles >= 16))) {
-        int limit = pipe_grid_limit<K, HAS_V>();
-        if (limit > kMaxPipeGrid) limit = kMaxPipeGrid;
-        const uint32_t grid = uint32_t(ptiles < uint64_t(limit) ? ptiles : uint64_t(limit));
-        pipe_args args{};
-        args.a = a;
-        args.av = av;
-        args.m = m;
-        args.b = b;
-        args.bv = bv;
-        args.n = n;
-        args.out = out;
-        args.outv = outv;
-        args.ntiles = ptiles;
-        args.trace = g_trace;
-        // static weighted split + dynamic tail of ~3 tiles per CTA (<= 15%)
-        uint64_t tail_tiles = 3ull * grid;
-        if (g_tune_static_pct > 0) tail_tiles = ptiles * uint64_t(100 - (g_tune_static_pct > 100 ? 100 : g_tune_static_pct)) / 100;
-        else if (tail_tiles > ptiles * 15 / 100) tail_tiles = ptiles * 15 / 100;
-        args.static_tiles = ptiles - tail_tiles;
-        scratch sc;
-        if (tail_tiles > 0) {
-            if (int rc = sc.acquire(ws, ws_bytes, 16 * (tail_tiles + 2), s)) return rc;
-            args.tail = static_cast<uint64_t*>(sc.ptr);
-            args.epoch = next_tail_epoch();
-        }
-        args.min_chunk = g_tune_min_chunk > 0 ? uint32_t(g_tune_min_chunk) : 2u;
-        args.lookahead = g_tune_lookahead > 0 ? uint32_t(g_tune_lookahead) : 4u;
-        balance().prepare(args, grid, ptiles);
-        g_last_path = 3;
-        mark_before(s);
-        merge_pipe_kernel<K, HAS_V><<<grid, PL::kThreads, PL::kSmem, s>>>(args);
-        mark_after(s);
-        return check_launch("comerge: pipeline merge launch");
-    }
+    if (aligned_all && (g_path == 3 || (g_path == 0 && ptiles >= 16)))
+        return launch_pipe<K, HAS_V, false>(a, av, m, b, bv, n, out, outv, nullptr, nullptr, 0, ws,
+                                            ws_bytes, s);
     if (aligned_all && g_path == 2) {
         const int limit = stream_grid_limit<K, HAS_V>();
         const unsigned grid = unsigned(stiles < uint64_t(limit) ? stiles : uint64_t(limit));
@@ -426,6 +444,11 @@ int merge_segmented_device(const K* a, const uint64_t* a_off, size_t m, const K*
         return rc;
     const uint64_t total = m + n;
     if (total == 0) return COMERGE_OK;
+    using PL = pipe_layout<K, false>;
+    if (aligned16(a) && aligned16(b) && aligned16(out) && g_path != 1 &&
+        (g_path == 3 || div_up(total, PL::T) >= 16))
+        return launch_pipe<K, false, true>(a, nullptr, m, b, nullptr, n, out, nullptr, a_off, b_off,
+                                           nseg, ws, ws_bytes, s);
     constexpr int T = seg_cfg<K>::kTile;
     const uint64_t ntiles = div_up(total, T);
     const uint64_t nbound = ntiles + 1;
@@ -693,9 +716,8 @@ const char* comerge_cuda_last_error(void) { return g_error.c_str(); }
 void comerge_cuda_set_path(int path) { g_path = path; }
 int comerge_cuda_last_path(void) { return g_last_path; }
 void comerge_cuda_set_trace(unsigned long long* device_buffer) { g_trace = device_buffer; }
-void comerge_cuda_set_tuning(int static_pct, int min_chunk, int lookahead) {
+void comerge_cuda_set_tuning(int static_pct, int /*reserved*/, int lookahead) {
     g_tune_static_pct = static_pct;
-    g_tune_min_chunk = min_chunk;
     g_tune_lookahead = lookahead;
 }
 

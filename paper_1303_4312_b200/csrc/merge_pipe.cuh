@@ -31,6 +31,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 
 #include "corank.cuh"
 #include "merge_stream.cuh"
@@ -38,12 +39,20 @@
 
 namespace comerge_b200 {
 
+#ifndef PIPE_K32_NC
+#define PIPE_K32_NC 256
+#define PIPE_K32_VT 15
+#define PIPE_K32_NST 6
+#endif
+#ifndef PIPE_KV32_NC
+#define PIPE_KV32_NC 256
+#endif
 template <typename K, bool HAS_V>
 struct pipe_cfg;
 // 32-bit keys only: tile 3840, 6 stages of ~15.5 KB.
 template <>
 struct pipe_cfg<int32_t, false> {
-    static constexpr int VT = 15, NST = 6;
+    static constexpr int NC = PIPE_K32_NC, VT = PIPE_K32_VT, NST = PIPE_K32_NST;
 };
 template <>
 struct pipe_cfg<uint32_t, false> : pipe_cfg<int32_t, false> {};
@@ -55,42 +64,46 @@ struct pipe_cfg<uint32_t, false> : pipe_cfg<int32_t, false> {};
 #endif
 template <>
 struct pipe_cfg<int32_t, true> {
-    static constexpr int VT = PIPE_KV32_VT, NST = PIPE_KV32_NST;
+    static constexpr int NC = PIPE_KV32_NC, VT = PIPE_KV32_VT, NST = PIPE_KV32_NST;
 };
 template <>
 struct pipe_cfg<uint32_t, true> : pipe_cfg<int32_t, true> {};
 // 64-bit keys only: tile 2816, 4 stages of ~23 KB.
 template <>
 struct pipe_cfg<uint64_t, false> {
-    static constexpr int VT = 11, NST = 4;
+    static constexpr int NC = 256, VT = 11, NST = 4;
 };
 // 64-bit keys + payload: tile 2816, 3 stages of ~34 KB.
 template <>
 struct pipe_cfg<uint64_t, true> {
-    static constexpr int VT = 11, NST = 3;
+    static constexpr int NC = 256, VT = 11, NST = 3;
 };
 
-template <typename K, bool HAS_V>
+template <typename K, bool HAS_V, bool SEG = false>
 struct pipe_layout {
     using C = pipe_cfg<K, HAS_V>;
-    static constexpr int kConsumers = 256;
+    static constexpr int kConsumers = C::NC;
     static constexpr int kThreads = kConsumers + 96;  // + producer, scheduler, tail warps
+    static constexpr int kCW = kConsumers / 32;       // consumer warps (roles follow them)
     static constexpr int VT = C::VT;
     static constexpr int T = kConsumers * VT;
     static constexpr int NST = C::NST;
     static constexpr int VECE = 16 / sizeof(K);
     static constexpr int NB = 64;  // tile-descriptor ring entries
     static_assert((T * sizeof(K)) % 16 == 0 && T % 4 == 0, "tile must be 16B multiple");
-    static constexpr int KW = ((T + 4 * VECE + VT + 2) + VECE - 1) / VECE * VECE;
+    static constexpr int KW = ((T + 4 * VECE + VT + 3) + VECE - 1) / VECE * VECE;
     static constexpr int VW = HAS_V ? ((T + 16 + VT + 2) + 3) / 4 * 4 : 0;
     static constexpr size_t kStageKeys = (size_t(KW) * sizeof(K) + 127) / 128 * 128;
     static constexpr size_t kStageVals = (size_t(VW) * 4 + 127) / 128 * 128;
-    static constexpr size_t kStage = kStageKeys + kStageVals;
+    // segmented batches: the tile's segment offsets {aoff, boff}[s0 .. s0+SEGCAP)
+    static constexpr int SEGCAP = 128;
+    static constexpr size_t kStageOffs = SEG ? size_t(2 * SEGCAP) * 8 : 0;
+    static constexpr size_t kStage = kStageKeys + kStageVals + kStageOffs;
     static constexpr size_t oStages = 0;
     static constexpr size_t oBars = oStages + NST * kStage;
-    static constexpr size_t oMeta = oBars + size_t(2 * NST) * 8;  // NST x 4 x u64
-    static constexpr size_t oDesc = oMeta + size_t(NST) * 32;      // NB x {i0, j0, j1, i1}
-    static constexpr size_t oScratch = oDesc + size_t(NB) * 32;    // 40 x u64
+    static constexpr size_t oMeta = oBars + size_t(2 * NST) * 8;  // NST x 8 x u64
+    static constexpr size_t oDesc = oMeta + size_t(NST) * 64;      // NB x {i0,j0,j1,i1,s0,s1,-,-}
+    static constexpr size_t oScratch = oDesc + size_t(NB) * 64;    // 40 x u64
     static constexpr size_t oMisc = oScratch + 40 * 8;
     static constexpr size_t kMisc = 64;
     static constexpr size_t kSmem = oMisc + kMisc;
@@ -108,11 +121,12 @@ struct pipe_args {
     void* out;
     uint32_t* outv;
     uint64_t ntiles;
-    unsigned int* work;          // chunk-claim counter, zero at launch
+    const uint64_t* aoff;        // segmented batches: nseg+1 offsets into a (else NULL)
+    const uint64_t* boff;        // segmented batches: nseg+1 offsets into b
+    uint64_t nseg;
     unsigned long long* trace;   // optional per-CTA timestamps (8 x u64 per CTA)
     uint64_t static_tiles;       // tiles [0, static_tiles) are split statically by weight
-    uint32_t min_chunk;          // smallest dynamically claimed chunk (tiles)
-    uint32_t lookahead;          // claim when fewer tiles than this are queued
+    uint32_t lookahead;          // claim a tail tile when fewer than this are queued
     unsigned long long* perf;    // optional: per-CTA {smid, stream ns, tiles, 1} at exit (host-mapped)
     uint64_t* tail;              // dynamic tail workspace (16B aligned): {tag, count} + slots
     uint64_t epoch;              // per-launch tag validating tail state (no memset needed)
@@ -120,15 +134,13 @@ struct pipe_args {
     uint16_t weights[kMaxPipeGrid];  // per-CTA share of the static tiles
 };
 
-// Lane-group (P+1)-ary search: the warp is split into 32/P groups of P lanes
-// (P a power of two); every group searches its own diagonal i for the
-// Lemma-1 split inside its bracket [lo, hi] (guard 1 of corank.hpp:93-94 is
-// the monotone predicate).  All 32 lanes must call it.
-template <typename K>
-__device__ __forceinline__ uint64_t group_search(uint64_t i, uint64_t lo, uint64_t hi, int P,
-                                                 const K* __restrict__ a,
-                                                 const K* __restrict__ b,
-                                                 uint32_t* rounds = nullptr) {
+// Lane-group (P+1)-ary search for the largest q in [lo, hi] with !pred(q),
+// given !pred(lo) and pred monotone (false ... false true ... true).  The
+// warp is split into 32/P groups of P lanes (P a power of two); every group
+// has its own bracket and predicate arguments.  All 32 lanes must call it.
+template <typename Pred>
+__device__ __forceinline__ uint64_t group_search_pred(uint64_t lo, uint64_t hi, int P, Pred pred,
+                                                      uint32_t* rounds) {
     const int lane = threadIdx.x & 31;
     const int g = lane / P, r = lane % P;
     const unsigned gmask = P == 32 ? 0xffffffffu : ((1u << P) - 1u) << (g * P);
@@ -138,7 +150,7 @@ __device__ __forceinline__ uint64_t group_search(uint64_t i, uint64_t lo, uint64
         const uint64_t width = hi - lo;
         const uint64_t q = lo + ((uint64_t(r) + 1) * width + P) / P1;  // in (lo, hi]
         bool not_far = true;
-        if (active) not_far = !(ldg_elem(b + (i - q)) < ldg_elem(a + (q - 1)));
+        if (active) not_far = !pred(q);
         const int nfalse = __popc(__ballot_sync(0xffffffffu, not_far) & gmask);
         if (active) {
             const int f = nfalse - 1;
@@ -150,6 +162,18 @@ __device__ __forceinline__ uint64_t group_search(uint64_t i, uint64_t lo, uint64
         if (rounds) ++*rounds;
     }
     return lo;
+}
+
+// Lemma-1 split of diagonal i of (a, b) inside [lo, hi] (guard 1 of
+// corank.hpp:93-94 is the monotone predicate).
+template <typename K>
+__device__ __forceinline__ uint64_t group_search(uint64_t i, uint64_t lo, uint64_t hi, int P,
+                                                 const K* __restrict__ a,
+                                                 const K* __restrict__ b,
+                                                 uint32_t* rounds = nullptr) {
+    return group_search_pred(
+        lo, hi, P, [=](uint64_t q) { return ldg_elem(b + (i - q)) < ldg_elem(a + (q - 1)); },
+        rounds);
 }
 
 // Stage src[lo, hi) for a TMA copy whose destination `dst` corresponds to
@@ -167,12 +191,55 @@ __device__ __forceinline__ uint32_t stage_copy_plan(const E* __restrict__ src, u
     return uint32_t((hi_al - lo_al) * sizeof(E));
 }
 
+__device__ __forceinline__ uint64_t ldg_u64(const uint64_t* p) {
+    return static_cast<uint64_t>(__ldg(reinterpret_cast<const unsigned long long*>(p)));
+}
+
+// A tile boundary: co-rank j of output rank i and, for segmented batches, the
+// segment s that holds it (largest s with aoff[s] + boff[s] <= i).
+struct boundary {
+    uint64_t j;
+    uint64_t s;
+};
+
+// Boundary search for the lane's group: i with j in [jlo, jhi] and, when SEG,
+// s >= slo.  Segmented: the segment by a lane-group search over the
+// (L2-resident) offsets, then the co-rank inside that segment (the batch is
+// one merge over (segment, key) composites, so the split of a rank inside
+// segment s is s's own co-rank).
+template <typename K, bool SEG>
+__device__ __forceinline__ boundary find_boundary(const pipe_args& args, uint64_t i, uint64_t jlo,
+                                                  uint64_t jhi, uint64_t slo, int P,
+                                                  uint32_t* rounds) {
+    const K* __restrict__ a = static_cast<const K*>(args.a);
+    const K* __restrict__ b = static_cast<const K*>(args.b);
+    if constexpr (!SEG) {
+        return {group_search<K>(i, jlo, jhi, P, a, b, rounds), 0};
+    } else {
+        const uint64_t* __restrict__ ao = args.aoff;
+        const uint64_t* __restrict__ bo = args.boff;
+        const uint64_t s = group_search_pred(
+            slo, args.nseg - 1, P,
+            [=](uint64_t q) { return ldg_u64(ao + q) + ldg_u64(bo + q) > i; }, rounds);
+        const uint64_t as = ldg_u64(ao + s), bs = ldg_u64(bo + s);
+        const uint64_t ma = ldg_u64(ao + s + 1) - as, nb = ldg_u64(bo + s + 1) - bs;
+        const uint64_t li = i - as - bs;  // <= ma + nb
+        uint64_t lo = li > nb ? li - nb : 0, hi = li < ma ? li : ma;
+        if (jlo > as && jlo - as > lo) lo = jlo - as;
+        if (jhi < as + hi) hi = jhi > as ? jhi - as : 0;
+        if (hi < lo) hi = lo;
+        return {as + group_search<K>(li, lo, hi, P, a + as, b + bs, rounds), s};
+    }
+}
+
 // ---- dynamic tail state.  The workspace is not cleared between launches;
 // every word is validated against this launch's 64-bit epoch instead:
-//   tail[0..1] = {tag, count}: reset once per launch by a 128-bit CAS
-//   slot q     = {j, hash(epoch, q, j)} at tail + 2 + 2q (16-byte stores)
-__device__ __forceinline__ uint64_t tail_hash(uint64_t epoch, uint64_t q, uint64_t j) {
-    uint64_t x = epoch ^ (q * 0x9e3779b97f4a7c15ULL) ^ (j + 0x632be59bd9b4e019ULL);
+//   tail[0..1]     = {tag, count}: reset once per launch by a 128-bit CAS
+//   slot q (32 B)  = {j, s, hash(epoch, q, j, s), 0} at tail + 4 + 4q
+__device__ __forceinline__ uint64_t tail_hash(uint64_t epoch, uint64_t q, uint64_t j,
+                                              uint64_t s) {
+    uint64_t x = epoch ^ (q * 0x9e3779b97f4a7c15ULL) ^ (j + 0x632be59bd9b4e019ULL) ^
+                 (s * 0xd1b54a32d192ed03ULL);
     x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
     x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
     return x ^ (x >> 31);
@@ -188,20 +255,20 @@ __device__ __forceinline__ void cas128(uint64_t* addr, uint64_t clo, uint64_t ch
         : "memory");
 }
 
-__device__ __forceinline__ void st_slot(uint64_t* p, uint64_t j, uint64_t tag) {
-    asm volatile("st.global.relaxed.gpu.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(j), "l"(tag)
+__device__ __forceinline__ void st_pair(uint64_t* p, uint64_t x, uint64_t y) {
+    asm volatile("st.global.relaxed.gpu.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(x), "l"(y)
                  : "memory");
 }
 
-__device__ __forceinline__ void ld_slot(const uint64_t* p, uint64_t& j, uint64_t& tag) {
-    asm volatile("ld.global.relaxed.gpu.v2.u64 {%0, %1}, [%2];" : "=l"(j), "=l"(tag) : "l"(p)
+__device__ __forceinline__ void ld_pair(const uint64_t* p, uint64_t& x, uint64_t& y) {
+    asm volatile("ld.global.relaxed.gpu.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "l"(p)
                  : "memory");
 }
 
 // Claim the next tail tile index (0-based) of this launch.
 __device__ __forceinline__ uint64_t tail_claim(uint64_t* tail, uint64_t epoch) {
     uint64_t tag, cnt;
-    ld_slot(tail, tag, cnt);
+    ld_pair(tail, tag, cnt);
     if (tag != epoch) {
         uint64_t dt, dc;
         cas128(tail, tag, cnt, epoch, 0, dt, dc);  // first claimer of this launch resets
@@ -224,16 +291,99 @@ struct pipe_min_blocks<int32_t, true> {
     static constexpr int value = PIPE_KV32_MINB;
 };
 
-template <typename K, bool HAS_V>
+// Segmented consumer merge: VT outputs from window diagonal `diag` of a tile
+// whose windows hold A[j0, j0+a_len) and B[k0, k0+b_len) of a batch of
+// independent pairs; s_lo..s_hi bound the segments the tile touches.
+// Segment offsets of a tile: staged in shared memory when the tile touches
+// few segments (so = first staged index), else read from global memory.
+struct seg_offsets {
+    const uint64_t* ao;  // aoff (global) or its staged copy (shared)
+    const uint64_t* bo;
+    uint64_t base;       // index of ao[0] / bo[0]
+    bool shared;
+    __device__ __forceinline__ uint64_t a(uint64_t s) const {
+        return shared ? ao[s - base] : ldg_u64(ao + s);
+    }
+    __device__ __forceinline__ uint64_t b(uint64_t s) const {
+        return shared ? bo[s - base] : ldg_u64(bo + s);
+    }
+};
+
+// Segmented consumer merge: VT outputs from window diagonal `diag` of a tile
+// whose windows hold A[j0, j0+a_len) and B[k0, k0+b_len) of a batch of
+// independent pairs; s_lo..s_hi bound the segments the tile touches.
+template <typename K, int VT>
+__device__ __forceinline__ void merge_thread_seg(const K* sA, int a_len, const K* sB, int b_len,
+                                                 int diag, uint64_t i0, uint64_t j0, uint64_t k0,
+                                                 uint64_t s_lo, uint64_t s_hi,
+                                                 const seg_offsets& off, K (&keys)[VT]) {
+    // segment holding output rank i0 + diag
+    const uint64_t gi = i0 + uint64_t(diag);
+    uint64_t lo = s_lo, hi = s_hi;
+    while (lo < hi) {
+        const uint64_t mid = lo + (hi - lo + 1) / 2;
+        if (off.a(mid) + off.b(mid) <= gi)
+            lo = mid;
+        else
+            hi = mid - 1;
+    }
+    uint64_t s = lo;
+    // the segment's part of the windows (window-relative [x0, x1) / [y0, y1))
+    auto seg_span = [&](uint64_t sg, int& x0, int& x1, int& y0, int& y1) {
+        const uint64_t as = off.a(sg), ae = off.a(sg + 1);
+        const uint64_t bs = off.b(sg), be = off.b(sg + 1);
+        x0 = as > j0 ? int(as - j0) : 0;
+        x1 = ae > j0 ? int(ae - j0 < uint64_t(a_len) ? ae - j0 : uint64_t(a_len)) : 0;
+        y0 = bs > k0 ? int(bs - k0) : 0;
+        y1 = be > k0 ? int(be - k0 < uint64_t(b_len) ? be - k0 : uint64_t(b_len)) : 0;
+    };
+    int x0, x1, y0, y1;
+    seg_span(s, x0, x1, y0, y1);
+    // split of the diagonal inside the segment (plain key order there)
+    const int dl = diag - x0 - y0;
+    const int na = x1 - x0, nb = y1 - y0;
+    int l = dl > nb ? dl - nb : 0, h = dl < na ? dl : na;
+    while (l < h) {
+        const int mid = (l + h + 1) >> 1;
+        if (sB[y0 + dl - mid] < sA[x0 + mid - 1])
+            h = mid - 1;
+        else
+            l = mid;
+    }
+    int ia = x0 + l, ib = y0 + dl - l;
+    K ka = sA[ia], kb = sB[ib];
+    K ka1 = sA[ia + 1], kb1 = sB[ib + 1];  // look-ahead (see merge_thread)
+#pragma unroll
+    for (int v = 0; v < VT; ++v) {
+        while (ia >= x1 && ib >= y1 && s < s_hi) {  // segment done: next one
+            ++s;
+            seg_span(s, x0, x1, y0, y1);
+        }
+        const bool take_b = ib < y1 && (ia >= x1 || kb < ka);
+        keys[v] = take_b ? kb : ka;
+        if (take_b) {
+            ++ib;
+            kb = kb1;
+            kb1 = sB[ib + 1];
+        } else {
+            ++ia;
+            ka = ka1;
+            ka1 = sA[ia + 1];
+        }
+    }
+}
+
+template <typename K, bool HAS_V, bool SEG>
 __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_blocks<K, HAS_V>::value)
     merge_pipe_kernel(const pipe_args args) {
-    using L = pipe_layout<K, HAS_V>;
+    using L = pipe_layout<K, HAS_V, SEG>;
     constexpr int NC = L::kConsumers;
     constexpr int VT = L::VT;
     constexpr int T = L::T;
     constexpr int NST = L::NST;
     constexpr int VECE = L::VECE;
     constexpr int NB = L::NB;
+    static_assert(!(SEG && HAS_V), "segmented batches are keys-only");
 
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::oBars);
@@ -261,6 +411,15 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         lo = i > n ? i - n : 0;
         hi = i < m ? i : m;
     };
+    // bracket of boundary i from a known boundary (ic, jc) below it: at least
+    // jc and at most jc + (i - ic) elements come from A
+    auto step_bracket = [=](uint64_t i, uint64_t ic, uint64_t jc, uint64_t& lo, uint64_t& hi) {
+        lo = jc;
+        if (i > n && i - n > lo) lo = i - n;
+        hi = jc + (i - ic);
+        if (i < hi) hi = i;
+        if (m < hi) hi = m;
+    };
 
     const unsigned long long t_start = globaltimer_ns();
     if (args.trace && tid == 0) {
@@ -282,8 +441,11 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
     // tiles, proportional to its weight (weights learned from the throughput
     // of earlier launches; any weights give a valid partition), then co-rank
     // its start with one warp (33-ary; few concurrent probes keep rounds short).
+    // scratch: [0..8] j of boundaries ts0..ts0+8, [10..18] their segments,
+    // [33] ts0, [34] te0
     uint64_t ts0 = 0, te0 = 0;
-    if (warp == 9) {
+    constexpr int W_PROD = L::kCW, W_SCHED = L::kCW + 1, W_TAIL = L::kCW + 2;
+    if (warp == W_SCHED) {
         uint64_t below = 0, all = 0;
         if (args.nweights == G) {
             for (uint32_t x = lane; x < G; x += 32) {
@@ -307,8 +469,11 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         if (te0 > ts0) {
             uint64_t lo, hi;
             full_bracket(diag_of(ts0), lo, hi);
-            const uint64_t j = group_search<K>(diag_of(ts0), lo, hi, 32, a, b);
-            if (lane == 0) scratch[0] = j;
+            const boundary bd = find_boundary<K, SEG>(args, diag_of(ts0), lo, hi, 0, 32, nullptr);
+            if (lane == 0) {
+                scratch[0] = bd.j;
+                scratch[10] = bd.s;
+            }
         }
     }
     __syncthreads();
@@ -321,18 +486,19 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         known = te0 - ts0 - 1 < 8 ? int(te0 - ts0 - 1) : 8;
         if (warp < known) {
             const uint64_t t = ts0 + 1 + warp;
-            const uint64_t i = diag_of(t), i0 = diag_of(ts0), j0 = scratch[0];
-            uint64_t lo = j0, hi = j0 + (i - i0);
-            if (i > n && i - n > lo) lo = i - n;
-            if (i < hi) hi = i;
-            if (m < hi) hi = m;
-            const uint64_t j = group_search<K>(i, lo, hi, 32, a, b);
-            if (lane == 0) scratch[1 + warp] = j;
+            uint64_t lo, hi;
+            step_bracket(diag_of(t), diag_of(ts0), scratch[0], lo, hi);
+            const boundary bd = find_boundary<K, SEG>(args, diag_of(t), lo, hi, scratch[10], 32,
+                                                      nullptr);
+            if (lane == 0) {
+                scratch[1 + warp] = bd.j;
+                scratch[11 + warp] = bd.s;
+            }
         }
     }
     __syncthreads();
     if (args.trace && tid == 0) args.trace[8 * c + 5] = globaltimer_ns();
-    if (warp == 10) {
+    if (warp == W_TAIL) {
         // ------------------------------------------------------ tail warp
         // co-rank the tail boundaries q = c, c+G, ... (in passes of up to 32,
         // lane groups, full-diagonal brackets) and publish them
@@ -346,27 +512,33 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             const uint64_t i = diag_of(NS + q);
             uint64_t lo, hi;
             full_bracket(i, lo, hi);
-            const uint64_t j = group_search<K>(i, lo, hi, P, a, b);
-            if (lane % P == 0 && g < k) st_slot(args.tail + 2 + 2 * q, j, tail_hash(args.epoch, q, j));
+            const boundary bd = find_boundary<K, SEG>(args, i, lo, hi, 0, P, nullptr);
+            if (lane % P == 0 && g < k) {
+                uint64_t* slot = args.tail + 4 + 4 * q;
+                st_pair(slot, bd.j, bd.s);
+                st_pair(slot + 2, tail_hash(args.epoch, q, bd.j, bd.s), 0);
+            }
         }
         return;
     }
 
-    if (warp == 9) {
+    if (warp == W_SCHED) {
         // ------------------------------------------------------ scheduler
         uint32_t n_rounds = 0, n_claims = 0;
         unsigned long long t_search = 0;
-        // push tile descriptors for tiles [t, t+k): lane g supplies tile t+g's
-        // boundary splits (j0, j1); waits for ring space.
-        auto push = [&](uint64_t t, int k, uint64_t j0, uint64_t j1) {
+        // push descriptors {i0, j0, j1, i1, s0, s1} for tiles [t, t+k): lane g
+        // supplies tile t+g's boundaries; waits for ring space.
+        auto push = [&](uint64_t t, int k, boundary b0, boundary b1) {
             const uint32_t p = *pushed;
-            while (p + uint32_t(k) > *issued + NB) __nanosleep(128);
+            while (p + uint32_t(k) > *issued + NB) __nanosleep(1000);  // far ahead: no hurry
             if (lane < k) {
-                uint64_t* d = desc + 4 * ((p + lane) % NB);
+                uint64_t* d = desc + 8 * ((p + lane) % NB);
                 d[0] = diag_of(t + lane);
-                d[1] = j0;
-                d[2] = j1;
+                d[1] = b0.j;
+                d[2] = b1.j;
                 d[3] = diag_of(t + lane + 1);
+                d[4] = b0.s;
+                d[5] = b1.s;
             }
             __syncwarp();
             if (lane == 0) {
@@ -375,19 +547,27 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             }
             __syncwarp();
         };
-        // co-rank and push every tile of chunk [ts, te) given its start split
-        // js.  Each pass co-ranks the next k boundaries (k = 1, 4, 8, then 32:
-        // the first tiles are ready fast, later passes amortise latency) in
-        // 32/k lane groups, every one bracketed by the last known boundary:
-        // at least j_c and at most j_c + (i - i_c) elements come from A.
-        auto run_chunk = [&](uint64_t ts, uint64_t te, uint64_t js, int known_inner) {
-            uint64_t cur = ts, jc = js;
-            if (known_inner > 0) {  // boundaries ts+1 .. ts+known_inner are in scratch[1..]
+        auto shfl_b = [](boundary x, int src) {
+            return boundary{__shfl_sync(0xffffffffu, x.j, src), __shfl_sync(0xffffffffu, x.s, src)};
+        };
+        auto shfl_up_b = [](boundary x) {
+            return boundary{__shfl_up_sync(0xffffffffu, x.j, 1),
+                            __shfl_up_sync(0xffffffffu, x.s, 1)};
+        };
+        // co-rank and push every tile of chunk [ts, te) given its start
+        // boundary bs.  Each pass co-ranks the next k boundaries (k = 1, 4, 8,
+        // then 32: the first tiles are ready fast, later passes amortise
+        // latency) in 32/k lane groups, each bracketed by the last known one.
+        auto run_chunk = [&](uint64_t ts, uint64_t te, boundary bs, int known_inner) {
+            uint64_t cur = ts;
+            boundary bc = bs;
+            if (known_inner > 0) {  // boundaries ts+1 .. ts+known_inner are in scratch
                 const int k = known_inner;
-                const uint64_t jb = scratch[1 + (lane < k ? lane : k - 1)];
-                const uint64_t jprev = __shfl_up_sync(0xffffffffu, jb, 1);
-                push(cur, k, lane == 0 ? jc : jprev, jb);
-                jc = __shfl_sync(0xffffffffu, jb, k - 1);
+                const int x = lane < k ? lane : k - 1;
+                const boundary bb{scratch[1 + x], scratch[11 + x]};
+                const boundary bp = shfl_up_b(bb);
+                push(cur, k, lane == 0 ? bc : bp, bb);
+                bc = shfl_b(bb, k - 1);
                 cur += uint64_t(k);
             }
             int cap = known_inner > 0 ? 32 : 1;
@@ -398,24 +578,21 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
                 const int g = lane / P;
                 const uint64_t tb = cur + 1 + uint64_t(g < k ? g : k - 1);
                 const uint64_t i = diag_of(tb);
-                const uint64_t ic = diag_of(cur);
-                uint64_t lo = jc, hi = jc + (i - ic);
-                if (i > n && i - n > lo) lo = i - n;
-                if (i < hi) hi = i;
-                if (m < hi) hi = m;
+                uint64_t lo, hi;
+                step_bracket(i, diag_of(cur), bc.j, lo, hi);
                 const unsigned long long t_s = args.trace ? globaltimer_ns() : 0;
-                const uint64_t j = group_search<K>(i, lo, hi, P, a, b, &n_rounds);
+                const boundary bd = find_boundary<K, SEG>(args, i, lo, hi, bc.s, P, &n_rounds);
                 if (args.trace) t_search += globaltimer_ns() - t_s;
                 // lane g <- boundary cur + 1 + g (the result of group g)
-                const uint64_t jb = __shfl_sync(0xffffffffu, j, (lane < k ? lane : k - 1) * P);
-                const uint64_t jprev = __shfl_up_sync(0xffffffffu, jb, 1);
-                push(cur, k, lane == 0 ? jc : jprev, jb);
-                jc = __shfl_sync(0xffffffffu, jb, k - 1);
+                const boundary bb = shfl_b(bd, (lane < k ? lane : k - 1) * P);
+                const boundary bp = shfl_up_b(bb);
+                push(cur, k, lane == 0 ? bc : bp, bb);
+                bc = shfl_b(bb, k - 1);
                 cur += uint64_t(k);
             }
         };
 
-        if (te0 > ts0) run_chunk(ts0, te0, scratch[0], known);
+        if (te0 > ts0) run_chunk(ts0, te0, boundary{scratch[0], scratch[10]}, known);
         // dynamic tail [NS, NT): one tile per claim; its boundaries were
         // co-ranked in the background by the tail warps (slot q = boundary
         // NS + q), a slot not yet valid is co-ranked here instead.
@@ -427,25 +604,28 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
                 q = __shfl_sync(0xffffffffu, q, 0);
                 if (NS + q >= NT) break;
                 ++n_claims;
-                uint64_t jj[2];
+                boundary bb[2];
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const uint64_t qq = q + e;
                     const uint64_t i = diag_of(NS + qq);
-                    uint64_t j = m, tag = 0;
-                    bool ok = NS + qq == NT;  // the last boundary is (m, n)
+                    boundary bd{m, SEG ? args.nseg - 1 : 0};  // the last boundary is (m, n)
+                    bool ok = NS + qq == NT;
                     if (!ok) {
-                        ld_slot(args.tail + 2 + 2 * qq, j, tag);
-                        ok = tag == tail_hash(args.epoch, qq, j);
+                        const uint64_t* slot = args.tail + 4 + 4 * qq;
+                        uint64_t tag, pad;
+                        ld_pair(slot, bd.j, bd.s);
+                        ld_pair(slot + 2, tag, pad);
+                        ok = tag == tail_hash(args.epoch, qq, bd.j, bd.s);
                     }
                     if (!__shfl_sync(0xffffffffu, ok, 0)) {
                         uint64_t lo, hi;
                         full_bracket(i, lo, hi);
-                        j = group_search<K>(i, lo, hi, 32, a, b, &n_rounds);
+                        bd = find_boundary<K, SEG>(args, i, lo, hi, 0, 32, &n_rounds);
                     }
-                    jj[e] = __shfl_sync(0xffffffffu, j, 0);
+                    bb[e] = shfl_b(bd, 0);
                 }
-                push(NS + q, 1, jj[0], jj[1]);
+                push(NS + q, 1, bb[0], bb[1]);
             }
         }
         if (args.trace && lane == 0) {
@@ -457,7 +637,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             const uint32_t p = *pushed;
             while (p + 1 > *issued + NB) __nanosleep(128);
             if (lane == 0) {
-                desc[4 * (p % NB)] = ~uint64_t(0);
+                desc[8 * (p % NB)] = ~uint64_t(0);
                 __threadfence_block();
                 *pushed = p + 1;
             }
@@ -465,7 +645,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         return;
     }
 
-    if (warp == 8) {
+    if (warp == W_PROD) {
         // ------------------------------------------------------ producer
         if (lane != 0) return;
         const uint64_t policy = policy_evict_first();
@@ -479,17 +659,32 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
                 if (args.trace) starve += globaltimer_ns() - w0;
             }
             __threadfence_block();
-            const uint64_t* d = desc + 4 * (s % NB);
+            const uint64_t* d = desc + 8 * (s % NB);
             const uint64_t i0 = d[0];
-            uint64_t* mt = meta + 4 * st;
+            uint64_t* mt = meta + 8 * st;
             if (i0 == ~uint64_t(0)) {
                 mt[3] = uint64_t(1) << 63;  // done
                 mbar_arrive(&full[st]);
                 if (args.trace) args.trace[8 * c + 6] = starve;
                 break;
             }
-            const uint64_t j0 = d[1], j1 = d[2], i1 = d[3];
+            // copy the whole descriptor out before its ring slot is released
+            const uint64_t j0 = d[1], j1 = d[2], i1 = d[3], seg0 = d[4], seg1 = d[5];
+            __threadfence_block();
             *issued = s + 1;
+#ifdef COMERGE_DEBUG_CHECKS
+            if (!(j0 <= j1 && i0 <= i1 && i1 - i0 <= uint64_t(T) && i0 >= j0 && i1 >= j1 &&
+                  i1 - j1 >= i0 - j0 && j1 <= m && i1 - j1 <= n && seg0 <= seg1 &&
+                  (!SEG || seg1 < args.nseg))) {
+                printf("comerge: bad tile descriptor cta %u s %u: i0 %llu i1 %llu j0 %llu j1 %llu "
+                       "s0 %llu s1 %llu\n", c, s, (unsigned long long)i0, (unsigned long long)i1,
+                       (unsigned long long)j0, (unsigned long long)j1,
+                       (unsigned long long)seg0, (unsigned long long)seg1);
+                __trap();
+            }
+#endif
+            mt[4] = seg0;
+            mt[5] = seg1;
             const uint64_t k0 = i0 - j0, k1 = i1 - j1;
             const uint32_t a_len = uint32_t(j1 - j0), b_len = uint32_t(k1 - k0);
             unsigned char* stage = smem + L::oStages + size_t(st) * L::kStage;
@@ -512,7 +707,25 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             mt[2] = (uint64_t(a_len) << 32) | b_len;
             mt[3] = (uint64_t(a_off) << 48) | (uint64_t(b_base) << 24) | (uint64_t(b_off) << 8) |
                     uint64_t(av_off);
-            mbar_arrive_expect_tx(&full[st], ab + bb + avb + bvb);
+            uint32_t ob = 0;
+            if constexpr (SEG) {
+                // the tile's segment offsets s0 .. s1+1 (16-byte aligned superset)
+                const uint64_t olo = seg0 - (seg0 & 1), ohi = seg1 + 2;
+                uint64_t* so = reinterpret_cast<uint64_t*>(stage + L::kStageKeys + L::kStageVals);
+                if (ohi - olo + 1 <= uint64_t(L::SEGCAP)) {
+                    const uint32_t oa = stage_copy_plan(args.aoff, args.nseg + 1, olo, ohi, so, 2);
+                    const uint32_t obb =
+                        stage_copy_plan(args.boff, args.nseg + 1, olo, ohi, so + L::SEGCAP, 2);
+                    ob = oa + obb;
+                    mt[6] = olo + 1;  // staged (0 = read from global)
+                    mbar_arrive_expect_tx(&full[st], ab + bb + ob);
+                    if (oa) tma_load_1d(so, args.aoff + olo, oa, &full[st], policy);
+                    if (obb) tma_load_1d(so + L::SEGCAP, args.boff + olo, obb, &full[st], policy);
+                } else {
+                    mt[6] = 0;
+                }
+            }
+            if (ob == 0) mbar_arrive_expect_tx(&full[st], ab + bb + avb + bvb);
             if (ab) tma_load_1d(sk, a + (j0 - j0 % VECE), ab, &full[st], policy);
             if (bb) tma_load_1d(sk + b_base, b + (k0 - k0 % VECE), bb, &full[st], policy);
             if constexpr (HAS_V) {
@@ -539,7 +752,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         }
         mbar_wait(&full[st], uint32_t((s / NST) & 1));
         if (s == 0) t_stream = globaltimer_ns();
-        const uint64_t* mt = meta + 4 * st;
+        const uint64_t* mt = meta + 8 * st;
         const uint64_t packed = mt[3];
         if (packed >> 63) {
             s_done = s;
@@ -558,7 +771,22 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         const int diag = min(tid * VT, len);
         K keys[VT];
         uint32_t src[VT];
-        merge_thread<K, VT, HAS_V>(sk + a_off, a_len, sk + b_base + b_off, b_len, diag, keys, src);
+        if constexpr (SEG) {
+            const uint64_t k0 = mt[1];
+            seg_offsets off;
+            if (mt[6]) {
+                const uint64_t* so =
+                    reinterpret_cast<const uint64_t*>(stage + L::kStageKeys + L::kStageVals);
+                off = seg_offsets{so, so + L::SEGCAP, mt[6] - 1, true};
+            } else {
+                off = seg_offsets{args.aoff, args.boff, 0, false};
+            }
+            merge_thread_seg<K, VT>(sk + a_off, a_len, sk + b_base + b_off, b_len, diag, i0,
+                                    i0 - k0, k0, mt[4], mt[5], off, keys);
+        } else {
+            merge_thread<K, VT, HAS_V>(sk + a_off, a_len, sk + b_base + b_off, b_len, diag, keys,
+                                       src);
+        }
         if constexpr (HAS_V) {
             const int bv_base = (av_off + a_len + 3) / 4 * 4;
             const int bv_off = int(mt[1] & 3);

@@ -113,8 +113,11 @@ __device__ __forceinline__ void merge_thread(const KC* sA, int a_len, const KC* 
     const int ia0 = co_rank_split<KC, int>(diag, sA, a_len, sB, b_len,
                                            [](const KC* p) { return *p; });
     int ia = ia0, ib = diag - ia0;
-    KC ka = sA[ia];
-    KC kb = sB[ib];
+    // one-element look-ahead on both sides: the shared-memory load for the
+    // next step is already in flight, so each step waits on compare/select
+    // only (reads may touch the window slack past a_len / b_len, never used)
+    KC ka = sA[ia], kb = sB[ib];
+    KC ka1 = sA[ia + 1], kb1 = sB[ib + 1];
 #pragma unroll
     for (int v = 0; v < VT; ++v) {
         const bool take_b = ib < b_len && (ia >= a_len || kb < ka);
@@ -122,10 +125,12 @@ __device__ __forceinline__ void merge_thread(const KC* sA, int a_len, const KC* 
         if constexpr (TRACK) src[v] = take_b ? (uint32_t(ib) | 0x80000000u) : uint32_t(ia);
         if (take_b) {
             ++ib;
-            kb = sB[ib];
+            kb = kb1;
+            kb1 = sB[ib + 1];
         } else {
             ++ia;
-            ka = sA[ia];
+            ka = ka1;
+            ka1 = sA[ia + 1];
         }
     }
 }
@@ -155,7 +160,7 @@ __global__ void __launch_bounds__(tile_cfg<K>::kThreads)
     constexpr int VT = tile_cfg<K>::kVT;
     constexpr int T = tile_cfg<K>::kTile;
     constexpr int VEC = 16 / sizeof(K);
-    constexpr int WIN = ((T + 4 * VEC + VT + 2) + VEC - 1) / VEC * VEC;
+    constexpr int WIN = ((T + 4 * VEC + VT + 3) + VEC - 1) / VEC * VEC;
     constexpr int WINV = HAS_V ? ((T + 16 + VT + 2) + 3) / 4 * 4 : 4;
     __shared__ __align__(16) K s_keys[WIN];
     __shared__ __align__(16) uint32_t s_vals[WINV];

@@ -159,7 +159,7 @@ def test_golden_key_value(cuda, path, golden):
         assert np.array_equal(hk, c["outk"]) and np.array_equal(hv, c["outv"]), name
 
 
-def test_golden_segmented(cuda, golden):
+def test_golden_segmented(cuda, path, golden):
     for name, c in _cases(golden, "seg"):
         out = P().merge_segmented(dev(c["a"], cuda), dev(c["aoff"], cuda), dev(c["b"], cuda),
                                   dev(c["boff"], cuda))
@@ -230,13 +230,17 @@ def test_misaligned_views(cuda, path, port, dt):
         assert np.array_equal(host(vo), port.merge(a, b)), (shift_a, shift_b, shift_o)
 
 
-def test_random_segmented(cuda, port):
+def test_random_segmented(cuda, path, port):
     rng = np.random.default_rng(99)
     for dt in (np.int32, np.uint32):
-        for nseg, maxlen in [(1, 10000), (3000, 8), (500, 600), (64, 4096)]:
+        for nseg, maxlen in [(1, 10000), (3000, 8), (500, 600), (64, 4096), (7, 30000)]:
             ma = rng.integers(0, maxlen + 1, nseg)
             nb = rng.integers(0, maxlen + 1, nseg)
             ma[rng.integers(0, nseg, nseg // 4)] = 0
+            nb[rng.integers(0, nseg, nseg // 5)] = 0
+            both = rng.integers(0, nseg, nseg // 10)
+            ma[both] = 0
+            nb[both] = 0
             a = np.concatenate([_draw(rng, dt, int(x), 100) for x in ma] + [np.empty(0, dt)])
             b = np.concatenate([_draw(rng, dt, int(x), 100) for x in nb] + [np.empty(0, dt)])
             ao = np.concatenate([[0], np.cumsum(ma)]).astype(np.uint64)

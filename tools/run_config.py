@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--lookahead", type=int, default=0)
     args = ap.parse_args()
     dev = torch.device("cuda:0")
+    bench.CONFIGS.update(bench.EXTRA)
     inp = bench.make_inputs(args.config, device=dev)
     out = bench.alloc_outputs(args.config, inp)
     P.set_kernel_path(args.path)
