@@ -72,6 +72,12 @@ void comerge_cuda_set_path(int path);
  * pipeline (one launch), 4 = segmented tile kernel (partition + merge),
  * 5 = segmented tile pipeline (one launch), 0 = none yet. */
 int comerge_cuda_last_path(void);
+/* Host-buffer strategy of the synchronous entry points on this thread
+ * (testing / benchmarking): 0 = chunked pipeline (default: output chunks
+ * co-ranked on the host, H2D / device merge / D2H overlapped on three
+ * streams), 1 = zero-copy for pinned host memory (the kernel reads and writes
+ * host memory over PCIe), 2 = plain staging (copy in, merge, copy out). */
+void comerge_cuda_set_host_mode(int mode);
 /* Debug tracing of the persistent kernels: when non-NULL, CTA c writes
  * %globaltimer stamps (start, block co-ranked, first tile done, end) to
  * device_buffer[8c .. 8c+3] and its SM id to device_buffer[8c+4].  NULL

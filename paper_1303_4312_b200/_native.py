@@ -65,6 +65,8 @@ def _load():
     lib.comerge_cuda_set_path.argtypes = [_i]
     lib.comerge_cuda_set_path.restype = None
     lib.comerge_cuda_last_path.restype = _i
+    lib.comerge_cuda_set_host_mode.argtypes = [_i]
+    lib.comerge_cuda_set_host_mode.restype = None
     lib.comerge_cuda_set_trace.argtypes = [_p]
     lib.comerge_cuda_set_trace.restype = None
     lib.comerge_cuda_set_tuning.argtypes = [_i, _i, _i]

@@ -6,8 +6,10 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <chrono>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -28,6 +30,7 @@ thread_local int g_last_path = 0;  // kernel of the last merge: 1 tile, 2 ring, 
 thread_local unsigned long long* g_trace = nullptr;  // debug: per-CTA timestamps
 // tuning knobs of the tile pipeline (0 = default)
 thread_local int g_tune_lookahead = 0, g_tune_static_pct = 0;
+thread_local int g_host_mode = 0;  // host buffers: 0 chunked pipeline, 1 zero-copy, 2 plain staging
 
 int sm_count() {
     static const int n = [] {
@@ -497,6 +500,18 @@ bool is_device_ptr(const void* p) {
     return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
 }
 
+// Pinned (page-locked) host memory: device-addressable under UVA, so kernels
+// can read and write it directly over PCIe.
+bool is_pinned_host(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return attr.type == cudaMemoryTypeHost && attr.devicePointer == p;
+}
+
 cudaStream_t sync_stream() {
     thread_local cudaStream_t s = [] {
         cudaStream_t st = nullptr;
@@ -576,6 +591,114 @@ struct event_pair {
     }
 };
 
+// ---------------------------------------------------------------- host pipeline
+//
+// Host buffers: the output is cut into chunks whose input windows are found by
+// co-ranking the chunk boundaries on the host (Algorithm 2 at the host level,
+// each chunk is an independent stable merge of its two
+// windows), and each chunk goes H2D -> merge on the device -> D2H on three
+// streams, so host->device and device->host traffic overlap (PCIe is full
+// duplex) while the device merges.  Nothing is merged on the host.
+struct host_streams {
+    cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+    cudaEvent_t in_done[3], merged[3], out_done[3];
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    host_streams() {
+        cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&comp, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking);
+        for (int i = 0; i < 3; ++i) {
+            cudaEventCreateWithFlags(&in_done[i], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&merged[i], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&out_done[i], cudaEventDisableTiming);
+        }
+        cudaEventCreate(&t0);
+        cudaEventCreate(&t1);
+    }
+};
+
+host_streams& hstreams() {
+    thread_local host_streams hs;
+    return hs;
+}
+
+template <typename K, bool HAS_V>
+int merge_host_pipeline(const K* a, const uint32_t* av, uint64_t m, const K* b,
+                        const uint32_t* bv, uint64_t n, K* out, uint32_t* outv, uint64_t* h2d,
+                        uint64_t* d2h, uint64_t* merge_ns) {
+    host_streams& hs = hstreams();
+    const uint64_t total = m + n;
+    static const uint64_t parts = [] {
+        const char* e = std::getenv("COMERGE_HOST_CHUNKS");  // tuning knob (benchmarking)
+        const long v = e ? std::atol(e) : 0;
+        return uint64_t(v > 0 ? v : 8);
+    }();
+    const uint64_t chunk = total / parts > (uint64_t(1) << 18) ? total / parts : (uint64_t(1) << 18);
+    const uint64_t nchunks = div_up(total, chunk);
+    // chunk boundaries: the Lemma-1 split of every chunk start, on host data
+    std::vector<uint64_t> js(nchunks + 1);
+    for (uint64_t c = 0; c <= nchunks; ++c) {
+        const uint64_t i = c * chunk < total ? c * chunk : total;
+        js[c] = co_rank_split<K, uint64_t>(i, a, m, b, n, [](const K* p) { return *p; });
+    }
+    // three slots of device windows (A, B, out [+ payloads]) from the pool
+    const size_t kb = chunk * sizeof(K), vb = HAS_V ? chunk * 4 : 0;
+    const size_t slot_bytes = round256(kb) * 3 + round256(vb) * 3;
+    void* buf = nullptr;
+    cudaError_t e = pool_alloc(&buf, 3 * slot_bytes, hs.comp);
+    if (e != cudaSuccess) return cuda_fail(e, "comerge: host pipeline staging");
+    cudaEventRecord(hs.in_done[0], hs.comp);  // allocation visible to the copy streams
+    cudaStreamWaitEvent(hs.h2d, hs.in_done[0], 0);
+    int rc = COMERGE_OK;
+    bool first = true;
+    for (uint64_t c = 0; c < nchunks && rc == COMERGE_OK; ++c) {
+        const int sl = int(c % 3);
+        unsigned char* base = static_cast<unsigned char*>(buf) + sl * slot_bytes;
+        K* dA = reinterpret_cast<K*>(base);
+        K* dB = reinterpret_cast<K*>(base + round256(kb));
+        K* dO = reinterpret_cast<K*>(base + 2 * round256(kb));
+        uint32_t* dAv = reinterpret_cast<uint32_t*>(base + 3 * round256(kb));
+        uint32_t* dBv = dAv + round256(vb) / 4;
+        uint32_t* dOv = dBv + round256(vb) / 4;
+        const uint64_t i0 = c * chunk, i1 = i0 + chunk < total ? i0 + chunk : total;
+        const uint64_t j0 = js[c], j1 = js[c + 1], k0 = i0 - j0, k1 = i1 - j1;
+        if (c >= 3) cudaStreamWaitEvent(hs.h2d, hs.out_done[sl], 0);  // slot free again
+        if (j1 > j0) cudaMemcpyAsync(dA, a + j0, (j1 - j0) * sizeof(K), cudaMemcpyHostToDevice, hs.h2d);
+        if (k1 > k0) cudaMemcpyAsync(dB, b + k0, (k1 - k0) * sizeof(K), cudaMemcpyHostToDevice, hs.h2d);
+        if (HAS_V) {
+            if (j1 > j0) cudaMemcpyAsync(dAv, av + j0, (j1 - j0) * 4, cudaMemcpyHostToDevice, hs.h2d);
+            if (k1 > k0) cudaMemcpyAsync(dBv, bv + k0, (k1 - k0) * 4, cudaMemcpyHostToDevice, hs.h2d);
+        }
+        *h2d += (i1 - i0) * (sizeof(K) + (HAS_V ? 4 : 0));
+        cudaEventRecord(hs.in_done[sl], hs.h2d);
+        cudaStreamWaitEvent(hs.comp, hs.in_done[sl], 0);
+        if (first) {
+            cudaEventRecord(hs.t0, hs.comp);
+            first = false;
+        }
+        rc = merge_device<K, HAS_V>(dA, HAS_V ? dAv : nullptr, j1 - j0, dB, HAS_V ? dBv : nullptr,
+                                    k1 - k0, dO, HAS_V ? dOv : nullptr, nullptr, 0, hs.comp);
+        cudaEventRecord(hs.merged[sl], hs.comp);
+        cudaStreamWaitEvent(hs.d2h, hs.merged[sl], 0);
+        cudaMemcpyAsync(out + i0, dO, (i1 - i0) * sizeof(K), cudaMemcpyDeviceToHost, hs.d2h);
+        if (HAS_V) cudaMemcpyAsync(outv + i0, dOv, (i1 - i0) * 4, cudaMemcpyDeviceToHost, hs.d2h);
+        *d2h += (i1 - i0) * (sizeof(K) + (HAS_V ? 4 : 0));
+        cudaEventRecord(hs.out_done[sl], hs.d2h);
+    }
+    cudaEventRecord(hs.t1, hs.comp);
+    cudaEventRecord(hs.in_done[0], hs.d2h);  // free the staging after the last copy-out
+    cudaStreamWaitEvent(hs.comp, hs.in_done[0], 0);
+    cudaFreeAsync(buf, hs.comp);
+    e = cudaStreamSynchronize(hs.d2h);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(hs.comp);
+    if (e != cudaSuccess) return cuda_fail(e, "comerge: host pipeline");
+    if (rc) return rc;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, hs.t0, hs.t1);
+    *merge_ns = uint64_t(double(ms) * 1e6);
+    return COMERGE_OK;
+}
+
 template <typename K, bool HAS_V>
 int merge_parallel_sync(const K* a, const uint32_t* av, size_t m, const K* b, const uint32_t* bv,
                         size_t n, K* out, uint32_t* outv, size_t out_len, size_t workers,
@@ -593,6 +716,96 @@ int merge_parallel_sync(const K* a, const uint32_t* av, size_t m, const K* b, co
     if (workers == 0)
         return fail(COMERGE_E_INVALID, "merge_parallel: worker count must be positive");
     const uint64_t total = m + n;
+    // opt-in zero-copy for pinned host (or device) buffers: the merge kernel
+    // loads its tile windows from and stores its tiles to host memory over
+    // PCIe (measured ~36 GB/s per direction on B200 PCIe Gen5 x16, below the
+    // copy engines' ~50, so the chunked pipeline below is the default)
+    auto pinned_or_dev = [](const void* p, size_t bytes) {
+        return bytes == 0 || is_pinned_host(p) || is_device_ptr(p);
+    };
+    const bool any_host = !is_device_ptr(a) || !is_device_ptr(b) || !is_device_ptr(out);
+    if (total >= (uint64_t(1) << 20) && any_host && g_host_mode == 1 &&
+        pinned_or_dev(a, m * sizeof(K)) && pinned_or_dev(b, n * sizeof(K)) &&
+        pinned_or_dev(out, total * sizeof(K)) &&
+        (!HAS_V || (pinned_or_dev(av, m * 4) && pinned_or_dev(bv, n * 4) &&
+                    pinned_or_dev(outv, total * 4)))) {
+        cudaStream_t s = sync_stream();
+        event_pair e2e;
+        cudaEventRecord(e2e.a, s);
+        if (int rc = merge_device<K, HAS_V>(a, av, m, b, bv, n, out, outv, nullptr, 0, s)) return rc;
+        cudaEventRecord(e2e.b, s);
+        const cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return cuda_fail(e, "comerge: zero-copy merge");
+        std::vector<uint64_t> ranks(workers + 1);
+        for (size_t r = 0; r <= workers; ++r) partition_output_impl(total, workers, r, &ranks[r]);
+        if (block_sizes)
+            for (size_t r = 0; r < workers; ++r) block_sizes[r] = ranks[r + 1] - ranks[r];
+        if (corank_iterations) {
+            for (size_t r = 0; r <= workers; ++r) {
+                corank_stats st{};
+                co_rank_alg1(ranks[r], a, m, b, n, [](const K* p) { return *p; }, &st);
+                if (synced) {
+                    if (r < workers) corank_iterations[r] = st.iterations;
+                } else {
+                    if (r < workers) corank_iterations[2 * r] = st.iterations;
+                    if (r > 0) corank_iterations[2 * r - 1] = st.iterations;
+                }
+            }
+        }
+        if (rep) {
+            const uint64_t eb = sizeof(K) + (HAS_V ? 4 : 0);
+            rep->m = m;
+            rep->n = n;
+            rep->workers = workers;
+            rep->wall_ns = e2e.ns();
+            rep->e2e_ns = e2e.ns();
+            rep->h2d_bytes = (is_device_ptr(a) ? 0 : m * eb) + (is_device_ptr(b) ? 0 : n * eb);
+            rep->d2h_bytes = is_device_ptr(out) ? 0 : total * eb;
+            rep->tiles = div_up(total, pipe_layout<K, HAS_V>::T);
+        }
+        return COMERGE_OK;
+    }
+    // all-host buffers: chunked, overlapped H2D / merge / D2H pipeline
+    const bool all_host = total >= (uint64_t(1) << 20) && g_host_mode == 0 && !is_device_ptr(a) && !is_device_ptr(b) &&
+                          !is_device_ptr(out) &&
+                          (!HAS_V || (!is_device_ptr(av) && !is_device_ptr(bv) && !is_device_ptr(outv)));
+    if (all_host && (m == 0 || a) && (n == 0 || b) && (!HAS_V || ((m == 0 || av) && (n == 0 || bv) && outv))) {
+        const auto w0 = std::chrono::steady_clock::now();
+        uint64_t h2d = 0, d2h = 0, merge_ns = 0;
+        if (int rc = merge_host_pipeline<K, HAS_V>(a, av, m, b, bv, n, out, outv, &h2d, &d2h,
+                                                   &merge_ns))
+            return rc;
+        const auto w1 = std::chrono::steady_clock::now();
+        std::vector<uint64_t> ranks(workers + 1);
+        for (size_t r = 0; r <= workers; ++r) partition_output_impl(total, workers, r, &ranks[r]);
+        if (block_sizes)
+            for (size_t r = 0; r < workers; ++r) block_sizes[r] = ranks[r + 1] - ranks[r];
+        if (corank_iterations) {
+            // the reference's co_rank_stats of every block boundary (parallel.hpp:273-275),
+            // Algorithm 1 over the host-resident inputs (report bookkeeping only)
+            for (size_t r = 0; r <= workers; ++r) {
+                corank_stats st{};
+                co_rank_alg1(ranks[r], a, m, b, n, [](const K* p) { return *p; }, &st);
+                if (synced) {
+                    if (r < workers) corank_iterations[r] = st.iterations;
+                } else {
+                    if (r < workers) corank_iterations[2 * r] = st.iterations;
+                    if (r > 0) corank_iterations[2 * r - 1] = st.iterations;
+                }
+            }
+        }
+        if (rep) {
+            rep->m = m;
+            rep->n = n;
+            rep->workers = workers;
+            rep->wall_ns = merge_ns;
+            rep->e2e_ns = uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(w1 - w0).count());
+            rep->h2d_bytes = h2d;
+            rep->d2h_bytes = d2h;
+            rep->tiles = div_up(total, pipe_layout<K, HAS_V>::T);
+        }
+        return COMERGE_OK;
+    }
     cudaStream_t s = sync_stream();
     event_pair e2e, dev;
     uint64_t h2d = 0, d2h = 0;
@@ -714,6 +927,7 @@ extern "C" {
 const char* comerge_cuda_last_error(void) { return g_error.c_str(); }
 
 void comerge_cuda_set_path(int path) { g_path = path; }
+void comerge_cuda_set_host_mode(int mode) { g_host_mode = mode; }
 int comerge_cuda_last_path(void) { return g_last_path; }
 void comerge_cuda_set_trace(unsigned long long* device_buffer) { g_trace = device_buffer; }
 void comerge_cuda_set_tuning(int static_pct, int /*reserved*/, int lookahead) {

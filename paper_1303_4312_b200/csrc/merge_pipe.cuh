@@ -41,15 +41,16 @@ namespace comerge_b200 {
 
 #ifndef PIPE_K32_NC
 #define PIPE_K32_NC 256
-#define PIPE_K32_VT 15
-#define PIPE_K32_NST 6
+#define PIPE_K32_VT 31
+#define PIPE_K32_NST 3
 #endif
 #ifndef PIPE_KV32_NC
 #define PIPE_KV32_NC 256
 #endif
 template <typename K, bool HAS_V>
 struct pipe_cfg;
-// 32-bit keys only: tile 3840, 6 stages of ~15.5 KB.
+// 32-bit keys only: tile 7936, 3 stages of ~31 KB (VT=31 halves the per-output
+// cost of the tile-local split search, which dominates keys-only merges).
 template <>
 struct pipe_cfg<int32_t, false> {
     static constexpr int NC = PIPE_K32_NC, VT = PIPE_K32_VT, NST = PIPE_K32_NST;

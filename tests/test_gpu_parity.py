@@ -187,7 +187,8 @@ def _draw(rng, dt, size, alphabet):
     return np.sort(v.astype(dt))
 
 
-TILES = {np.int32: 256 * 15, np.uint32: 256 * 15, np.uint64: 256 * 11}
+# tile sizes of the pipeline (keys-only) and tile kernels: shapes straddle both
+TILES = {np.int32: 256 * 31, np.uint32: 256 * 15, np.uint64: 256 * 11}
 
 
 @pytest.mark.parametrize("dt", [np.int32, np.uint32, np.uint64])
@@ -340,3 +341,54 @@ def test_baseline_config_full_size(cuda, port, cfg):
             window = host(hk[lo:int(i)])
             pref = np.sort(np.concatenate([ha[max(0, j - 64):j], hb[max(0, k - 64):k]]))
             assert np.array_equal(window, pref[len(pref) - len(window):])
+
+
+def test_host_buffers_pipelined(cuda, port):
+    """Host inputs >= 1M elements take the chunked H2D/merge/D2H pipeline
+    (host co-ranks of the chunk boundaries); pinned and pageable buffers."""
+    rng = np.random.default_rng(77)
+    for dt, (m, n), alphabet in [(np.int32, (1_500_000, 2_100_000), 1000),
+                                 (np.uint64, (3_000_001, 17), 0), (np.int32, (2_000_000, 0), 5)]:
+        a, b = _draw(rng, dt, m, alphabet), _draw(rng, dt, n, alphabet)
+        expect = port.merge(a, b)
+        out = np.zeros(m + n, dt)
+        rep = P().merge_parallel(a, b, out, 7)
+        assert np.array_equal(out, expect)
+        assert rep.h2d_bytes == (m + n) * out.itemsize and rep.d2h_bytes == (m + n) * out.itemsize
+        ra = P().merge_parallel(a, b, out, 7)  # repeatable
+        assert np.array_equal(out, expect) and ra.block_sizes == rep.block_sizes
+        # pinned host memory
+        tdt = TDT[np.dtype(dt)]
+        pa = torch.from_numpy(a).pin_memory()
+        pb = torch.from_numpy(b).pin_memory()
+        po = torch.zeros(m + n, dtype=tdt).pin_memory()
+        P().merge_parallel(pa.numpy(), pb.numpy(), po.numpy(), 3)
+        assert np.array_equal(po.numpy(), expect)
+        from paper_1303_4312_b200 import _native as N
+        for mode in (1, 2):  # zero-copy, plain staging
+            N.lib.comerge_cuda_set_host_mode(mode)
+            try:
+                po.zero_()
+                P().merge_parallel(pa.numpy(), pb.numpy(), po.numpy(), 3)
+                assert np.array_equal(po.numpy(), expect), mode
+            finally:
+                N.lib.comerge_cuda_set_host_mode(0)
+        av, bv = tagged(m, n)
+        ek, ev = port.merge(a, b, av, bv)
+        ok, ov = np.empty_like(ek), np.empty_like(ev)
+        P().merge_pairs(a, av, b, bv, ok, ov)
+        assert np.array_equal(ok, ek) and np.array_equal(ov, ev)
+
+
+def test_host_pipeline_report_matches_reference_stats(cuda, port):
+    """merge_report.corank_iterations of the host pipeline = Algorithm 1's."""
+    rng = np.random.default_rng(5)
+    a, b = _draw(rng, np.uint64, 1_200_000, 64), _draw(rng, np.uint64, 900_000, 64)
+    out = np.empty(len(a) + len(b), np.uint64)
+    rep = P().merge_parallel(a, b, out, 5)
+    total = len(a) + len(b)
+    bounds = [port.partition_output(total, 5, r) for r in range(6)]
+    its = [port.co_rank(i, a, b, stats=True)[1][0] for i in bounds]
+    assert rep.corank_iterations == [x for r in range(5) for x in (its[r], its[r + 1])]
+    rep_s = P().merge_parallel_synced(a, b, out, 5)
+    assert rep_s.corank_iterations == its[:5]
