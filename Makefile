@@ -11,7 +11,15 @@ SRCS := $(PKG)/csrc/comerge_cuda.cu $(PKG)/csrc/testkit.cu
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/comerge_cuda.h include/comerge_cuda_testkit.h
 OBJS := $(patsubst $(PKG)/csrc/%.cu,$(PKG)/lib/%.o,$(SRCS))
 
-all: $(LIB) oracle
+SHIM_TEST := tests/cpp/shim_test
+
+all: $(LIB) oracle $(SHIM_TEST)
+
+# C++ drop-in shim test (include/comerge/cuda.hpp over the C ABI)
+$(SHIM_TEST): tests/cpp/shim_test.cpp include/comerge/cuda.hpp include/comerge_cuda.h $(LIB)
+	g++ -std=c++20 -O2 -Wall -Wextra -Iinclude -I/usr/local/cuda/include -o $@ $< \
+	    -L$(PKG)/lib -lcomerge_cuda -L/usr/local/cuda/lib64 -lcudart \
+	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)/lib' -Wl,-rpath,/usr/local/cuda/lib64
 
 $(PKG)/lib/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	@mkdir -p $(PKG)/lib
@@ -24,7 +32,7 @@ oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -f $(PKG)/lib/*.o $(PKG)/lib/*.so $(PKG)/lib/*.ptxas.txt
+	rm -f $(PKG)/lib/*.o $(PKG)/lib/*.so $(PKG)/lib/*.ptxas.txt $(SHIM_TEST)
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean

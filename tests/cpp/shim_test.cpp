@@ -1,0 +1,185 @@
+// shim_test.cpp -- the reference's own unit-test cases (corank_test.cpp,
+// merge_test.cpp, parallel_test.cpp; /root/reference/proj/tests), replayed
+// against the B200 drop-in comerge::cuda (include/comerge/cuda.hpp), plus
+// seeded sweeps checked against a naive two-finger merge (test-only oracle,
+// written as plainly as the reference's oracle.hpp:98-119).
+//
+// Exit code = number of failed checks.  Needs a GPU (run by tests/test_cpp_shim.py).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <functional>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "comerge/cuda.hpp"
+
+namespace cm = comerge::cuda;
+
+static int g_fail = 0;
+#define CHECK(cond)                                                            \
+    do {                                                                       \
+        if (!(cond)) {                                                         \
+            ++g_fail;                                                          \
+            std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+        }                                                                      \
+    } while (0)
+
+template <typename Ex, typename Fn>
+static bool throws_with(Fn&& fn, const char* needle) {
+    try {
+        fn();
+    } catch (const Ex& e) {
+        return std::string(e.what()).find(needle) != std::string::npos;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+template <typename K>
+static std::vector<K> naive_merge(const std::vector<K>& a, const std::vector<K>& b) {
+    std::vector<K> out;
+    std::size_t x = 0, y = 0;
+    while (x < a.size() && y < b.size()) out.push_back(a[x] <= b[y] ? a[x++] : b[y++]);
+    while (x < a.size()) out.push_back(a[x++]);
+    while (y < b.size()) out.push_back(b[y++]);
+    return out;
+}
+
+using keys = std::vector<std::uint64_t>;
+
+static void kats() {
+    // corank_test.cpp:22-56
+    cm::co_rank_stats st;
+    CHECK((cm::co_rank(0, keys{1, 3, 5, 7}, keys{2, 4, 6, 8}, {}, &st) == cm::co_ranks{0, 0}));
+    CHECK(st.iterations == 0 && st.comparisons == 0);
+    CHECK((cm::co_rank(8, keys{1, 3, 5, 7}, keys{2, 4, 6, 8}, {}, &st) == cm::co_ranks{4, 4}));
+    CHECK(st.iterations == 0 && st.comparisons == 0);
+    CHECK((cm::co_rank(0, keys{}, keys{}) == cm::co_ranks{0, 0}));
+    CHECK((cm::co_rank(4, keys{1, 3, 5, 7}, keys{2, 4, 6, 8}) == cm::co_ranks{2, 2}));
+    CHECK((cm::co_rank(2, keys{2, 2}, keys{2, 2}) == cm::co_ranks{2, 0}));
+    CHECK((cm::co_rank(3, keys{10, 20}, keys{1, 2, 3, 4, 5}) == cm::co_ranks{0, 3}));
+    CHECK((cm::co_rank(1, keys{1}, keys{2}) == cm::co_ranks{1, 0}));
+    for (std::size_t i = 0; i <= 3; ++i) {
+        CHECK((cm::co_rank(i, keys{5, 6, 7}, keys{}, {}, &st) == cm::co_ranks{i, 0}));
+        CHECK(st.comparisons == 0);
+        CHECK((cm::co_rank(i, keys{}, keys{5, 6, 7}, {}, &st) == cm::co_ranks{0, i}));
+    }
+    // corank_test.cpp:58-63
+    CHECK(throws_with<std::out_of_range>([] { cm::co_rank(4, keys{1, 2}, keys{3}); },
+                                         "rank out of range"));
+    CHECK(throws_with<std::out_of_range>([] { cm::co_rank(100, keys{1, 2}, keys{3}); },
+                                         "rank out of range"));
+    // merge_test.cpp:17-35, :53-70
+    keys out(2);
+    cm::stable_merge(keys{}, keys{1, 2}, out);
+    CHECK((out == keys{1, 2}));
+    keys out4(4);
+    cm::stable_merge(keys{1, 3}, keys{2, 3}, out4);
+    CHECK((out4 == keys{1, 2, 3, 3}));
+    CHECK(throws_with<std::invalid_argument>(
+        [] {
+            keys small(2);
+            cm::stable_merge(keys{1, 2}, keys{3}, small);
+        },
+        "output length must equal |a| + |b|"));
+    // stability through payloads (merge_test.cpp:37-51)
+    {
+        const std::vector<std::uint32_t> ak{5, 5}, bk{5};
+        const std::vector<std::uint32_t> av{0, 1}, bv{0x80000000u};
+        std::vector<std::uint32_t> ok(3), ov(3);
+        cm::merge_parallel_pairs(ak, av, bk, bv, ok, std::span<std::uint32_t>(ov));
+        CHECK((ov == std::vector<std::uint32_t>{0, 1, 0x80000000u}));
+    }
+    // parallel_test.cpp:28-32, :63-71
+    const std::vector<std::size_t> expect{0, 3, 6, 10};
+    for (std::size_t r = 0; r <= 3; ++r) CHECK(cm::partition_output(10, 3, r) == expect[r]);
+    const std::size_t big = std::size_t{1} << 62;
+    CHECK(cm::partition_output(big, 3, 3) == big);
+    CHECK(cm::partition_output(big, 3, 1) == big / 3);
+    CHECK(throws_with<std::invalid_argument>([] { cm::partition_output(10, 0, 0); }, "worker"));
+    // parallel_test.cpp:74-91
+    {
+        const auto p = cm::plan(keys{2, 2}, keys{2, 2}, 2);
+        CHECK((p.blocks[0] == cm::block_assignment{0, 0, 2, 0, 2, 0, 0}));
+        CHECK((p.blocks[1] == cm::block_assignment{1, 2, 4, 2, 2, 0, 2}));
+        const auto q = cm::plan(keys{}, keys{0, 1, 2, 3, 4, 5, 6, 7, 8, 9}, 2);
+        CHECK((q.blocks[0] == cm::block_assignment{0, 0, 5, 0, 0, 0, 5}));
+    }
+    // parallel_test.cpp:190-212
+    {
+        keys e;
+        const auto rep = cm::merge_parallel(keys{}, keys{}, e, 4);
+        CHECK((rep.block_sizes == std::vector<std::size_t>(4, 0)));
+        keys o3(3);
+        cm::merge_parallel(keys{1, 3}, keys{2}, o3, 9);
+        CHECK((o3 == keys{1, 2, 3}));
+        CHECK(throws_with<std::invalid_argument>(
+            [] {
+                keys w(3);
+                cm::merge_parallel(keys{1}, keys{2}, w, 2);
+            },
+            "output length must equal"));
+        CHECK(throws_with<std::invalid_argument>(
+            [] {
+                keys w(2);
+                cm::merge_parallel(keys{1}, keys{2}, w, 0);
+            },
+            "worker count must be positive"));
+    }
+}
+
+template <typename K>
+static void sweep(std::uint64_t seed) {
+    std::mt19937_64 rng(seed);
+    const std::vector<std::pair<std::size_t, std::size_t>> shapes = {
+        {0, 5}, {7, 0}, {1, 1}, {3000, 20000}, {20000, 3}, {4096, 4096}, {100000, 77777},
+        {1 << 20, 5000}};
+    for (auto [m, n] : shapes) {
+        for (std::uint64_t alphabet : {std::uint64_t{3}, std::uint64_t{1} << 20}) {
+            std::vector<K> a(m), b(n);
+            for (auto& x : a) x = K(rng() % alphabet);
+            for (auto& x : b) x = K(rng() % alphabet);
+            std::sort(a.begin(), a.end());
+            std::sort(b.begin(), b.end());
+            const std::vector<K> expect = naive_merge(a, b);
+            for (std::size_t workers : {1, 3, 16}) {
+                std::vector<K> out(m + n, K(0x5a));
+                const auto rep = cm::merge_parallel(a, b, out, workers);
+                CHECK(out == expect);
+                CHECK(rep.block_sizes.size() == workers);
+                CHECK(rep.corank_iterations.size() == 2 * workers);
+            }
+            // device spans through the same entry point
+            K *da = nullptr, *db = nullptr, *dout = nullptr;
+            cudaMalloc(&da, (m + 1) * sizeof(K));
+            cudaMalloc(&db, (n + 1) * sizeof(K));
+            cudaMalloc(&dout, (m + n + 1) * sizeof(K));
+            cudaMemcpy(da, a.data(), m * sizeof(K), cudaMemcpyHostToDevice);
+            cudaMemcpy(db, b.data(), n * sizeof(K), cudaMemcpyHostToDevice);
+            cm::device_span<const K> sa{da, m}, sb{db, n};
+            cm::device_span<K> so{dout, m + n};
+            cm::merge_parallel_synced(sa, sb, so, 4);
+            std::vector<K> back(m + n);
+            cudaMemcpy(back.data(), dout, (m + n) * sizeof(K), cudaMemcpyDeviceToHost);
+            CHECK(back == expect);
+            cudaFree(da);
+            cudaFree(db);
+            cudaFree(dout);
+        }
+    }
+}
+
+int main() {
+    kats();
+    sweep<std::int32_t>(1);
+    sweep<std::uint32_t>(2);
+    sweep<std::uint64_t>(3);
+    std::printf("shim_test: %d failure(s)\n", g_fail);
+    return g_fail;
+}
