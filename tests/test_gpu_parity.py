@@ -392,3 +392,17 @@ def test_host_pipeline_report_matches_reference_stats(cuda, port):
     assert rep.corank_iterations == [x for r in range(5) for x in (its[r], its[r + 1])]
     rep_s = P().merge_parallel_synced(a, b, out, 5)
     assert rep_s.corank_iterations == its[:5]
+
+
+def test_rank_shards_concatenate(cuda, port):
+    """Algorithm 2 across ranks (paper_1303_4312_b200.shard): each rank merges
+    only its co-ranked windows; the shards concatenate to the full merge."""
+    from paper_1303_4312_b200.shard import merge_shard
+    rng = np.random.default_rng(8)
+    a, b = _draw(rng, np.int32, 300_001, 40), _draw(rng, np.int32, 200_003, 40)
+    expect = port.merge(a, b)
+    ta, tb = dev(a, cuda), dev(b, cuda)
+    for world in (1, 2, 3, 8):
+        parts = [merge_shard(ta, tb, r, world)[1] for r in range(world)]
+        torch.cuda.synchronize()
+        assert np.array_equal(np.concatenate([host(p) for p in parts]), expect), world
