@@ -78,10 +78,10 @@ int comerge_cuda_last_path(void);
  * streams), 1 = zero-copy for pinned host memory (the kernel reads and writes
  * host memory over PCIe), 2 = plain staging (copy in, merge, copy out). */
 void comerge_cuda_set_host_mode(int mode);
-/* Debug tracing of the persistent kernels: when non-NULL, CTA c writes
- * %globaltimer stamps (start, block co-ranked, first tile done, end) to
- * device_buffer[8c .. 8c+3] and its SM id to device_buffer[8c+4].  NULL
- * disables. */
+/* Debug tracing of the persistent kernels: when non-NULL (at least
+ * 12*4096 uint64), CTA c writes %globaltimer stamps and counters to
+ * device_buffer[8c .. 8c+7] and consumer phase sums to
+ * device_buffer[8*4096 + 4c ..].  NULL disables. */
 void comerge_cuda_set_trace(unsigned long long* device_buffer);
 /* Tuning knobs of the tile pipeline (benchmarking only; 0 = default): the
  * statically assigned share of tiles in percent (default: all but ~3 tiles per

@@ -26,8 +26,9 @@
 //     aligned supersets, payloads too): every input byte crosses HBM once.
 //   * Consumers (8 warps): tile-local co-rank per VT-slot diagonal and the
 //     branch-free serial merge (merge.hpp:22-31, ties to A) of merge_tile.cuh;
-//     the merged tile is written back into the stage and stored with one TMA
-//     bulk store, then the stage is released.
+//     the merged tile is written back into the stage and handed to the store
+//     warp, which stores it with one TMA bulk store and releases the stage
+//     once the store has read it (consumers never wait on a store).
 #pragma once
 
 #include <cstdint>
@@ -84,7 +85,7 @@ template <typename K, bool HAS_V, bool SEG = false>
 struct pipe_layout {
     using C = pipe_cfg<K, HAS_V>;
     static constexpr int kConsumers = C::NC;
-    static constexpr int kThreads = kConsumers + 96;  // + producer, scheduler, tail warps
+    static constexpr int kThreads = kConsumers + 128;  // + producer, scheduler, tail, store warps
     static constexpr int kCW = kConsumers / 32;       // consumer warps (roles follow them)
     static constexpr int VT = C::VT;
     static constexpr int T = kConsumers * VT;
@@ -102,7 +103,7 @@ struct pipe_layout {
     static constexpr size_t kStage = kStageKeys + kStageVals + kStageOffs;
     static constexpr size_t oStages = 0;
     static constexpr size_t oBars = oStages + NST * kStage;
-    static constexpr size_t oMeta = oBars + size_t(2 * NST) * 8;  // NST x 8 x u64
+    static constexpr size_t oMeta = oBars + size_t(3 * NST) * 8;  // NST x 8 x u64
     static constexpr size_t oDesc = oMeta + size_t(NST) * 64;      // NB x {i0,j0,j1,i1,s0,s1,-,-}
     static constexpr size_t oScratch = oDesc + size_t(NB) * 64;    // 40 x u64
     static constexpr size_t oMisc = oScratch + 40 * 8;
@@ -356,9 +357,11 @@ __device__ __forceinline__ void merge_thread_seg(const K* sA, int a_len, const K
     K ka1 = sA[ia + 1], kb1 = sB[ib + 1];  // look-ahead (see merge_thread)
 #pragma unroll
     for (int v = 0; v < VT; ++v) {
-        while (ia >= x1 && ib >= y1 && s < s_hi) {  // segment done: next one
-            ++s;
-            seg_span(s, x0, x1, y0, y1);
+        if (ia >= x1 && ib >= y1) {  // segment done: next non-empty one (rare)
+            while (ia >= x1 && ib >= y1 && s < s_hi) {
+                ++s;
+                seg_span(s, x0, x1, y0, y1);
+            }
         }
         const bool take_b = ib < y1 && (ia >= x1 || kb < ka);
         keys[v] = take_b ? kb : ka;
@@ -389,6 +392,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::oBars);
     uint64_t* empty = full + NST;
+    uint64_t* staged = empty + NST;  // consumers -> store warp: tile written to the stage
     uint64_t* meta = reinterpret_cast<uint64_t*>(smem + L::oMeta);
     uint64_t* desc = reinterpret_cast<uint64_t*>(smem + L::oDesc);
     uint64_t* scratch = reinterpret_cast<uint64_t*>(smem + L::oScratch);
@@ -433,6 +437,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         for (int s = 0; s < NST; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
+            mbar_init(&staged[s], 1);
         }
         *pushed = 0;
         *issued = 0;
@@ -445,7 +450,8 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
     // scratch: [0..8] j of boundaries ts0..ts0+8, [10..18] their segments,
     // [33] ts0, [34] te0
     uint64_t ts0 = 0, te0 = 0;
-    constexpr int W_PROD = L::kCW, W_SCHED = L::kCW + 1, W_TAIL = L::kCW + 2;
+    constexpr int W_PROD = L::kCW, W_SCHED = L::kCW + 1, W_TAIL = L::kCW + 2,
+                  W_STORE = L::kCW + 3;
     if (warp == W_SCHED) {
         uint64_t below = 0, all = 0;
         if (args.nweights == G) {
@@ -599,7 +605,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         // NS + q), a slot not yet valid is co-ranked here instead.
         if (NS < NT) {
             for (;;) {
-                while (*pushed - *issued >= args.lookahead) __nanosleep(128);
+                while (*pushed - *issued >= args.lookahead) __nanosleep(500);
                 uint64_t q = 0;
                 if (lane == 0) q = tail_claim(args.tail, args.epoch);
                 q = __shfl_sync(0xffffffffu, q, 0);
@@ -646,6 +652,41 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         return;
     }
 
+    if (warp == W_STORE) {
+        // ------------------------------------------------------ store warp
+        // Stores each merged tile from its stage with one TMA bulk store and
+        // releases the stage to the producer once the store has read it, so
+        // the consumer warps never wait on a store.
+        if (lane != 0) return;
+        K* __restrict__ out = static_cast<K*>(args.out);
+        uint32_t* __restrict__ outv = args.outv;
+        for (uint32_t s = 0;; ++s) {
+            const int st = int(s % NST);
+            mbar_wait_sleepy(&staged[st], uint32_t((s / NST) & 1), 2000);
+            const uint64_t* mt = meta + 8 * st;
+            if (mt[3] >> 63) break;  // end of work
+            const uint64_t i0 = mt[0];
+            const uint64_t lens = mt[2];
+            const int len = int(lens >> 32) + int(lens & 0xffffffffu);
+            unsigned char* stage = smem + L::oStages + size_t(st) * L::kStage;
+            const K* sk = reinterpret_cast<const K*>(stage);
+            const uint32_t* sv = reinterpret_cast<const uint32_t*>(stage + L::kStageKeys);
+            const uint32_t kb_bytes = uint32_t(len * sizeof(K)) & ~15u;
+            if (kb_bytes) tma_store_1d(out + i0, sk, kb_bytes);
+            for (int x = kb_bytes / sizeof(K); x < len; ++x) out[i0 + x] = sk[x];
+            if constexpr (HAS_V) {
+                const uint32_t vb_bytes = uint32_t(len * 4) & ~15u;
+                if (vb_bytes) tma_store_1d(outv + i0, sv, vb_bytes);
+                for (int x = vb_bytes / 4; x < len; ++x) outv[i0 + x] = sv[x];
+            }
+            tma_store_commit();
+            tma_store_wait_read<0>();  // the stage has been read by the store
+            mbar_arrive(&empty[st]);
+        }
+        tma_store_wait_all();
+        return;
+    }
+
     if (warp == W_PROD) {
         // ------------------------------------------------------ producer
         if (lane != 0) return;
@@ -653,10 +694,10 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         unsigned long long starve = 0;  // ns spent waiting for descriptors
         for (uint32_t s = 0;; ++s) {
             const int st = int(s % NST);
-            if (s >= uint32_t(NST)) mbar_wait(&empty[st], uint32_t((s / NST - 1) & 1));
+            if (s >= uint32_t(NST)) mbar_wait_sleepy(&empty[st], uint32_t((s / NST - 1) & 1), 1000);
             if (*pushed <= s) {
                 const unsigned long long w0 = args.trace ? globaltimer_ns() : 0;
-                while (*pushed <= s) __nanosleep(64);
+                while (*pushed <= s) __nanosleep(200);
                 if (args.trace) starve += globaltimer_ns() - w0;
             }
             __threadfence_block();
@@ -742,21 +783,23 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
     K* __restrict__ out = static_cast<K*>(args.out);
     uint32_t* __restrict__ outv = args.outv;
     unsigned long long data_wait = 0;  // ns consumers waited for stage data
+    unsigned long long ph[4] = {0, 0, 0, 0};  // trace: merge, barrier 1, staging+barrier 2, store
     uint32_t s_done = 0;
     unsigned long long t_stream = 0;   // when the first tile's data arrived
     for (uint32_t s = 0;; ++s) {
         const int st = int(s % NST);
         if (args.trace && tid == 0) {
             const unsigned long long w0 = globaltimer_ns();
-            mbar_wait(&full[st], uint32_t((s / NST) & 1));
+            mbar_wait_sleepy(&full[st], uint32_t((s / NST) & 1), 500);
             data_wait += globaltimer_ns() - w0;
         }
-        mbar_wait(&full[st], uint32_t((s / NST) & 1));
+        mbar_wait_sleepy(&full[st], uint32_t((s / NST) & 1), 500);
         if (s == 0) t_stream = globaltimer_ns();
         const uint64_t* mt = meta + 8 * st;
         const uint64_t packed = mt[3];
         if (packed >> 63) {
             s_done = s;
+            if (tid == 0) mbar_arrive(&staged[st]);  // the store warp sees the end marker
             break;
         }
         const uint64_t i0 = mt[0];
@@ -772,6 +815,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         const int diag = min(tid * VT, len);
         K keys[VT];
         uint32_t src[VT];
+        const unsigned long long p0 = args.trace && tid == 0 ? globaltimer_ns() : 0;
         if constexpr (SEG) {
             const uint64_t k0 = mt[1];
             seg_offsets off;
@@ -798,7 +842,9 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
                 if (diag + v < len)
                     src[v] = (src[v] & 0x80000000u) ? sbv[src[v] & 0x7fffffffu] : sav[src[v]];
         }
+        const unsigned long long p1 = args.trace && tid == 0 ? globaltimer_ns() : 0;
         named_bar_sync(1, NC);  // every thread is done reading the windows
+        const unsigned long long p2 = args.trace && tid == 0 ? globaltimer_ns() : 0;
         const int cnt = len - diag < VT ? len - diag : VT;
 #pragma unroll
         for (int v = 0; v < VT; ++v)
@@ -808,22 +854,17 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             }
         fence_proxy_async_smem();
         named_bar_sync(1, NC);
+        const unsigned long long p3 = args.trace && tid == 0 ? globaltimer_ns() : 0;
         if (tid == 0) {
-            const uint32_t kb_bytes = uint32_t(len * sizeof(K)) & ~15u;
-            if (kb_bytes) tma_store_1d(out + i0, sk, kb_bytes);
-            for (int x = kb_bytes / sizeof(K); x < len; ++x) out[i0 + x] = sk[x];
-            if constexpr (HAS_V) {
-                const uint32_t vb_bytes = uint32_t(len * 4) & ~15u;
-                if (vb_bytes) tma_store_1d(outv + i0, sv, vb_bytes);
-                for (int x = vb_bytes / 4; x < len; ++x) outv[i0 + x] = sv[x];
+            mbar_arrive(&staged[st]);  // hand the tile to the store warp
+            if (args.trace) {
+                ph[0] += p1 - p0;
+                ph[1] += p2 - p1;
+                ph[2] += p3 - p2;
             }
-            tma_store_commit();
-            tma_store_wait_read<0>();  // the stage has been read by the store
-            mbar_arrive(&empty[st]);
         }
         if (args.trace && tid == 0 && s == 0) args.trace[8 * c + 2] = globaltimer_ns();
     }
-    if (tid == 0) tma_store_wait_all();
     if (args.perf && tid == 0) {
         uint32_t smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -835,6 +876,8 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
     if (args.trace && tid == 0) {
         args.trace[8 * c + 3] = globaltimer_ns();
         args.trace[8 * c + 7] = data_wait;
+        unsigned long long* ext = args.trace + 8 * 4096;  // phase sums, 4 per CTA
+        for (int q = 0; q < 4; ++q) ext[4 * c + q] = ph[q];
     }
 }
 

@@ -83,6 +83,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     } while (!ok);
 }
 
+// Same, letting the waiting thread sleep up to `hint_ns` inside try_wait
+// (returns as soon as the phase completes): fewer spin iterations for
+// latency-tolerant waiters.
+__device__ __forceinline__ void mbar_wait_sleepy(uint64_t* bar, uint32_t parity,
+                                                 uint32_t hint_ns) {
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(hint_ns)
+            : "memory");
+    } while (!ok);
+}
+
 // 1-D TMA bulk copy global -> shared, completing `bytes` on `bar`.
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
                                             uint64_t* bar, uint64_t policy) {

@@ -34,7 +34,7 @@ def main():
     P.set_kernel_path(args.path)
     N.lib.comerge_cuda_set_tuning(args.static_pct, args.min_chunk, args.lookahead)
     flush = torch.empty(512 * 2**20 // 4, dtype=torch.int32, device=dev)
-    trace = torch.zeros(8 * 4096, dtype=torch.int64, device=dev) if args.trace else None
+    trace = torch.zeros(16 * 4096, dtype=torch.int64, device=dev) if args.trace else None
     for r in range(args.reps):
         flush.fill_(r)
         if trace is not None and r == args.reps - 1:
@@ -48,8 +48,10 @@ def main():
         print(f"{args.config} rep {r}: {s.elapsed_time(e) * 1e3:.1f} us "
               f"(path {N.lib.comerge_cuda_last_path()})")
     if trace is not None:
-        full = trace.view(-1, 8).cpu()
-        full = full[full[:, 0] > 0]
+        rows = trace[: 8 * 4096].view(-1, 8).cpu()
+        live = rows[:, 0] > 0
+        ext = trace[8 * 4096: 8 * 4096 + 4 * 4096].view(-1, 4).cpu()[live].double() / 1e3
+        full = rows[live]
         t = full[:, :4]
         t0 = t[:, 0].min()
         rel = (t - t0).double() / 1e3
@@ -67,6 +69,8 @@ def main():
         order = torch.argsort(dur)
         print("  stream dur ", q(dur))
         print("  startup done", q((full[:, 5] - t0).double() / 1e3))
+        print("  consumer us: merge", q(ext[:, 0]), "bar1", q(ext[:, 1]), "stage+bar2", q(ext[:, 2]),
+              "store", q(ext[:, 3]))
         print("  producer starved us", q(full[:, 6].double() / 1e3))
         print("  consumer data-wait us", q(full[:, 7].double() / 1e3))
         print("  slowest 12 (cta, smid, us):",
