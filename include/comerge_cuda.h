@@ -84,9 +84,9 @@ void comerge_cuda_set_host_mode(int mode);
  * device_buffer[8*4096 + 4c ..].  NULL disables. */
 void comerge_cuda_set_trace(unsigned long long* device_buffer);
 /* Tuning knobs of the tile pipeline (benchmarking only; 0 = default): the
- * statically assigned share of tiles in percent (default: all but ~3 tiles per
- * CTA, at most 15% dynamic), an unused slot, and the claim look-ahead (queued
- * tiles below which the next tail tile is claimed, default 4). */
+ * statically assigned share of tiles in percent (default 75; the rest is the
+ * dynamic tail), an unused slot, and the claim look-ahead (queued tiles below
+ * which the next tail tile is claimed, default 2). */
 void comerge_cuda_set_tuning(int static_pct, int reserved, int lookahead);
 
 /* ------------------------------------------------------------ workspace */

@@ -294,7 +294,11 @@ size_t merge_ws_bytes(size_t m, size_t n) {
     if (total == 0) return 0;
     // tile kernel: one co-rank per tile boundary; pipeline: tail counter + slots
     const size_t tile_ws = round256((div_up(total, tile_cfg<K>::kTile) + 1) * sizeof(uint64_t));
-    const size_t pipe_ws = round256(32 * (3 * size_t(kMaxPipeGrid) + 2));
+    // one 32-byte slot per pipeline tile covers any tail fraction
+    constexpr uint64_t pt = pipe_layout<K, false>::T < pipe_layout<K, true>::T
+                                ? pipe_layout<K, false>::T
+                                : pipe_layout<K, true>::T;
+    const size_t pipe_ws = round256(32 * (div_up(total, pt) + 2));
     return tile_ws > pipe_ws ? tile_ws : pipe_ws;
 }
 
@@ -302,7 +306,7 @@ template <typename K>
 size_t seg_ws_bytes(size_t total) {
     if (total == 0) return 0;
     const size_t tile_ws = 2 * round256((div_up(total, seg_cfg<K>::kTile) + 1) * sizeof(uint64_t));
-    const size_t pipe_ws = round256(32 * (3 * size_t(kMaxPipeGrid) + 2));
+    const size_t pipe_ws = round256(32 * (div_up(total, pipe_layout<K, false, true>::T) + 2));
     return tile_ws > pipe_ws ? tile_ws : pipe_ws;
 }
 
@@ -360,12 +364,12 @@ int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const ui
     args.boff = boff;
     args.nseg = nseg;
     args.trace = g_trace;
-    // static weighted split + dynamic tail of ~3 tiles per CTA (<= 15%)
-    uint64_t tail_tiles = 3ull * grid;
-    if (g_tune_static_pct > 0)
-        tail_tiles = ptiles * uint64_t(100 - (g_tune_static_pct > 100 ? 100 : g_tune_static_pct)) / 100;
-    else if (tail_tiles > ptiles * 15 / 100)
-        tail_tiles = ptiles * 15 / 100;
+    // static weighted split of 75% of the tiles + a dynamic tail of 25%: the
+    // tail absorbs start-up skew (~10 us between the first and last CTA to
+    // start streaming) and the per-SM speed spread the weights miss
+    const uint64_t static_pct =
+        g_tune_static_pct > 0 ? uint64_t(g_tune_static_pct > 100 ? 100 : g_tune_static_pct) : 75;
+    const uint64_t tail_tiles = ptiles * (100 - static_pct) / 100;
     args.static_tiles = ptiles - tail_tiles;
     scratch sc;
     if (tail_tiles > 0) {
@@ -373,7 +377,7 @@ int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const ui
         args.tail = static_cast<uint64_t*>(sc.ptr);
         args.epoch = next_tail_epoch();
     }
-    args.lookahead = g_tune_lookahead > 0 ? uint32_t(g_tune_lookahead) : 4u;
+    args.lookahead = g_tune_lookahead > 0 ? uint32_t(g_tune_lookahead) : 2u;
     balance().prepare(args, grid, ptiles);
     g_last_path = SEG ? 5 : 3;
     mark_before(s);

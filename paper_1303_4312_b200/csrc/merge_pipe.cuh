@@ -108,7 +108,11 @@ struct pipe_layout {
     static constexpr size_t oScratch = oDesc + size_t(NB) * 64;    // 40 x u64
     static constexpr size_t oMisc = oScratch + 40 * 8;
     static constexpr size_t kMisc = 64;
-    static constexpr size_t kSmem = oMisc + kMisc;
+    // segmented batches: window-relative ends of the current tile's segments
+    // (x1 | y1 << 16), built by the consumers once per tile
+    static constexpr size_t oSegEnd = oMisc + kMisc;
+    static_assert(!SEG || KW < 65536, "segment ends are packed as 16-bit window offsets");
+    static constexpr size_t kSmem = oSegEnd + (SEG ? size_t(SEGCAP) * 4 : 0);
 };
 
 constexpr int kMaxPipeGrid = 512;
@@ -362,6 +366,65 @@ __device__ __forceinline__ void merge_thread_seg(const K* sA, int a_len, const K
                 ++s;
                 seg_span(s, x0, x1, y0, y1);
             }
+        }
+        const bool take_b = ib < y1 && (ia >= x1 || kb < ka);
+        keys[v] = take_b ? kb : ka;
+        if (take_b) {
+            ++ib;
+            kb = kb1;
+            kb1 = sB[ib + 1];
+        } else {
+            ++ia;
+            ka = ka1;
+            ka1 = sA[ia + 1];
+        }
+    }
+}
+
+// Segmented consumer merge from the tile's segment-end table `se` (entry k:
+// window-relative end of segment s_lo + k, x1 | y1 << 16; the last entry is
+// (a_len, b_len)).  A segment's windows start where the previous one's end,
+// so a segment change only moves the limits x1 / y1: the per-step cost over
+// merge_thread is one test, and the rare change is two shared loads.
+template <typename K, int VT>
+__device__ __forceinline__ void merge_thread_segends(const K* sA, const K* sB, int diag,
+                                                     const uint32_t* se, int nse,
+                                                     K (&keys)[VT]) {
+    int lo = 0, hi = nse - 1;  // first segment whose window part ends past diag
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const uint32_t e = se[mid];
+        if (int(e & 0xffffu) + int(e >> 16) > diag)
+            hi = mid;
+        else
+            lo = mid + 1;
+    }
+    int k = lo;
+    const uint32_t e0 = k > 0 ? se[k - 1] : 0u;
+    const int x0 = int(e0 & 0xffffu), y0 = int(e0 >> 16);
+    uint32_t e1 = se[k];
+    int x1 = int(e1 & 0xffffu), y1 = int(e1 >> 16);
+    const int dl = diag - x0 - y0;
+    const int na = x1 - x0, nb = y1 - y0;
+    int l = dl > nb ? dl - nb : 0, h = dl < na ? dl : na;
+    while (l < h) {
+        const int mid = (l + h + 1) >> 1;
+        if (sB[y0 + dl - mid] < sA[x0 + mid - 1])
+            h = mid - 1;
+        else
+            l = mid;
+    }
+    int ia = x0 + l, ib = y0 + dl - l;
+    K ka = sA[ia], kb = sB[ib];
+    K ka1 = sA[ia + 1], kb1 = sB[ib + 1];
+#pragma unroll
+    for (int v = 0; v < VT; ++v) {
+        if (ia >= x1 && ib >= y1 && k < nse - 1) {  // next segment (rare)
+            do {
+                e1 = se[++k];
+                x1 = int(e1 & 0xffffu);
+                y1 = int(e1 >> 16);
+            } while (ia >= x1 && ib >= y1 && k < nse - 1);
         }
         const bool take_b = ib < y1 && (ia >= x1 || kb < ka);
         keys[v] = take_b ? kb : ka;
@@ -684,6 +747,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             mbar_arrive(&empty[st]);
         }
         tma_store_wait_all();
+        if (args.trace) args.trace[8 * 4096 + 4 * c + 3] = globaltimer_ns();  // stores drained
         return;
     }
 
@@ -818,16 +882,27 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         const unsigned long long p0 = args.trace && tid == 0 ? globaltimer_ns() : 0;
         if constexpr (SEG) {
             const uint64_t k0 = mt[1];
-            seg_offsets off;
-            if (mt[6]) {
+            const uint64_t s_lo = mt[4], s_hi = mt[5];
+            if (mt[6]) {  // offsets staged: build the segment-end table, then merge
                 const uint64_t* so =
                     reinterpret_cast<const uint64_t*>(stage + L::kStageKeys + L::kStageVals);
-                off = seg_offsets{so, so + L::SEGCAP, mt[6] - 1, true};
+                uint32_t* se = reinterpret_cast<uint32_t*>(smem + L::oSegEnd);
+                const int nse = int(s_hi - s_lo) + 1;
+                if (tid < nse) {
+                    const uint64_t x = s_lo + uint64_t(tid) + 1 - (mt[6] - 1);
+                    const uint64_t ae = so[x], be = so[L::SEGCAP + x];
+                    const uint64_t j0 = i0 - k0;
+                    const uint32_t x1 = ae > j0 ? uint32_t(min(ae - j0, uint64_t(a_len))) : 0u;
+                    const uint32_t y1 = be > k0 ? uint32_t(min(be - k0, uint64_t(b_len))) : 0u;
+                    se[tid] = x1 | (y1 << 16);
+                }
+                named_bar_sync(1, NC);
+                merge_thread_segends<K, VT>(sk + a_off, sk + b_base + b_off, diag, se, nse, keys);
             } else {
-                off = seg_offsets{args.aoff, args.boff, 0, false};
+                const seg_offsets off{args.aoff, args.boff, 0, false};
+                merge_thread_seg<K, VT>(sk + a_off, a_len, sk + b_base + b_off, b_len, diag, i0,
+                                        i0 - k0, k0, s_lo, s_hi, off, keys);
             }
-            merge_thread_seg<K, VT>(sk + a_off, a_len, sk + b_base + b_off, b_len, diag, i0,
-                                    i0 - k0, k0, mt[4], mt[5], off, keys);
         } else {
             merge_thread<K, VT, HAS_V>(sk + a_off, a_len, sk + b_base + b_off, b_len, diag, keys,
                                        src);
@@ -877,7 +952,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         args.trace[8 * c + 3] = globaltimer_ns();
         args.trace[8 * c + 7] = data_wait;
         unsigned long long* ext = args.trace + 8 * 4096;  // phase sums, 4 per CTA
-        for (int q = 0; q < 4; ++q) ext[4 * c + q] = ph[q];
+        for (int q = 0; q < 3; ++q) ext[4 * c + q] = ph[q];
     }
 }
 

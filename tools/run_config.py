@@ -50,7 +50,8 @@ def main():
     if trace is not None:
         rows = trace[: 8 * 4096].view(-1, 8).cpu()
         live = rows[:, 0] > 0
-        ext = trace[8 * 4096: 8 * 4096 + 4 * 4096].view(-1, 4).cpu()[live].double() / 1e3
+        ext_raw = trace[8 * 4096: 8 * 4096 + 4 * 4096].view(-1, 4).cpu()[live]
+        ext = ext_raw.double() / 1e3
         full = rows[live]
         t = full[:, :4]
         t0 = t[:, 0].min()
@@ -69,8 +70,8 @@ def main():
         order = torch.argsort(dur)
         print("  stream dur ", q(dur))
         print("  startup done", q((full[:, 5] - t0).double() / 1e3))
-        print("  consumer us: merge", q(ext[:, 0]), "bar1", q(ext[:, 1]), "stage+bar2", q(ext[:, 2]),
-              "store", q(ext[:, 3]))
+        print("  consumer us: merge", q(ext[:, 0]), "bar1", q(ext[:, 1]), "stage+bar2", q(ext[:, 2]))
+        print("  stores drained after consumer end us", q((ext_raw[:, 3] - full[:, 3]).double() / 1e3))
         print("  producer starved us", q(full[:, 6].double() / 1e3))
         print("  consumer data-wait us", q(full[:, 7].double() / 1e3))
         print("  slowest 12 (cta, smid, us):",
