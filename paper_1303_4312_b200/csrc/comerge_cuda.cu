@@ -369,7 +369,9 @@ int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const ui
     // start streaming) and the per-SM speed spread the weights miss
     const uint64_t static_pct =
         g_tune_static_pct > 0 ? uint64_t(g_tune_static_pct > 100 ? 100 : g_tune_static_pct) : 75;
-    const uint64_t tail_tiles = ptiles * (100 - static_pct) / 100;
+    // (a few tiles per CTA: nothing to balance, all static)
+    const uint64_t tail_tiles =
+        ptiles < 4ull * grid && g_tune_static_pct == 0 ? 0 : ptiles * (100 - static_pct) / 100;
     args.static_tiles = ptiles - tail_tiles;
     scratch sc;
     if (tail_tiles > 0) {
@@ -378,6 +380,9 @@ int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const ui
         args.epoch = next_tail_epoch();
     }
     args.lookahead = g_tune_lookahead > 0 ? uint32_t(g_tune_lookahead) : 2u;
+    // small inputs: co-rank the first boundaries of every CTA concurrently
+    // (their random probes hit L2; on large inputs they would contend in HBM)
+    args.eager_start = total * sizeof(K) <= (size_t(32) << 20) ? 1u : 0u;
     balance().prepare(args, grid, ptiles);
     g_last_path = SEG ? 5 : 3;
     mark_before(s);

@@ -137,6 +137,7 @@ struct pipe_args {
     uint64_t* tail;              // dynamic tail workspace (16B aligned): {tag, count} + slots
     uint64_t epoch;              // per-launch tag validating tail state (no memset needed)
     uint32_t nweights;           // == gridDim.x when weights are given, else 0 (uniform)
+    uint32_t eager_start;        // co-rank the first tiles' boundaries concurrently (small inputs)
     uint16_t weights[kMaxPipeGrid];  // per-CTA share of the static tiles
 };
 
@@ -509,13 +510,14 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
     // ---- start-up: this worker's static range [ts0, te0) of the first NS
     // tiles, proportional to its weight (weights learned from the throughput
     // of earlier launches; any weights give a valid partition), then co-rank
-    // its start with one warp (33-ary; few concurrent probes keep rounds short).
+    // its start with one warp (33-ary; few concurrent probes keep rounds
+    // short) and the next 8 boundaries bracketed by it.
     // scratch: [0..8] j of boundaries ts0..ts0+8, [10..18] their segments,
     // [33] ts0, [34] te0
     uint64_t ts0 = 0, te0 = 0;
     constexpr int W_PROD = L::kCW, W_SCHED = L::kCW + 1, W_TAIL = L::kCW + 2,
                   W_STORE = L::kCW + 3;
-    if (warp == W_SCHED) {
+    auto static_range = [&](uint64_t& r0, uint64_t& r1) {  // warp-collective
         uint64_t below = 0, all = 0;
         if (args.nweights == G) {
             for (uint32_t x = lane; x < G; x += 32) {
@@ -530,8 +532,11 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             below = c;
             all = G;
         }
-        ts0 = NS * below / all;
-        te0 = NS * (below + (args.nweights == G ? args.weights[c] : 1)) / all;
+        r0 = NS * below / all;
+        r1 = NS * (below + (args.nweights == G ? args.weights[c] : 1)) / all;
+    };
+    if (warp == W_SCHED) {
+        static_range(ts0, te0);
         if (lane == 0) {
             scratch[33] = ts0;
             scratch[34] = te0;
@@ -545,6 +550,22 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
                 scratch[10] = bd.s;
             }
         }
+    } else if (args.eager_start && warp < (L::kCW < 8 ? L::kCW : 8)) {
+        // small inputs (their probes stay in L2): the consumer warps co-rank
+        // boundaries ts0+1 .. ts0+8 over the full diagonal at the same time
+        // as the start, instead of bracketed after it
+        uint64_t s0, e0;
+        static_range(s0, e0);
+        if (s0 + 1 + uint64_t(warp) <= e0) {
+            const uint64_t i = diag_of(s0 + 1 + uint64_t(warp));
+            uint64_t lo, hi;
+            full_bracket(i, lo, hi);
+            const boundary bd = find_boundary<K, SEG>(args, i, lo, hi, 0, 32, nullptr);
+            if (lane == 0) {
+                scratch[1 + warp] = bd.j;
+                scratch[11 + warp] = bd.s;
+            }
+        }
     }
     __syncthreads();
     ts0 = scratch[33];
@@ -553,8 +574,8 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
     // 33-ary, bracketed by the start split) so the first tiles are ready fast
     int known = 0;
     if (te0 > ts0) {
-        known = te0 - ts0 - 1 < 8 ? int(te0 - ts0 - 1) : 8;
-        if (warp < known) {
+        known = te0 - ts0 < 8 ? int(te0 - ts0) : 8;
+        if (warp < known && !args.eager_start) {
             const uint64_t t = ts0 + 1 + warp;
             uint64_t lo, hi;
             step_bracket(diag_of(t), diag_of(ts0), scratch[0], lo, hi);
@@ -566,7 +587,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             }
         }
     }
-    __syncthreads();
+    if (!args.eager_start) __syncthreads();
     if (args.trace && tid == 0) args.trace[8 * c + 5] = globaltimer_ns();
     if (warp == W_TAIL) {
         // ------------------------------------------------------ tail warp
