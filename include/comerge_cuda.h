@@ -85,9 +85,10 @@ void comerge_cuda_set_host_mode(int mode);
 void comerge_cuda_set_trace(unsigned long long* device_buffer);
 /* Tuning knobs of the tile pipeline (benchmarking only; 0 = default): the
  * statically assigned share of tiles in percent (default 75; the rest is the
- * dynamic tail), an unused slot, and the claim look-ahead (queued tiles below
- * which the next tail tile is claimed, default 2). */
-void comerge_cuda_set_tuning(int static_pct, int reserved, int lookahead);
+ * dynamic tail), experiment flags (bit 0: co-rank the start-up boundaries one
+ * after the other), and the claim look-ahead (queued tiles below which the next
+ * tail tile is claimed, default 2). */
+void comerge_cuda_set_tuning(int static_pct, int flags, int lookahead);
 
 /* ------------------------------------------------------------ workspace */
 

@@ -29,7 +29,7 @@ thread_local int g_path = 0;  // 0 auto, 1 tile (v1), 2 ring streaming (v2), 3 t
 thread_local int g_last_path = 0;  // kernel of the last merge: 1 tile, 2 ring, 3 pipe, 4 segmented
 thread_local unsigned long long* g_trace = nullptr;  // debug: per-CTA timestamps
 // tuning knobs of the tile pipeline (0 = default)
-thread_local int g_tune_lookahead = 0, g_tune_static_pct = 0;
+thread_local int g_tune_lookahead = 0, g_tune_static_pct = 0, g_tune_flags = 0;
 thread_local int g_host_mode = 0;  // host buffers: 0 chunked pipeline, 1 zero-copy, 2 plain staging
 
 int sm_count() {
@@ -107,9 +107,16 @@ struct balance_state {
         std::memset(perf_host, 0, 4 * kMaxPipeGrid * sizeof(unsigned long long));
     }
 
+    // Static tile ranges: CTA c gets [starts[c], starts[c+1]) of the first
+    // static_tiles tiles, proportional to its SM's learned speed (uniform
+    // when there is no history or the merge is small).
     void prepare(pipe_args& args, uint32_t G, uint64_t ntiles) {
-        args.nweights = 0;
         args.perf = nullptr;
+        const uint64_t NS = args.static_tiles;
+        auto uniform = [&] {
+            for (uint32_t c = 0; c <= G; ++c) args.starts[c] = uint32_t(NS * c / G);
+        };
+        uniform();
         if (G > uint32_t(kMaxPipeGrid)) return;
         std::lock_guard<std::mutex> lock(mu);
         if (!perf_host) {
@@ -130,12 +137,18 @@ struct balance_state {
         }
         fold();
         if (ntiles < 8ull * G) return;  // small merges: uniform split, no report
+        uint64_t w[kMaxPipeGrid], all = 0;
         for (uint32_t c = 0; c < G; ++c) {
-            const double w = cta_sm[c] >= 0 ? sm_speed[cta_sm[c]] : 1.0;
-            const double q = w * 1024.0;
-            args.weights[c] = uint16_t(q < 256 ? 256 : (q > 4096 ? 4096 : q + 0.5));
+            const double q = (cta_sm[c] >= 0 ? sm_speed[cta_sm[c]] : 1.0) * 1024.0;
+            w[c] = uint64_t(q < 256 ? 256 : (q > 4096 ? 4096 : q + 0.5));
+            all += w[c];
         }
-        args.nweights = G;
+        uint64_t below = 0;
+        for (uint32_t c = 0; c < G; ++c) {
+            args.starts[c] = uint32_t(NS * below / all);
+            below += w[c];
+        }
+        args.starts[G] = uint32_t(NS);
         args.perf = perf_dev;
         last_grid = G;
     }
@@ -383,6 +396,7 @@ int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const ui
     // small inputs: co-rank the first boundaries of every CTA concurrently
     // (their random probes hit L2; on large inputs they would contend in HBM)
     args.eager_start = total * sizeof(K) <= (size_t(32) << 20) ? 1u : 0u;
+    args.flags = uint32_t(g_tune_flags);
     balance().prepare(args, grid, ptiles);
     g_last_path = SEG ? 5 : 3;
     mark_before(s);
@@ -939,8 +953,9 @@ void comerge_cuda_set_path(int path) { g_path = path; }
 void comerge_cuda_set_host_mode(int mode) { g_host_mode = mode; }
 int comerge_cuda_last_path(void) { return g_last_path; }
 void comerge_cuda_set_trace(unsigned long long* device_buffer) { g_trace = device_buffer; }
-void comerge_cuda_set_tuning(int static_pct, int /*reserved*/, int lookahead) {
+void comerge_cuda_set_tuning(int static_pct, int flags, int lookahead) {
     g_tune_static_pct = static_pct;
+    g_tune_flags = flags;
     g_tune_lookahead = lookahead;
 }
 

@@ -136,24 +136,27 @@ struct pipe_args {
     unsigned long long* perf;    // optional: per-CTA {smid, stream ns, tiles, 1} at exit (host-mapped)
     uint64_t* tail;              // dynamic tail workspace (16B aligned): {tag, count} + slots
     uint64_t epoch;              // per-launch tag validating tail state (no memset needed)
-    uint32_t nweights;           // == gridDim.x when weights are given, else 0 (uniform)
     uint32_t eager_start;        // co-rank the first tiles' boundaries concurrently (small inputs)
-    uint16_t weights[kMaxPipeGrid];  // per-CTA share of the static tiles
+    uint32_t flags;              // benchmarking knobs (bit 0: no split start-up search)
+    uint32_t starts[kMaxPipeGrid + 1];  // CTA c's static tiles: [starts[c], starts[c+1])
 };
 
 // Lane-group (P+1)-ary search for the largest q in [lo, hi] with !pred(q),
 // given !pred(lo) and pred monotone (false ... false true ... true).  The
 // warp is split into 32/P groups of P lanes (P a power of two); every group
 // has its own bracket and predicate arguments.  All 32 lanes must call it.
+// With stop > 0 it returns early, once every bracket is at most stop wide:
+// the answer is then in [lo, hi] (both updated; the return value is lo).
 template <typename Pred>
-__device__ __forceinline__ uint64_t group_search_pred(uint64_t lo, uint64_t hi, int P, Pred pred,
-                                                      uint32_t* rounds) {
+__device__ __forceinline__ uint64_t group_search_pred(uint64_t& lo, uint64_t& hi, int P,
+                                                      Pred pred, uint32_t* rounds,
+                                                      uint64_t stop = 0) {
     const int lane = threadIdx.x & 31;
     const int g = lane / P, r = lane % P;
     const unsigned gmask = P == 32 ? 0xffffffffu : ((1u << P) - 1u) << (g * P);
     const uint64_t P1 = uint64_t(P) + 1;
-    while (__any_sync(0xffffffffu, hi > lo)) {
-        const bool active = hi > lo;
+    while (__any_sync(0xffffffffu, hi - lo > stop)) {
+        const bool active = hi - lo > stop;
         const uint64_t width = hi - lo;
         const uint64_t q = lo + ((uint64_t(r) + 1) * width + P) / P1;  // in (lo, hi]
         bool not_far = true;
@@ -181,6 +184,15 @@ __device__ __forceinline__ uint64_t group_search(uint64_t i, uint64_t lo, uint64
     return group_search_pred(
         lo, hi, P, [=](uint64_t q) { return ldg_elem(b + (i - q)) < ldg_elem(a + (q - 1)); },
         rounds);
+}
+// group_search narrowed only until the bracket [lo, hi] is at most stop wide
+template <typename K>
+__device__ __forceinline__ void group_narrow(uint64_t i, uint64_t& lo, uint64_t& hi, int P,
+                                             const K* __restrict__ a, const K* __restrict__ b,
+                                             uint64_t stop) {
+    group_search_pred(
+        lo, hi, P, [=](uint64_t q) { return ldg_elem(b + (i - q)) < ldg_elem(a + (q - 1)); },
+        nullptr, stop);
 }
 
 // Stage src[lo, hi) for a TMA copy whose destination `dst` corresponds to
@@ -225,9 +237,10 @@ __device__ __forceinline__ boundary find_boundary(const pipe_args& args, uint64_
     } else {
         const uint64_t* __restrict__ ao = args.aoff;
         const uint64_t* __restrict__ bo = args.boff;
+        uint64_t shi = args.nseg - 1;
         const uint64_t s = group_search_pred(
-            slo, args.nseg - 1, P,
-            [=](uint64_t q) { return ldg_u64(ao + q) + ldg_u64(bo + q) > i; }, rounds);
+            slo, shi, P, [=](uint64_t q) { return ldg_u64(ao + q) + ldg_u64(bo + q) > i; },
+            rounds);
         const uint64_t as = ldg_u64(ao + s), bs = ldg_u64(bo + s);
         const uint64_t ma = ldg_u64(ao + s + 1) - as, nb = ldg_u64(bo + s + 1) - bs;
         const uint64_t li = i - as - bs;  // <= ma + nb
@@ -508,58 +521,63 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         mbar_fence_init();
     }
     // ---- start-up: this worker's static range [ts0, te0) of the first NS
-    // tiles, proportional to its weight (weights learned from the throughput
-    // of earlier launches; any weights give a valid partition), then co-rank
+    // tiles, proportional to its weight (weights learned by the host from the
+    // throughput of earlier launches; any split gives a valid partition), then co-rank
     // its start with one warp (33-ary; few concurrent probes keep rounds
     // short) and the next 8 boundaries bracketed by it.
     // scratch: [0..8] j of boundaries ts0..ts0+8, [10..18] their segments,
-    // [33] ts0, [34] te0
+    // [36..37] the start's bracket after the first rounds
     uint64_t ts0 = 0, te0 = 0;
     constexpr int W_PROD = L::kCW, W_SCHED = L::kCW + 1, W_TAIL = L::kCW + 2,
                   W_STORE = L::kCW + 3;
-    auto static_range = [&](uint64_t& r0, uint64_t& r1) {  // warp-collective
-        uint64_t below = 0, all = 0;
-        if (args.nweights == G) {
-            for (uint32_t x = lane; x < G; x += 32) {
-                all += args.weights[x];
-                if (x < c) below += args.weights[x];
-            }
-            for (int o = 16; o; o >>= 1) {
-                all += __shfl_xor_sync(0xffffffffu, all, o);
-                below += __shfl_xor_sync(0xffffffffu, below, o);
-            }
-        } else {
-            below = c;
-            all = G;
-        }
-        r0 = NS * below / all;
-        r1 = NS * (below + (args.nweights == G ? args.weights[c] : 1)) / all;
-    };
+    ts0 = args.starts[c];  // static range, weighted by the host (kernel arguments)
+    te0 = args.starts[c + 1];
+    // boundaries ts0+1 .. ts0+known are co-ranked at start-up by the consumer warps
+    const int known = te0 > ts0 ? (te0 - ts0 < 8 ? int(te0 - ts0) : 8) : 0;
+    // large plain merges: the scheduler narrows the start's bracket to one tile,
+    // hands it to the consumer warps (named barrier 2), and both finish their
+    // searches concurrently (boundary w is in [lo, hi + (i_w - i_0)])
+    const bool split_start = !SEG && !args.eager_start && known > 0 && !(args.flags & 1u);
+    constexpr int kSplitBar = 32 * (L::kCW + 1);
     if (warp == W_SCHED) {
-        static_range(ts0, te0);
-        if (lane == 0) {
-            scratch[33] = ts0;
-            scratch[34] = te0;
-        }
         if (te0 > ts0) {
+            const uint64_t i = diag_of(ts0);
             uint64_t lo, hi;
-            full_bracket(diag_of(ts0), lo, hi);
-            const boundary bd = find_boundary<K, SEG>(args, diag_of(ts0), lo, hi, 0, 32, nullptr);
+            full_bracket(i, lo, hi);
+            boundary bd{0, 0};
+            if constexpr (!SEG) {
+                if (split_start) {
+                    group_narrow<K>(i, lo, hi, 32, a, b, uint64_t(T));
+                    if (lane == 0) {
+                        scratch[36] = lo;
+                        scratch[37] = hi;
+                    }
+                    __syncwarp();
+                    named_bar_sync(2, kSplitBar);
+                }
+            }
+            bd = find_boundary<K, SEG>(args, i, lo, hi, 0, 32, nullptr);
             if (lane == 0) {
                 scratch[0] = bd.j;
                 scratch[10] = bd.s;
             }
         }
-    } else if (args.eager_start && warp < (L::kCW < 8 ? L::kCW : 8)) {
-        // small inputs (their probes stay in L2): the consumer warps co-rank
-        // boundaries ts0+1 .. ts0+8 over the full diagonal at the same time
-        // as the start, instead of bracketed after it
-        uint64_t s0, e0;
-        static_range(s0, e0);
-        if (s0 + 1 + uint64_t(warp) <= e0) {
-            const uint64_t i = diag_of(s0 + 1 + uint64_t(warp));
+    } else if (warp < L::kCW && (split_start || (args.eager_start && known > 0))) {
+        uint64_t lo0 = 0, hi0 = 0;
+        if (split_start) {
+            named_bar_sync(2, kSplitBar);
+            lo0 = scratch[36];
+            hi0 = scratch[37];
+        }
+        if (warp < known) {
+            const uint64_t i = diag_of(ts0 + 1 + uint64_t(warp));
             uint64_t lo, hi;
             full_bracket(i, lo, hi);
+            if (split_start) {  // j(i) >= j(i_0) >= lo0, j(i) <= j(i_0) + (i - i_0)
+                const uint64_t up = hi0 + (i - diag_of(ts0));
+                if (lo0 > lo) lo = lo0;
+                if (up < hi) hi = up;
+            }
             const boundary bd = find_boundary<K, SEG>(args, i, lo, hi, 0, 32, nullptr);
             if (lane == 0) {
                 scratch[1 + warp] = bd.j;
@@ -568,14 +586,9 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         }
     }
     __syncthreads();
-    ts0 = scratch[33];
-    te0 = scratch[34];
-    // the idle consumer warps co-rank boundaries ts0+1 .. ts0+8 (one warp each,
-    // 33-ary, bracketed by the start split) so the first tiles are ready fast
-    int known = 0;
-    if (te0 > ts0) {
-        known = te0 - ts0 < 8 ? int(te0 - ts0) : 8;
-        if (warp < known && !args.eager_start) {
+    if (!split_start && !args.eager_start && known > 0) {
+        // segmented batches: boundaries ts0+1 .. ts0+known bracketed by the start
+        if (warp < known) {
             const uint64_t t = ts0 + 1 + warp;
             uint64_t lo, hi;
             step_bracket(diag_of(t), diag_of(ts0), scratch[0], lo, hi);
@@ -586,8 +599,8 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
                 scratch[11 + warp] = bd.s;
             }
         }
+        __syncthreads();
     }
-    if (!args.eager_start) __syncthreads();
     if (args.trace && tid == 0) args.trace[8 * c + 5] = globaltimer_ns();
     if (warp == W_TAIL) {
         // ------------------------------------------------------ tail warp

@@ -24,7 +24,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--static-pct", type=int, default=0)
-    ap.add_argument("--min-chunk", type=int, default=0)
+    ap.add_argument("--flags", type=int, default=0)
     ap.add_argument("--lookahead", type=int, default=0)
     args = ap.parse_args()
     dev = torch.device("cuda:0")
@@ -32,7 +32,7 @@ def main():
     inp = bench.make_inputs(args.config, device=dev)
     out = bench.alloc_outputs(args.config, inp)
     P.set_kernel_path(args.path)
-    N.lib.comerge_cuda_set_tuning(args.static_pct, args.min_chunk, args.lookahead)
+    N.lib.comerge_cuda_set_tuning(args.static_pct, args.flags, args.lookahead)
     flush = torch.empty(512 * 2**20 // 4, dtype=torch.int32, device=dev)
     trace = torch.zeros(16 * 4096, dtype=torch.int64, device=dev) if args.trace else None
     for r in range(args.reps):
