@@ -84,7 +84,7 @@ void comerge_cuda_set_host_mode(int mode);
  * device_buffer[8*4096 + 4c ..].  NULL disables. */
 void comerge_cuda_set_trace(unsigned long long* device_buffer);
 /* Tuning knobs of the tile pipeline (benchmarking only; 0 = default): the
- * statically assigned share of tiles in percent (default 75; the rest is the
+ * statically assigned share of tiles in percent (default 70; the rest is the
  * dynamic tail), experiment flags (bit 0: co-rank the start-up boundaries one
  * after the other), and the claim look-ahead (queued tiles below which the next
  * tail tile is claimed, default 2). */

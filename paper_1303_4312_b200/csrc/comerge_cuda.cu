@@ -42,123 +42,6 @@ int sm_count() {
     return n;
 }
 
-// Self-calibrating static partition of the tile pipeline.  Every launch
-// reports per CTA {SM id, streaming ns, tiles} into host-mapped pinned memory;
-// the next launch folds the streaming rates into a per-SM speed table
-// (exponential moving average, shared by every kernel instantiation on the
-// device) and gives CTA c a share of the tiles proportional to the speed of
-// the SM it last ran on (placement of a persistent grid is deterministic).
-// The weights are hints only: any weights give a valid partition, so a stale
-// or concurrent update never affects the output.
-struct balance_state {
-    std::mutex mu;
-    double sm_speed[256];
-    uint32_t sm_seen[256];
-    int32_t cta_sm[kMaxPipeGrid];
-    unsigned long long* perf_host = nullptr;  // 4 * kMaxPipeGrid entries (mapped)
-    unsigned long long* perf_dev = nullptr;
-    uint32_t last_grid = 0;
-    balance_state() {
-        for (int i = 0; i < 256; ++i) {
-            sm_speed[i] = 1.0;
-            sm_seen[i] = 0;
-        }
-        for (int c = 0; c < kMaxPipeGrid; ++c) cta_sm[c] = -1;
-    }
-
-    void fold() {  // consume the last report
-        if (!perf_host || last_grid == 0) return;
-        const uint32_t G = last_grid;
-        double rate[kMaxPipeGrid];
-        double sum = 0;
-        uint64_t tiles = 0;
-        for (uint32_t c = 0; c < G; ++c) {
-            const unsigned long long* p = perf_host + 4 * c;
-            if (p[3] != 1 || p[1] == 0 || p[0] >= 256) return;  // incomplete report
-            rate[c] = double(p[2]) / double(p[1]);
-            sum += rate[c];
-            tiles += p[2];
-        }
-        for (uint32_t c = 0; c < G; ++c) cta_sm[c] = int32_t(perf_host[4 * c]);
-        if (tiles >= 16ull * G && sum > 0) {
-            // the per-SM rate is the sum over its CTAs, normalised by the mean SM
-            double sm_rate[256] = {0};
-            uint32_t sm_ctas[256] = {0};
-            for (uint32_t c = 0; c < G; ++c) {
-                sm_rate[cta_sm[c]] += rate[c];
-                sm_ctas[cta_sm[c]]++;
-            }
-            double mean = 0;
-            int nsm = 0;
-            for (int x = 0; x < 256; ++x)
-                if (sm_ctas[x]) {
-                    mean += sm_rate[x];
-                    ++nsm;
-                }
-            mean /= nsm;
-            for (int x = 0; x < 256; ++x)
-                if (sm_ctas[x]) {
-                    double r = sm_rate[x] / mean;
-                    r = r < 0.5 ? 0.5 : (r > 2.0 ? 2.0 : r);
-                    sm_speed[x] = sm_seen[x] ? 0.5 * sm_speed[x] + 0.5 * r : r;
-                    sm_seen[x]++;
-                }
-        }
-        std::memset(perf_host, 0, 4 * kMaxPipeGrid * sizeof(unsigned long long));
-    }
-
-    // Static tile ranges: CTA c gets [starts[c], starts[c+1]) of the first
-    // static_tiles tiles, proportional to its SM's learned speed (uniform
-    // when there is no history or the merge is small).
-    void prepare(pipe_args& args, uint32_t G, uint64_t ntiles) {
-        args.perf = nullptr;
-        const uint64_t NS = args.static_tiles;
-        auto uniform = [&] {
-            for (uint32_t c = 0; c <= G; ++c) args.starts[c] = uint32_t(NS * c / G);
-        };
-        uniform();
-        if (G > uint32_t(kMaxPipeGrid)) return;
-        std::lock_guard<std::mutex> lock(mu);
-        if (!perf_host) {
-            void* h = nullptr;
-            if (cudaHostAlloc(&h, 4 * kMaxPipeGrid * sizeof(unsigned long long),
-                              cudaHostAllocMapped) != cudaSuccess) {
-                cudaGetLastError();
-                return;
-            }
-            perf_host = static_cast<unsigned long long*>(h);
-            std::memset(perf_host, 0, 4 * kMaxPipeGrid * sizeof(unsigned long long));
-            void* d = nullptr;
-            if (cudaHostGetDevicePointer(&d, h, 0) != cudaSuccess) {
-                cudaGetLastError();
-                return;
-            }
-            perf_dev = static_cast<unsigned long long*>(d);
-        }
-        fold();
-        if (ntiles < 8ull * G) return;  // small merges: uniform split, no report
-        uint64_t w[kMaxPipeGrid], all = 0;
-        for (uint32_t c = 0; c < G; ++c) {
-            const double q = (cta_sm[c] >= 0 ? sm_speed[cta_sm[c]] : 1.0) * 1024.0;
-            w[c] = uint64_t(q < 256 ? 256 : (q > 4096 ? 4096 : q + 0.5));
-            all += w[c];
-        }
-        uint64_t below = 0;
-        for (uint32_t c = 0; c < G; ++c) {
-            args.starts[c] = uint32_t(NS * below / all);
-            below += w[c];
-        }
-        args.starts[G] = uint32_t(NS);
-        args.perf = perf_dev;
-        last_grid = G;
-    }
-};
-
-balance_state& balance() {
-    static balance_state st;  // per process (one device in practice)
-    return st;
-}
-
 // Persistent grid size for the tile-pipeline kernel (resident CTAs, cached).
 template <typename K, bool HAS_V, bool SEG>
 int pipe_grid_limit() {
@@ -377,11 +260,14 @@ int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const ui
     args.boff = boff;
     args.nseg = nseg;
     args.trace = g_trace;
-    // static weighted split of 75% of the tiles + a dynamic tail of 25%: the
-    // tail absorbs start-up skew (~10 us between the first and last CTA to
-    // start streaming) and the per-SM speed spread the weights miss
+    // equal static split of 70% of the tiles + a dynamic tail of 30%: the tail
+    // absorbs the start-up skew (~10 us between the first and last CTA to
+    // start streaming) and the ~25% spread of per-SM streaming rates (B200
+    // GPCs differ).  (An earlier per-SM speed table learned from host-mapped
+    // per-CTA reports cost 4 us of kernel completion on C2 for the mapped
+    // writes, and bought nothing once the tail was 25-30%.)
     const uint64_t static_pct =
-        g_tune_static_pct > 0 ? uint64_t(g_tune_static_pct > 100 ? 100 : g_tune_static_pct) : 75;
+        g_tune_static_pct > 0 ? uint64_t(g_tune_static_pct > 100 ? 100 : g_tune_static_pct) : 70;
     // (a few tiles per CTA: nothing to balance, all static)
     const uint64_t tail_tiles =
         ptiles < 4ull * grid && g_tune_static_pct == 0 ? 0 : ptiles * (100 - static_pct) / 100;
@@ -397,7 +283,6 @@ int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const ui
     // (their random probes hit L2; on large inputs they would contend in HBM)
     args.eager_start = total * sizeof(K) <= (size_t(32) << 20) ? 1u : 0u;
     args.flags = uint32_t(g_tune_flags);
-    balance().prepare(args, grid, ptiles);
     g_last_path = SEG ? 5 : 3;
     mark_before(s);
     merge_pipe_kernel<K, HAS_V, SEG><<<grid, PL::kThreads, PL::kSmem, s>>>(args);

@@ -133,12 +133,10 @@ struct pipe_args {
     unsigned long long* trace;   // optional per-CTA timestamps (8 x u64 per CTA)
     uint64_t static_tiles;       // tiles [0, static_tiles) are split statically by weight
     uint32_t lookahead;          // claim a tail tile when fewer than this are queued
-    unsigned long long* perf;    // optional: per-CTA {smid, stream ns, tiles, 1} at exit (host-mapped)
     uint64_t* tail;              // dynamic tail workspace (16B aligned): {tag, count} + slots
     uint64_t epoch;              // per-launch tag validating tail state (no memset needed)
     uint32_t eager_start;        // co-rank the first tiles' boundaries concurrently (small inputs)
     uint32_t flags;              // benchmarking knobs (bit 0: no split start-up search)
-    uint32_t starts[kMaxPipeGrid + 1];  // CTA c's static tiles: [starts[c], starts[c+1])
 };
 
 // Lane-group (P+1)-ary search for the largest q in [lo, hi] with !pred(q),
@@ -520,18 +518,17 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         *issued = 0;
         mbar_fence_init();
     }
-    // ---- start-up: this worker's static range [ts0, te0) of the first NS
-    // tiles, proportional to its weight (weights learned by the host from the
-    // throughput of earlier launches; any split gives a valid partition), then co-rank
-    // its start with one warp (33-ary; few concurrent probes keep rounds
-    // short) and the next 8 boundaries bracketed by it.
+    // ---- start-up: this worker's static range [ts0, te0), an equal share of
+    // the first NS tiles, then co-rank its start with one warp (33-ary; few
+    // concurrent probes keep rounds short) and the next 8 boundaries
+    // bracketed by it.
     // scratch: [0..8] j of boundaries ts0..ts0+8, [10..18] their segments,
     // [36..37] the start's bracket after the first rounds
     uint64_t ts0 = 0, te0 = 0;
     constexpr int W_PROD = L::kCW, W_SCHED = L::kCW + 1, W_TAIL = L::kCW + 2,
                   W_STORE = L::kCW + 3;
-    ts0 = args.starts[c];  // static range, weighted by the host (kernel arguments)
-    te0 = args.starts[c + 1];
+    ts0 = NS * c / G;  // static range
+    te0 = NS * (c + 1) / G;
     // boundaries ts0+1 .. ts0+known are co-ranked at start-up by the consumer warps
     const int known = te0 > ts0 ? (te0 - ts0 < 8 ? int(te0 - ts0) : 8) : 0;
     // large plain merges: the scheduler narrows the start's bracket to one tile,
@@ -882,8 +879,6 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
     uint32_t* __restrict__ outv = args.outv;
     unsigned long long data_wait = 0;  // ns consumers waited for stage data
     unsigned long long ph[4] = {0, 0, 0, 0};  // trace: merge, barrier 1, staging+barrier 2, store
-    uint32_t s_done = 0;
-    unsigned long long t_stream = 0;   // when the first tile's data arrived
     for (uint32_t s = 0;; ++s) {
         const int st = int(s % NST);
         if (args.trace && tid == 0) {
@@ -892,11 +887,9 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             data_wait += globaltimer_ns() - w0;
         }
         mbar_wait_sleepy(&full[st], uint32_t((s / NST) & 1), 500);
-        if (s == 0) t_stream = globaltimer_ns();
         const uint64_t* mt = meta + 8 * st;
         const uint64_t packed = mt[3];
         if (packed >> 63) {
-            s_done = s;
             if (tid == 0) mbar_arrive(&staged[st]);  // the store warp sees the end marker
             break;
         }
@@ -973,14 +966,6 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             }
         }
         if (args.trace && tid == 0 && s == 0) args.trace[8 * c + 2] = globaltimer_ns();
-    }
-    if (args.perf && tid == 0) {
-        uint32_t smid;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        args.perf[4 * c] = smid;
-        args.perf[4 * c + 1] = globaltimer_ns() - t_stream;
-        args.perf[4 * c + 2] = s_done;
-        args.perf[4 * c + 3] = 1;  // valid
     }
     if (args.trace && tid == 0) {
         args.trace[8 * c + 3] = globaltimer_ns();

@@ -1,5 +1,6 @@
-for c in C2 X1 C4 C3; do
- for f in 0 1 0 1; do
-  echo "$c flags=$f $(timeout 120 python tools/run_config.py $c --reps 5 --flags $f --trace 2>&1 | grep -E 'rep 4|first tile|startup' | tr '\n' ' ')"
+timeout 300 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
+for c in C2 X1 C4 C3 C5; do
+ for sp in 0 60 65 70 80; do
+  echo "$c sp=$sp $(timeout 120 python tools/run_config.py $c --reps 6 --static-pct $sp 2>&1 | grep -E 'rep 5' | tr '\n' ' ')"
  done
 done
