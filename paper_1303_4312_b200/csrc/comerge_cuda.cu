@@ -530,28 +530,72 @@ host_streams& hstreams() {
     return hs;
 }
 
+// Key and payload windows of one chunk side go over PCIe as ONE 2-row
+// cudaMemcpy2DAsync when the two arrays are a fixed positive pitch apart on
+// both sides (measured: 6 separate copies per chunk cost ~1 ms more per C2
+// merge than 3 two-row copies; every extra copy command costs ~40 us here).
+// The device rows are laid out to match the host order (`swap`).
+struct pair_copy {
+    static size_t max_pitch() {
+        static const size_t v = [] {
+            int dev = 0, p = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&p, cudaDevAttrMaxPitch, dev);
+            return size_t(p);
+        }();
+        return v;
+    }
+    // host arrays x, y: device rows are dev (first) and dev + P (second)
+    static bool swapped(const void* x, const void* y) { return y < x; }
+    // copy `width` bytes of host rows hx, hy <-> device rows dx, dy
+    static cudaError_t run(void* dx, void* dy, const void* sx, const void* sy, size_t width,
+                           cudaMemcpyKind kind, cudaStream_t st) {
+        if (width == 0) return cudaSuccess;
+        const char *s0 = static_cast<const char*>(sx), *s1 = static_cast<const char*>(sy);
+        char *d0 = static_cast<char*>(dx), *d1 = static_cast<char*>(dy);
+        if (s1 < s0) {
+            std::swap(s0, s1);
+            std::swap(d0, d1);
+        }
+        const size_t sp = size_t(s1 - s0);
+        const bool dpos = d1 > d0;
+        const size_t dp = dpos ? size_t(d1 - d0) : 0;
+        if (dpos && sp >= width && dp >= width && sp <= max_pitch() && dp <= max_pitch()) {
+            if (cudaMemcpy2DAsync(d0, dp, s0, sp, width, 2, kind, st) == cudaSuccess)
+                return cudaSuccess;
+            cudaGetLastError();  // fall back to two copies
+        }
+        cudaError_t e = cudaMemcpyAsync(d0, s0, width, kind, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d1, s1, width, kind, st);
+        return e;
+    }
+};
+
 template <typename K, bool HAS_V>
 int merge_host_pipeline(const K* a, const uint32_t* av, uint64_t m, const K* b,
                         const uint32_t* bv, uint64_t n, K* out, uint32_t* outv, uint64_t* h2d,
                         uint64_t* d2h, uint64_t* merge_ns) {
     host_streams& hs = hstreams();
     const uint64_t total = m + n;
+    // `parts` equal output chunks of at least 2^18 elements (more chunks
+    // shorten the fill / drain but every copy command costs ~4-16 us on this
+    // PCIe path: 8 measured best for C2)
     static const uint64_t parts = [] {
         const char* e = std::getenv("COMERGE_HOST_CHUNKS");  // tuning knob (benchmarking)
         const long v = e ? std::atol(e) : 0;
         return uint64_t(v > 0 ? v : 8);
     }();
-    const uint64_t chunk = total / parts > (uint64_t(1) << 18) ? total / parts : (uint64_t(1) << 18);
+    const uint64_t chunk = std::max(div_up(total, parts), uint64_t(1) << 18);
     const uint64_t nchunks = div_up(total, chunk);
+    std::vector<uint64_t> cuts(nchunks + 1);
+    for (uint64_t c = 0; c <= nchunks; ++c) cuts[c] = std::min(total, c * chunk);
     // chunk boundaries: the Lemma-1 split of every chunk start, on host data
     std::vector<uint64_t> js(nchunks + 1);
-    for (uint64_t c = 0; c <= nchunks; ++c) {
-        const uint64_t i = c * chunk < total ? c * chunk : total;
-        js[c] = co_rank_split<K, uint64_t>(i, a, m, b, n, [](const K* p) { return *p; });
-    }
+    for (uint64_t c = 0; c <= nchunks; ++c)
+        js[c] = co_rank_split<K, uint64_t>(cuts[c], a, m, b, n, [](const K* p) { return *p; });
     // three slots of device windows (A, B, out [+ payloads]) from the pool
     const size_t kb = chunk * sizeof(K), vb = HAS_V ? chunk * 4 : 0;
-    const size_t slot_bytes = round256(kb) * 3 + round256(vb) * 3;
+    const size_t slot_bytes = 6 * (round256(kb) > round256(vb) ? round256(kb) : round256(vb));
     void* buf = nullptr;
     cudaError_t e = pool_alloc(&buf, 3 * slot_bytes, hs.comp);
     if (e != cudaSuccess) return cuda_fail(e, "comerge: host pipeline staging");
@@ -562,20 +606,31 @@ int merge_host_pipeline(const K* a, const uint32_t* av, uint64_t m, const K* b,
     for (uint64_t c = 0; c < nchunks && rc == COMERGE_OK; ++c) {
         const int sl = int(c % 3);
         unsigned char* base = static_cast<unsigned char*>(buf) + sl * slot_bytes;
-        K* dA = reinterpret_cast<K*>(base);
-        K* dB = reinterpret_cast<K*>(base + round256(kb));
-        K* dO = reinterpret_cast<K*>(base + 2 * round256(kb));
-        uint32_t* dAv = reinterpret_cast<uint32_t*>(base + 3 * round256(kb));
-        uint32_t* dBv = dAv + round256(vb) / 4;
-        uint32_t* dOv = dBv + round256(vb) / 4;
-        const uint64_t i0 = c * chunk, i1 = i0 + chunk < total ? i0 + chunk : total;
+        // slot: [A-pair | B-pair | out-pair], each pair's rows P apart, keys
+        // first unless the host payload array lies below the host key array
+        const size_t P = round256(kb) > round256(vb) ? round256(kb) : round256(vb);
+        auto row = [&](int pair, bool second) { return base + size_t(pair) * 2 * P + (second ? P : 0); };
+        const bool sa = HAS_V && pair_copy::swapped(a, av), sb = HAS_V && pair_copy::swapped(b, bv);
+        const bool so = HAS_V && pair_copy::swapped(out, outv);
+        K* dA = reinterpret_cast<K*>(row(0, sa));
+        uint32_t* dAv = reinterpret_cast<uint32_t*>(row(0, !sa));
+        K* dB = reinterpret_cast<K*>(row(1, sb));
+        uint32_t* dBv = reinterpret_cast<uint32_t*>(row(1, !sb));
+        K* dO = reinterpret_cast<K*>(row(2, so));
+        uint32_t* dOv = reinterpret_cast<uint32_t*>(row(2, !so));
+        const uint64_t i0 = cuts[c], i1 = cuts[c + 1];
         const uint64_t j0 = js[c], j1 = js[c + 1], k0 = i0 - j0, k1 = i1 - j1;
         if (c >= 3) cudaStreamWaitEvent(hs.h2d, hs.out_done[sl], 0);  // slot free again
-        if (j1 > j0) cudaMemcpyAsync(dA, a + j0, (j1 - j0) * sizeof(K), cudaMemcpyHostToDevice, hs.h2d);
-        if (k1 > k0) cudaMemcpyAsync(dB, b + k0, (k1 - k0) * sizeof(K), cudaMemcpyHostToDevice, hs.h2d);
-        if (HAS_V) {
-            if (j1 > j0) cudaMemcpyAsync(dAv, av + j0, (j1 - j0) * 4, cudaMemcpyHostToDevice, hs.h2d);
-            if (k1 > k0) cudaMemcpyAsync(dBv, bv + k0, (k1 - k0) * 4, cudaMemcpyHostToDevice, hs.h2d);
+        if (HAS_V && sizeof(K) == 4) {  // keys and payloads of a side in one command
+            pair_copy::run(dA, dAv, a + j0, av + j0, (j1 - j0) * 4, cudaMemcpyHostToDevice, hs.h2d);
+            pair_copy::run(dB, dBv, b + k0, bv + k0, (k1 - k0) * 4, cudaMemcpyHostToDevice, hs.h2d);
+        } else {
+            if (j1 > j0) cudaMemcpyAsync(dA, a + j0, (j1 - j0) * sizeof(K), cudaMemcpyHostToDevice, hs.h2d);
+            if (k1 > k0) cudaMemcpyAsync(dB, b + k0, (k1 - k0) * sizeof(K), cudaMemcpyHostToDevice, hs.h2d);
+            if (HAS_V) {
+                if (j1 > j0) cudaMemcpyAsync(dAv, av + j0, (j1 - j0) * 4, cudaMemcpyHostToDevice, hs.h2d);
+                if (k1 > k0) cudaMemcpyAsync(dBv, bv + k0, (k1 - k0) * 4, cudaMemcpyHostToDevice, hs.h2d);
+            }
         }
         *h2d += (i1 - i0) * (sizeof(K) + (HAS_V ? 4 : 0));
         cudaEventRecord(hs.in_done[sl], hs.h2d);
@@ -588,8 +643,12 @@ int merge_host_pipeline(const K* a, const uint32_t* av, uint64_t m, const K* b,
                                     k1 - k0, dO, HAS_V ? dOv : nullptr, nullptr, 0, hs.comp);
         cudaEventRecord(hs.merged[sl], hs.comp);
         cudaStreamWaitEvent(hs.d2h, hs.merged[sl], 0);
-        cudaMemcpyAsync(out + i0, dO, (i1 - i0) * sizeof(K), cudaMemcpyDeviceToHost, hs.d2h);
-        if (HAS_V) cudaMemcpyAsync(outv + i0, dOv, (i1 - i0) * 4, cudaMemcpyDeviceToHost, hs.d2h);
+        if (HAS_V && sizeof(K) == 4) {
+            pair_copy::run(out + i0, outv + i0, dO, dOv, (i1 - i0) * 4, cudaMemcpyDeviceToHost, hs.d2h);
+        } else {
+            cudaMemcpyAsync(out + i0, dO, (i1 - i0) * sizeof(K), cudaMemcpyDeviceToHost, hs.d2h);
+            if (HAS_V) cudaMemcpyAsync(outv + i0, dOv, (i1 - i0) * 4, cudaMemcpyDeviceToHost, hs.d2h);
+        }
         *d2h += (i1 - i0) * (sizeof(K) + (HAS_V ? 4 : 0));
         cudaEventRecord(hs.out_done[sl], hs.d2h);
     }
