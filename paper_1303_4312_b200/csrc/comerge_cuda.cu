@@ -283,6 +283,21 @@ int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const ui
     // (their random probes hit L2; on large inputs they would contend in HBM)
     args.eager_start = total * sizeof(K) <= (size_t(32) << 20) ? 1u : 0u;
     args.flags = uint32_t(g_tune_flags);
+    // scheduler look-ahead (see merge_pipe.cuh); experiment flags override:
+    // bits 2-3 pass cap (1: 8, 2: 16, 3: 32), bits 4-7 look-ahead / 4,
+    // bit 8 / bit 9 force the store hint on / off
+    args.sched_cap = 8;
+    args.sched_ahead = 8;
+    // 64-bit keys: probes are a larger share of the traffic, and keeping the
+    // streamed output out of L2's way keeps them resident until the load
+    // (C4 1051 -> 1028 us); for 32-bit keys the hint costs more than it saves
+    // (the output left dirty in L2 at kernel end is written back after it)
+    args.store_evict_first = sizeof(K) == 8 ? 1u : 0u;
+    if (const uint32_t c = (uint32_t(g_tune_flags) >> 2) & 3u) args.sched_cap = 4u << c;
+    if (const uint32_t a = (uint32_t(g_tune_flags) >> 4) & 15u) args.sched_ahead = 4u * a;
+    if (args.sched_ahead < args.sched_cap) args.sched_ahead = args.sched_cap;
+    if (g_tune_flags & 256) args.store_evict_first = 1;
+    if (g_tune_flags & 512) args.store_evict_first = 0;
     g_last_path = SEG ? 5 : 3;
     mark_before(s);
     merge_pipe_kernel<K, HAS_V, SEG><<<grid, PL::kThreads, PL::kSmem, s>>>(args);

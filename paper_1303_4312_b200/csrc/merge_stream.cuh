@@ -116,6 +116,15 @@ __device__ __forceinline__ void tma_store_1d(void* dst, const void* src, uint32_
                  : "memory");
 }
 
+// bulk store with an L2 eviction-priority hint (streamed output: evict_first
+// keeps it from displacing lines that are read again soon)
+__device__ __forceinline__ void tma_store_1d_hint(void* dst, const void* src, uint32_t bytes,
+                                                  uint64_t policy) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes), "l"(policy)
+                 : "memory");
+}
+
 __device__ __forceinline__ void tma_store_commit() {
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }

@@ -64,6 +64,17 @@ __device__ __forceinline__ T ldg_elem(const T* p) {
         return __ldg(p);
 }
 
+// A co-rank probe: one scattered element, cached in L2 only.  (Through the
+// read-only L1 path every probe fetched a whole 128-byte line -- ncu: L2
+// requests of C4 exceeded the window bytes by 3.5 sectors per probe.)
+template <typename T>
+__device__ __forceinline__ T probe_elem(const T* p) {
+    if constexpr (sizeof(T) == 8)
+        return static_cast<T>(__ldcg(reinterpret_cast<const unsigned long long*>(p)));
+    else
+        return __ldcg(p);
+}
+
 // Stage src[lo, hi) into shared memory: element x lands at
 // dst[x - (lo & ~(VEC-1))], so 16-byte vectors of src map onto 16-byte
 // aligned shared-memory slots.  Vectors that straddle the array end (or any

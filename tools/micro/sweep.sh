@@ -1,6 +1,3 @@
 timeout 300 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
-for c in C2 X1 C4 C3 C5; do
- for sp in 0 60 65 70 80; do
-  echo "$c sp=$sp $(timeout 120 python tools/run_config.py $c --reps 6 --static-pct $sp 2>&1 | grep -E 'rep 5' | tr '\n' ' ')"
- done
-done
+timeout 300 python tools/ab.py C4 0,512 --rounds 2
+for c in C1 C2 C3 C5; do timeout 300 python tools/ab.py $c 0 --rounds 2; done
