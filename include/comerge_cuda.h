@@ -70,7 +70,8 @@ void comerge_cuda_set_path(int path);
 /* Kernel used by the last merge on this thread: 1 = tile kernel (partition
  * + merge launches), 2 = ring-streaming kernel (one launch), 3 = tile
  * pipeline (one launch), 4 = segmented tile kernel (partition + merge),
- * 5 = segmented tile pipeline (one launch), 0 = none yet. */
+ * 5 = segmented tile pipeline (one launch), 6 = merge pass of the sort
+ * (tile pipeline over runs), 0 = none yet. */
 int comerge_cuda_last_path(void);
 /* Host-buffer strategy of the synchronous entry points on this thread
  * (testing / benchmarking): 0 = chunked pipeline (default: output chunks
@@ -144,6 +145,21 @@ int comerge_cuda_merge_segmented_u32(const uint32_t* a, const uint64_t* a_off, s
                                      const uint32_t* b, const uint64_t* b_off, size_t n,
                                      size_t nseg, uint32_t* out, void* ws, size_t ws_bytes,
                                      comerge_stream_t stream);
+
+/* Stable merge sort (the merge path's natural consumer; no
+ * reference counterpart -- its result is std::stable_sort's, i.e. repeated
+ * stable_merge of adjacent runs, merge.hpp:52-68): keys[0, n) -> out[0, n),
+ * out may equal keys (in place) but must not partially overlap it.  Block
+ * sort of runs in shared memory, then log2(n / run) merge passes of the tile
+ * pipeline.  Workspace from comerge_cuda_sort_workspace_bytes (NULL: the
+ * library pool).  Up to 2^40 keys. */
+size_t comerge_cuda_sort_workspace_bytes(size_t n, int key_kind);
+int comerge_cuda_sort_keys_i32(const int32_t* keys, size_t n, int32_t* out, void* ws,
+                               size_t ws_bytes, comerge_stream_t stream);
+int comerge_cuda_sort_keys_u32(const uint32_t* keys, size_t n, uint32_t* out, void* ws,
+                               size_t ws_bytes, comerge_stream_t stream);
+int comerge_cuda_sort_keys_u64(const uint64_t* keys, size_t n, uint64_t* out, void* ws,
+                               size_t ws_bytes, comerge_stream_t stream);
 
 /* Batched co-rank (Algorithm 1 exactly, corank.hpp:72-121): for each
  * ranks[q] (device array) writes j (k = ranks[q] - j) and, if the pointers

@@ -212,6 +212,35 @@ void oracle_merge_into(int kind, const void* a, const uint32_t* av, uint64_t m, 
     }
 }
 
+/* ------------------------------------------- merge sort (test oracle only) */
+
+int oracle_merge_sort(int kind, const void* in, uint64_t n, void* out) {
+    const size_t s = key_size(kind);
+    char* x = (char*)malloc(n ? n * s : 1);
+    char* y = (char*)malloc(n ? n * s : 1);
+    if (!x || !y) {
+        free(x);
+        free(y);
+        return -1;
+    }
+    memcpy(x, in, n * s);
+    for (uint64_t w = 1; w < n; w *= 2) {  /* merge runs 2q and 2q+1 of length w */
+        for (uint64_t lo = 0; lo < n; lo += 2 * w) {
+            const uint64_t mid = lo + w < n ? lo + w : n;
+            const uint64_t hi = lo + 2 * w < n ? lo + 2 * w : n;
+            oracle_merge_into(kind, x + lo * s, NULL, mid - lo, x + mid * s, NULL, hi - mid,
+                              y + lo * s, NULL);
+        }
+        char* t = x;
+        x = y;
+        y = t;
+    }
+    memcpy(out, x, n * s);
+    free(x);
+    free(y);
+    return 0;
+}
+
 /* ---------------------------------------------- Algorithm 2 (parallel.hpp) */
 
 typedef struct {

@@ -60,6 +60,7 @@ class Port:
         lib.oracle_merge_parallel.argtypes = [C.c_int, _p, _p, _u64, _p, _p, _u64, _p, _p, _u64,
                                               C.c_int, _p, _p]
         lib.oracle_merge_segmented.argtypes = [C.c_int, _p, _p, _p, _p, _u64, _p, C.c_int]
+        lib.oracle_merge_sort.argtypes = [C.c_int, _p, _u64, _p]
         lib.oracle_generate_sorted.argtypes = [C.c_int, _u64, _u64, _u64, _u64, _p]
         lib.oracle_generate_sorted.restype = None
         lib.oracle_generate_raw.argtypes = [_u64, _u64, _u64, _u64, _p]
@@ -110,6 +111,14 @@ class Port:
         rc = self.lib.oracle_merge_segmented(kind_of(a), ptr(a), ptr(a_off), ptr(b), ptr(b_off),
                                              nseg, ptr(out), threads)
         _raise(rc, "merge_segmented: offsets must be nondecreasing")
+        return out
+
+    def merge_sort(self, keys):
+        keys = np.ascontiguousarray(keys)
+        out = np.empty_like(keys)
+        rc = self.lib.oracle_merge_sort(kind_of(keys), ptr(keys), len(keys), ptr(out))
+        if rc:
+            raise MemoryError("oracle_merge_sort: allocation failed")
         return out
 
     def generate_sorted(self, dtype, seed, lane, length, width):

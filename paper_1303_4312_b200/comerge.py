@@ -359,3 +359,28 @@ def merge_segmented(a, a_off, b, b_off, out=None, workspace=None):
         _ptr(a), _ptr(a_off), _len(a), _ptr(b), _ptr(b_off), _len(b), max(nseg, 0), _ptr(out),
         wsp, wsb, _stream(a)))
     return out
+
+
+def sort_workspace_bytes(n, dtype):
+    """Workspace for sort() of n keys of `dtype` (CUB-style query)."""
+    name = str(dtype).replace("torch.", "") if torch is not None and isinstance(dtype, torch.dtype) \
+        else np.dtype(dtype).name
+    return int(N.lib.comerge_cuda_sort_workspace_bytes(int(n), _KIND[_SUFFIX[name]]))
+
+
+def sort(keys, out=None, workspace=None):
+    """Stable merge sort of a device tensor of int32 / uint32 / uint64 keys
+    (block-sorted runs, then merge passes of the pipeline).
+    ``out`` may be ``keys`` itself (in place)."""
+    if not (_is_torch(keys) and keys.is_cuda):
+        raise TypeError("sort: keys must be a CUDA tensor (there is no host path)")
+    suf = _suffix(keys)
+    if out is None:
+        out = _empty_like_merge(keys, _len(keys))
+    if _len(out) != _len(keys):
+        raise ValueError("sort: output length must equal the input length")
+    wsp, wsb = _ws(workspace)
+    N.check(getattr(N.lib, f"comerge_cuda_sort_keys_{suf}")(
+        _ptr(keys), _len(keys), _ptr(out), wsp, wsb, _stream(keys)))
+    return out
+

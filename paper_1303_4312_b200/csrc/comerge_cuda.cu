@@ -18,6 +18,7 @@
 #include "merge_pipe.cuh"
 #include "merge_stream.cuh"
 #include "merge_tile.cuh"
+#include "sort.cuh"
 
 using namespace comerge_b200;
 
@@ -43,7 +44,7 @@ int sm_count() {
 }
 
 // Persistent grid size for the tile-pipeline kernel (resident CTAs, cached).
-template <typename K, bool HAS_V, bool SEG>
+template <typename K, bool HAS_V, int SEG>
 int pipe_grid_limit() {
     static const int limit = [] {
         using L = pipe_layout<K, HAS_V, SEG>;
@@ -202,7 +203,7 @@ template <typename K>
 size_t seg_ws_bytes(size_t total) {
     if (total == 0) return 0;
     const size_t tile_ws = 2 * round256((div_up(total, seg_cfg<K>::kTile) + 1) * sizeof(uint64_t));
-    const size_t pipe_ws = round256(32 * (div_up(total, pipe_layout<K, false, true>::T) + 2));
+    const size_t pipe_ws = round256(32 * (div_up(total, pipe_layout<K, false, 1>::T) + 2));
     return tile_ws > pipe_ws ? tile_ws : pipe_ws;
 }
 
@@ -236,10 +237,10 @@ int check_merge_args(const char* who, const K* a, size_t m, const K* b, size_t n
 
 // Launch the persistent tile pipeline (merge_pipe.cuh) for a plain merge or a
 // segmented batch (aoff/boff/nseg).  Scratch: the dynamic-tail state.
-template <typename K, bool HAS_V, bool SEG>
+template <typename K, bool HAS_V, int SEG>
 int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const uint32_t* bv,
                 uint64_t n, K* out, uint32_t* outv, const uint64_t* aoff, const uint64_t* boff,
-                uint64_t nseg, void* ws, size_t ws_bytes, cudaStream_t s) {
+                uint64_t nseg, void* ws, size_t ws_bytes, cudaStream_t s, uint64_t run_len = 0) {
     using PL = pipe_layout<K, HAS_V, SEG>;
     const uint64_t total = m + n;
     const uint64_t ptiles = div_up(total, PL::T);
@@ -259,6 +260,7 @@ int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const ui
     args.aoff = aoff;
     args.boff = boff;
     args.nseg = nseg;
+    args.run_len = run_len;
     args.trace = g_trace;
     // equal static split of 70% of the tiles + a dynamic tail of 30%: the tail
     // absorbs the start-up skew (~10 us between the first and last CTA to
@@ -298,7 +300,7 @@ int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const ui
     if (args.sched_ahead < args.sched_cap) args.sched_ahead = args.sched_cap;
     if (g_tune_flags & 256) args.store_evict_first = 1;
     if (g_tune_flags & 512) args.store_evict_first = 0;
-    g_last_path = SEG ? 5 : 3;
+    g_last_path = SEG == 2 ? 6 : (SEG ? 5 : 3);
     mark_before(s);
     merge_pipe_kernel<K, HAS_V, SEG><<<grid, PL::kThreads, PL::kSmem, s>>>(args);
     mark_after(s);
@@ -321,7 +323,7 @@ int merge_device(const K* a, const uint32_t* av, size_t m, const K* b, const uin
     using PL = pipe_layout<K, HAS_V>;
     const uint64_t ptiles = div_up(total, PL::T);
     if (aligned_all && (g_path == 3 || (g_path == 0 && ptiles >= 16)))
-        return launch_pipe<K, HAS_V, false>(a, av, m, b, bv, n, out, outv, nullptr, nullptr, 0, ws,
+        return launch_pipe<K, HAS_V, 0>(a, av, m, b, bv, n, out, outv, nullptr, nullptr, 0, ws,
                                             ws_bytes, s);
     if (aligned_all && g_path == 2) {
         const int limit = stream_grid_limit<K, HAS_V>();
@@ -373,7 +375,7 @@ int merge_segmented_device(const K* a, const uint64_t* a_off, size_t m, const K*
     using PL = pipe_layout<K, false>;
     if (aligned16(a) && aligned16(b) && aligned16(out) && g_path != 1 &&
         (g_path == 3 || div_up(total, PL::T) >= 16))
-        return launch_pipe<K, false, true>(a, nullptr, m, b, nullptr, n, out, nullptr, a_off, b_off,
+        return launch_pipe<K, false, 1>(a, nullptr, m, b, nullptr, n, out, nullptr, a_off, b_off,
                                            nseg, ws, ws_bytes, s);
     constexpr int T = seg_cfg<K>::kTile;
     const uint64_t ntiles = div_up(total, T);
@@ -904,6 +906,67 @@ int co_rank_sync(uint64_t target, const K* a, size_t m, const K* b, size_t n, ui
 
 }  // namespace
 
+// ------------------------------------------------------------ merge sort
+// Stable sort of keys[0, n) into out (may equal keys): block sort of runs of
+// R = sort_cfg<K>::R, then log2(n / R) merge passes of the pipeline in
+// merge-pass mode (sort.cuh).  Workspace: one n-element buffer (two when out
+// is not 16-byte aligned) plus the pipeline's tail slots.
+template <typename K>
+size_t sort_ws_bytes(size_t n) {
+    if (n == 0) return 0;
+    const size_t buf = round256(n * sizeof(K));
+    const size_t tail = round256(32 * (div_up(n, pipe_layout<K, false, 1>::T) + 2));
+    return 2 * buf + tail;
+}
+
+template <typename K>
+int sort_device(const K* keys, size_t n, K* out, void* ws, size_t ws_bytes, cudaStream_t s) {
+    if (n && (!keys || !out)) return fail(COMERGE_E_INVALID, "sort: null pointer");
+    if (n == 0) return COMERGE_OK;
+    if (n > (size_t(1) << 40)) return fail(COMERGE_E_LENGTH, "sort: more than 2^40 elements");
+    if (keys != out && overlaps(keys, n * sizeof(K), out, n * sizeof(K)))
+        return fail(COMERGE_E_INVALID, "sort: output must not partially overlap the input");
+    constexpr uint64_t R = sort_cfg<K>::R;
+    const uint64_t nblocks = div_up(n, R);
+    uint32_t passes = 0;
+    while ((R << passes) < n) ++passes;
+    if (passes == 0) {
+        block_sort_kernel<K><<<unsigned(nblocks), sort_cfg<K>::NT, 0, s>>>(keys, out, n);
+        return check_launch("comerge: block sort launch");
+    }
+    scratch sc;
+    if (int rc = sc.acquire(ws, ws_bytes, sort_ws_bytes<K>(n), s)) return rc;
+    unsigned char* w = static_cast<unsigned char*>(sc.ptr);
+    const size_t buf = round256(n * sizeof(K));
+    K* t0 = reinterpret_cast<K*>(w);
+    K* t1 = reinterpret_cast<K*>(w + buf);
+    unsigned char* tail = w + 2 * buf;
+    const size_t tail_bytes = sort_ws_bytes<K>(n) - 2 * buf;
+    // ping-pong so the last pass lands in out (or in t0, then one copy when out
+    // is not 16-byte aligned for the pipeline's bulk stores)
+    const bool direct = aligned16(out);
+    K* bufs[2] = {direct ? out : t1, t0};  // bufs[x]: the result of a stage with passes-left parity x
+    K* cur = bufs[passes & 1];
+    block_sort_kernel<K><<<unsigned(nblocks), sort_cfg<K>::NT, 0, s>>>(keys, cur, n);
+    if (int rc = check_launch("comerge: block sort launch")) return rc;
+    uint64_t L = R;
+    for (uint32_t p = 0; p < passes; ++p, L *= 2) {
+        K* dst = bufs[(passes - p - 1) & 1];
+        const uint64_t full = n / (2 * L), rem = n % (2 * L);
+        const uint64_t ma = full * L + (rem < L ? rem : L), mb = n - ma;
+        const uint64_t nseg = div_up(n, 2 * L);
+        if (int rc = launch_pipe<K, false, 2>(cur, nullptr, ma, cur, nullptr, mb, dst, nullptr,
+                                                 nullptr, nullptr, nseg, tail, tail_bytes, s, L))
+            return rc;
+        cur = dst;
+    }
+    if (cur != out) {
+        const cudaError_t e = cudaMemcpyAsync(out, cur, n * sizeof(K), cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) return cuda_fail(e, "comerge: sort result copy");
+    }
+    return COMERGE_OK;
+}
+
 extern "C" {
 
 const char* comerge_cuda_last_error(void) { return g_error.c_str(); }
@@ -989,6 +1052,22 @@ int comerge_cuda_merge_segmented_u32(const uint32_t* a, const uint64_t* a_off, s
                                      comerge_stream_t stream) {
     return merge_segmented_device<uint32_t>(a, a_off, m, b, b_off, n, nseg, out, ws, ws_bytes,
                                             stream);
+}
+
+size_t comerge_cuda_sort_workspace_bytes(size_t n, int key_kind) {
+    return key_kind == COMERGE_KEY_U64 ? sort_ws_bytes<uint64_t>(n) : sort_ws_bytes<uint32_t>(n);
+}
+int comerge_cuda_sort_keys_i32(const int32_t* keys, size_t n, int32_t* out, void* ws,
+                               size_t ws_bytes, comerge_stream_t stream) {
+    return sort_device<int32_t>(keys, n, out, ws, ws_bytes, stream);
+}
+int comerge_cuda_sort_keys_u32(const uint32_t* keys, size_t n, uint32_t* out, void* ws,
+                               size_t ws_bytes, comerge_stream_t stream) {
+    return sort_device<uint32_t>(keys, n, out, ws, ws_bytes, stream);
+}
+int comerge_cuda_sort_keys_u64(const uint64_t* keys, size_t n, uint64_t* out, void* ws,
+                               size_t ws_bytes, comerge_stream_t stream) {
+    return sort_device<uint64_t>(keys, n, out, ws, ws_bytes, stream);
 }
 
 int comerge_partition_output(uint64_t total, uint64_t workers, uint64_t r, uint64_t* out) {

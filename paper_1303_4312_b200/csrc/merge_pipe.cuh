@@ -81,7 +81,9 @@ struct pipe_cfg<uint64_t, true> {
     static constexpr int NC = 256, VT = 11, NST = 3;
 };
 
-template <typename K, bool HAS_V, bool SEG = false>
+// SEG: 0 plain merge, 1 segmented batch (explicit offsets), 2 merge pass
+// (runs of run_len, implicit offsets; sort.cuh)
+template <typename K, bool HAS_V, int SEG = 0>
 struct pipe_layout {
     using C = pipe_cfg<K, HAS_V>;
     static constexpr int kConsumers = C::NC;
@@ -140,6 +142,12 @@ struct pipe_args {
     uint32_t sched_cap;          // most boundaries co-ranked per scheduler pass (<= 32)
     uint32_t sched_ahead;        // most descriptors queued beyond the producer (<= NB, >= sched_cap)
     uint32_t store_evict_first;  // output stores with an L2 evict_first hint
+    // merge-pass mode (SEG only; sort passes): a == b == one array of sorted
+    // runs of run_len elements, segment s pairs run 2s (its A part) with run
+    // 2s+1 (its B part); offsets are implicit: aoff(s) = min(s*L, m),
+    // boff(s) = min(s*L, n), A index x at element x + (x/L)*L, B index y at
+    // y + (y/L + 1)*L; aoff / boff are NULL.  0 = explicit offsets.
+    uint64_t run_len;
 };
 
 // Lane-group (P+1)-ary search for the largest q in [lo, hi] with !pred(q),
@@ -211,9 +219,51 @@ __device__ __forceinline__ uint32_t stage_copy_plan(const E* __restrict__ src, u
     return uint32_t((hi_al - lo_al) * sizeof(E));
 }
 
+// Merge pass: stage the window [x0, x1) of one side's index space, element x
+// at src[x + (x/L + shift) * L] (shift 0 for A, 1 for B), as one TMA copy per
+// run it touches (runs are physically contiguous; L is a multiple of vece, so
+// every piece after the first starts 16-byte aligned at its place in `dst`,
+// which corresponds to index x0 - x0 % vece).  issue == false: plan only
+// (scalar tails copied, bytes returned); issue == true: the copies.
+template <typename E>
+__device__ __forceinline__ uint32_t stage_runs(const E* __restrict__ src, uint64_t phys_len,
+                                               uint64_t x0, uint64_t x1, uint64_t L,
+                                               uint64_t shift, E* dst, int vece, bool issue,
+                                               uint64_t* bar, uint64_t policy) {
+    uint32_t total = 0;
+    const uint64_t base = x0 - x0 % vece;
+    for (uint64_t x = x0; x < x1;) {
+        const uint64_t run = x / L;
+        const uint64_t y = x1 < (run + 1) * L ? x1 : (run + 1) * L;
+        const uint64_t sh = (run + shift) * L;  // physical = index + sh
+        E* d = dst + ((x - x % vece) - base);
+        if (!issue) {
+            total += stage_copy_plan(src, phys_len, x + sh, y + sh, d, vece);
+        } else {
+            const uint64_t lo = x + sh, lo_al = lo - lo % vece;
+            uint64_t hi_al = (y + sh + vece - 1) / vece * vece;
+            const uint64_t len_al = phys_len - phys_len % vece;
+            if (hi_al > phys_len) hi_al = len_al > lo_al ? len_al : lo_al;
+            const uint32_t bytes = uint32_t((hi_al - lo_al) * sizeof(E));
+            if (bytes) tma_load_1d(d, src + lo_al, bytes, bar, policy);
+            total += bytes;
+        }
+        x = y;
+    }
+    return total;
+}
+
 __device__ __forceinline__ uint64_t ldg_u64(const uint64_t* p) {  // L2-only, like probe_elem
     return static_cast<uint64_t>(__ldcg(reinterpret_cast<const unsigned long long*>(p)));
 }
+
+// merge-pass mode: implicit offsets and element positions (see pipe_args)
+__device__ __forceinline__ uint64_t run_off(uint64_t s, uint64_t L, uint64_t len) {
+    const uint64_t o = s * L;
+    return o < len ? o : len;
+}
+__device__ __forceinline__ uint64_t run_pos_a(uint64_t x, uint64_t L) { return x + (x / L) * L; }
+__device__ __forceinline__ uint64_t run_pos_b(uint64_t y, uint64_t L) { return y + (y / L + 1) * L; }
 
 // A tile boundary: co-rank j of output rank i and, for segmented batches, the
 // segment s that holds it (largest s with aoff[s] + boff[s] <= i).
@@ -227,7 +277,7 @@ struct boundary {
 // (L2-resident) offsets, then the co-rank inside that segment (the batch is
 // one merge over (segment, key) composites, so the split of a rank inside
 // segment s is s's own co-rank).
-template <typename K, bool SEG>
+template <typename K, int SEG>
 __device__ __forceinline__ boundary find_boundary(const pipe_args& args, uint64_t i, uint64_t jlo,
                                                   uint64_t jhi, uint64_t slo, int P,
                                                   uint32_t* rounds) {
@@ -236,6 +286,21 @@ __device__ __forceinline__ boundary find_boundary(const pipe_args& args, uint64_
     if constexpr (!SEG) {
         return {group_search<K>(i, jlo, jhi, P, a, b, rounds), 0};
     } else {
+        if constexpr (SEG == 2) {  // merge pass: pair s holds output ranks [2sL, 2sL + 2L)
+            const uint64_t L = args.run_len;
+            uint64_t s = i / (2 * L);
+            if (s > args.nseg - 1) s = args.nseg - 1;
+            const uint64_t as = run_off(s, L, args.m), bs = run_off(s, L, args.n);
+            const uint64_t ma = run_off(s + 1, L, args.m) - as, nb = run_off(s + 1, L, args.n) - bs;
+            const uint64_t li = i - as - bs;
+            uint64_t lo = li > nb ? li - nb : 0, hi = li < ma ? li : ma;
+            if (jlo > as && jlo - as > lo) lo = jlo - as;
+            if (jhi < as + hi) hi = jhi > as ? jhi - as : 0;
+            if (hi < lo) hi = lo;
+            return {as + group_search<K>(li, lo, hi, P, a + run_pos_a(as, L), b + run_pos_b(bs, L),
+                                         rounds),
+                    s};
+        }
         const uint64_t* __restrict__ ao = args.aoff;
         const uint64_t* __restrict__ bo = args.boff;
         uint64_t shi = args.nseg - 1;
@@ -455,7 +520,7 @@ __device__ __forceinline__ void merge_thread_segends(const K* sA, const K* sB, i
     }
 }
 
-template <typename K, bool HAS_V, bool SEG>
+template <typename K, bool HAS_V, int SEG>
 __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_blocks<K, HAS_V>::value)
     merge_pipe_kernel(const pipe_args args) {
     using L = pipe_layout<K, HAS_V, SEG>;
@@ -847,8 +912,12 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             const uint32_t a_off = uint32_t(j0 % VECE);
             const uint32_t b_base = (a_off + a_len + VECE - 1) / VECE * VECE;
             const uint32_t b_off = uint32_t(k0 % VECE);
-            const uint32_t ab = stage_copy_plan(a, m, j0, j1, sk, VECE);
-            const uint32_t bb = stage_copy_plan(b, n, k0, k1, sk + b_base, VECE);
+            const uint64_t RL = SEG == 2 ? args.run_len : 0;  // merge pass (see pipe_args)
+            const uint32_t ab = RL ? stage_runs(a, m + n, j0, j1, RL, 0, sk, VECE, false, nullptr, 0)
+                                   : stage_copy_plan(a, m, j0, j1, sk, VECE);
+            const uint32_t bb = RL ? stage_runs(b, m + n, k0, k1, RL, 1, sk + b_base, VECE, false,
+                                                nullptr, 0)
+                                   : stage_copy_plan(b, n, k0, k1, sk + b_base, VECE);
             uint32_t avb = 0, bvb = 0, av_off = 0, bv_base = 0;
             if constexpr (HAS_V) {
                 av_off = uint32_t(j0 % 4);
@@ -866,7 +935,9 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
                 // the tile's segment offsets s0 .. s1+1 (16-byte aligned superset)
                 const uint64_t olo = seg0 - (seg0 & 1), ohi = seg1 + 2;
                 uint64_t* so = reinterpret_cast<uint64_t*>(stage + L::kStageKeys + L::kStageVals);
-                if (ohi - olo + 1 <= uint64_t(L::SEGCAP)) {
+                if (RL) {
+                    mt[6] = ~uint64_t(0);  // implicit offsets
+                } else if (ohi - olo + 1 <= uint64_t(L::SEGCAP)) {
                     const uint32_t oa = stage_copy_plan(args.aoff, args.nseg + 1, olo, ohi, so, 2);
                     const uint32_t obb =
                         stage_copy_plan(args.boff, args.nseg + 1, olo, ohi, so + L::SEGCAP, 2);
@@ -880,8 +951,13 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
                 }
             }
             if (ob == 0) mbar_arrive_expect_tx(&full[st], ab + bb + avb + bvb);
-            if (ab) tma_load_1d(sk, a + (j0 - j0 % VECE), ab, &full[st], policy);
-            if (bb) tma_load_1d(sk + b_base, b + (k0 - k0 % VECE), bb, &full[st], policy);
+            if (RL) {
+                stage_runs(a, m + n, j0, j1, RL, 0, sk, VECE, true, &full[st], policy);
+                stage_runs(b, m + n, k0, k1, RL, 1, sk + b_base, VECE, true, &full[st], policy);
+            } else {
+                if (ab) tma_load_1d(sk, a + (j0 - j0 % VECE), ab, &full[st], policy);
+                if (bb) tma_load_1d(sk + b_base, b + (k0 - k0 % VECE), bb, &full[st], policy);
+            }
             if constexpr (HAS_V) {
                 if (avb) tma_load_1d(sv, args.av + (j0 - j0 % 4), avb, &full[st], policy);
                 if (bvb)
@@ -927,14 +1003,24 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         if constexpr (SEG) {
             const uint64_t k0 = mt[1];
             const uint64_t s_lo = mt[4], s_hi = mt[5];
-            if (mt[6]) {  // offsets staged: build the segment-end table, then merge
+            if (SEG == 2 && s_lo == s_hi) {  // merge pass, one segment: a plain merge
+                merge_thread<K, VT, false>(sk + a_off, a_len, sk + b_base + b_off, b_len, diag,
+                                           keys, src);
+            } else if (mt[6]) {  // offsets staged: build the segment-end table, then merge
                 const uint64_t* so =
                     reinterpret_cast<const uint64_t*>(stage + L::kStageKeys + L::kStageVals);
                 uint32_t* se = reinterpret_cast<uint32_t*>(smem + L::oSegEnd);
                 const int nse = int(s_hi - s_lo) + 1;
                 if (tid < nse) {
-                    const uint64_t x = s_lo + uint64_t(tid) + 1 - (mt[6] - 1);
-                    const uint64_t ae = so[x], be = so[L::SEGCAP + x];
+                    uint64_t ae, be;
+                    if (SEG == 2) {  // merge pass: implicit offsets
+                        ae = run_off(s_lo + uint64_t(tid) + 1, args.run_len, args.m);
+                        be = run_off(s_lo + uint64_t(tid) + 1, args.run_len, args.n);
+                    } else {
+                        const uint64_t x = s_lo + uint64_t(tid) + 1 - (mt[6] - 1);
+                        ae = so[x];
+                        be = so[L::SEGCAP + x];
+                    }
                     const uint64_t j0 = i0 - k0;
                     const uint32_t x1 = ae > j0 ? uint32_t(min(ae - j0, uint64_t(a_len))) : 0u;
                     const uint32_t y1 = be > k0 ? uint32_t(min(be - k0, uint64_t(b_len))) : 0u;

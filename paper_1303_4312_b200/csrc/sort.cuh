@@ -1,0 +1,100 @@
+// sort.cuh -- stable merge sort built on the merge path (SURVEY.md §8f row 1:
+// "GPU merge sort built on the segmented kernel").
+//
+//   1. block_sort_kernel: every CTA sorts one run of R = NT*VT elements in
+//      shared memory -- VT elements per thread by odd-even transposition in
+//      registers (swap only on strictly-less, so equal keys keep their
+//      order), then log2(NT) rounds of pairwise merges of the sorted lists,
+//      each thread taking VT outputs at its merge-path split (the Lemma-1
+//      split of corank.hpp:93-94, ties to the left list as merge.hpp:22-31).
+//   2. log2(n/R) merge passes of the tile pipeline in merge-pass mode
+//      (merge_pipe.cuh, pipe_args::run_len): pass p merges runs 2s and 2s+1
+//      of length R*2^p as one segmented batch with implicit offsets.
+//
+// The result equals a stable sort (std::stable_sort) of the keys: bottom-up
+// merging of adjacent runs with left-first ties preserves input order.
+#pragma once
+
+#include <cstdint>
+#include <limits>
+
+#include "corank.cuh"
+
+namespace comerge_b200 {
+
+template <typename K>
+struct sort_cfg {
+    static constexpr int NT = 512;
+    static constexpr int VT = sizeof(K) == 8 ? 8 : 16;
+    static constexpr int R = NT * VT;  // base run (a power of two)
+};
+
+// Shared-memory index with one pad word per 32 elements: thread t's VT
+// consecutive elements (t*VT + v) then fall in distinct banks across a warp
+// (without it VT = 16 is a 16-way bank conflict on every staging access).
+__device__ __forceinline__ int spad(int i) { return i + (i >> 5); }
+
+template <typename K>
+__global__ void __launch_bounds__(sort_cfg<K>::NT)
+    block_sort_kernel(const K* __restrict__ in, K* __restrict__ out, uint64_t n) {
+    constexpr int NT = sort_cfg<K>::NT, VT = sort_cfg<K>::VT, R = sort_cfg<K>::R;
+    // + slack: a finished list may be read one past its end (never used)
+    __shared__ K s[R + R / 32 + 4];
+    const uint64_t base = uint64_t(blockIdx.x) * R;
+    const int cnt = n - base < uint64_t(R) ? int(n - base) : R;
+    const int t = threadIdx.x;
+    // padding sorts last and, being last in input order, stays behind real maxima
+    const K pad = std::numeric_limits<K>::max();
+    for (int x = t; x < R; x += NT) s[spad(x)] = x < cnt ? in[base + x] : pad;
+    __syncthreads();
+    K k[VT];
+#pragma unroll
+    for (int v = 0; v < VT; ++v) k[v] = s[spad(t * VT + v)];
+#pragma unroll
+    for (int pass = 0; pass < VT; ++pass) {
+#pragma unroll
+        for (int v = pass & 1; v + 1 < VT; v += 2) {
+            if (k[v + 1] < k[v]) {
+                const K x = k[v];
+                k[v] = k[v + 1];
+                k[v + 1] = x;
+            }
+        }
+    }
+    for (int w = VT; w < R; w *= 2) {
+        __syncthreads();  // previous round's reads are done
+#pragma unroll
+        for (int v = 0; v < VT; ++v) s[spad(t * VT + v)] = k[v];
+        __syncthreads();
+        const int d = t * VT;
+        const int a0 = d / (2 * w) * (2 * w), b0 = a0 + w;  // list starts
+        const int diag = d - a0;
+        int lo = diag > w ? diag - w : 0, hi = diag < w ? diag : w;
+        while (lo < hi) {  // Lemma-1 split (ties to the left list)
+            const int mid = (lo + hi + 1) >> 1;
+            if (s[spad(b0 + diag - mid)] < s[spad(a0 + mid - 1)])
+                hi = mid - 1;
+            else
+                lo = mid;
+        }
+        int ia = lo, ib = diag - lo;
+        K ka = s[spad(a0 + ia)], kb = s[spad(b0 + ib)];
+#pragma unroll
+        for (int v = 0; v < VT; ++v) {  // branch-free: one shared load per output
+            const bool take_b = ib < w && (ia >= w || kb < ka);
+            k[v] = take_b ? kb : ka;
+            ia += take_b ? 0 : 1;
+            ib += take_b ? 1 : 0;
+            const K nx = s[spad(take_b ? b0 + ib : a0 + ia)];
+            ka = take_b ? ka : nx;
+            kb = take_b ? nx : kb;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int v = 0; v < VT; ++v) s[spad(t * VT + v)] = k[v];
+    __syncthreads();
+    for (int x = t; x < cnt; x += NT) out[base + x] = s[spad(x)];
+}
+
+}  // namespace comerge_b200

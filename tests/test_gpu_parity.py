@@ -406,3 +406,65 @@ def test_rank_shards_concatenate(cuda, port):
         parts = [merge_shard(ta, tb, r, world)[1] for r in range(world)]
         torch.cuda.synchronize()
         assert np.array_equal(np.concatenate([host(p) for p in parts]), expect), world
+
+
+# ------------------------------------------------------------ merge sort
+# block-sorted runs + merge passes of the pipeline in
+# merge-pass mode.  Oracle: oracle_merge_sort (repeated stable_merge of
+# adjacent runs, merge.hpp:52-68), bit-exact.
+
+SORT_RUN = {np.dtype(np.int32): 8192, np.dtype(np.uint32): 8192, np.dtype(np.uint64): 4096}
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.uint32, np.uint64])
+def test_sort_sizes_against_oracle(cuda, port, dt):
+    R = SORT_RUN[np.dtype(dt)]
+    rng = np.random.default_rng(7)
+    sizes = [0, 1, 2, 7, R - 1, R, R + 1, 2 * R, 2 * R + 3, 3 * R + 17, 8 * R, 8 * R + 5,
+             100_003, 1 << 20]
+    for n in sizes:
+        for alphabet in (3, 1 << 20, None):
+            if alphabet is None:
+                info = np.iinfo(dt)
+                k = rng.integers(info.min, info.max, n, dtype=dt, endpoint=True)
+            else:
+                k = rng.integers(0, alphabet, n).astype(dt)
+            got = host(P().sort(dev(k, cuda)))
+            assert np.array_equal(got, port.merge_sort(k)), (dt, n, alphabet)
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.uint64])
+def test_sort_presorted_reversed_and_in_place(cuda, port, dt):
+    n = 300_001
+    rng = np.random.default_rng(3)
+    base = np.sort(rng.integers(0, 1 << 30, n).astype(dt))
+    for k in (base, base[::-1].copy(), np.full(n, 5, dtype=dt)):
+        t = dev(k, cuda)
+        P().sort(t, out=t)  # in place
+        assert np.array_equal(host(t), port.merge_sort(k))
+
+
+def test_sort_misaligned_output_and_workspace(cuda, port):
+    n = 70_001
+    k = np.random.default_rng(5).integers(-1000, 1000, n).astype(np.int32)
+    buf = torch.empty(n + 1, dtype=torch.int32, device=cuda)
+    out = buf[1:]  # 4-byte offset: the last pass goes through scratch + a copy
+    ws = torch.empty(P().sort_workspace_bytes(n, torch.int32), dtype=torch.uint8, device=cuda)
+    P().sort(dev(k, cuda), out=out, workspace=ws)
+    assert np.array_equal(host(out), port.merge_sort(k))
+    with pytest.raises(ValueError):
+        P().sort(dev(k, cuda), out=torch.empty(n - 1, dtype=torch.int32, device=cuda))
+
+
+def test_sort_large_properties(cuda):
+    """2^26 int32 keys (the C5 total): sorted, same multiset (size-independent)."""
+    from paper_1303_4312_b200 import testkit as tk
+    n = 1 << 26
+    import paper_1303_4312_b200._native as N
+    raw = torch.empty(n, dtype=torch.int64, device=cuda)
+    N.check(N.lib.comerge_testkit_generate_raw(11, 0, n, 1 << 31, raw.data_ptr(), None), True)
+    keys = raw.to(torch.int32)  # draws below 2^31
+    out = P().sort(keys)
+    torch.cuda.synchronize()
+    assert tk.count_unsorted(out) == 0
+    assert tk.checksum(out) == tk.checksum(keys)

@@ -246,3 +246,12 @@ def test_reference_errors_match_port(port):
         ref.merge_parallel(a, b, 2, out=np.zeros(2, np.uint64))
     with pytest.raises(ValueError, match="worker count must be positive"):
         ref.merge_parallel(a, b, 0)
+
+
+def test_oracle_merge_sort_is_stable_sort(port):
+    """oracle_merge_sort (the GPU sort's checker) equals numpy's stable sort."""
+    rng = np.random.default_rng(2)
+    for dt in (np.int32, np.uint32, np.uint64):
+        for n in (0, 1, 2, 3, 31, 1000, 4097):
+            k = rng.integers(0, 40, n).astype(dt)
+            assert np.array_equal(port.merge_sort(k), np.sort(k, kind="stable"))
