@@ -56,7 +56,8 @@ struct comparison_counter {
 enum class run_mode { threads, simulated };
 
 // `mode` is accepted for API compatibility (the device schedule does not
-// depend on it); count_comparisons is not available on the device.
+// depend on it); count_comparisons fills merge_report::comparisons with the
+// reference's total (co-ranks + every block's merge_into), computed exactly.
 struct merge_options {
     run_mode mode = run_mode::threads;
     bool count_comparisons = false;
@@ -151,6 +152,14 @@ struct abi;
             return comerge_merge_parallel_##SUF(a, m, b, n, out, out_len, workers, synced, rep, \
                                                 bs, its);                                       \
         }                                                                                       \
+        static int merge_ex(const K* a, const std::uint32_t* av, std::size_t m, const K* b,    \
+                            const std::uint32_t* bv, std::size_t n, K* out, std::uint32_t* ov, \
+                            std::size_t out_len, std::size_t workers,                          \
+                            const comerge_merge_options* o, comerge_merge_report* rep,         \
+                            std::uint64_t* bs, std::uint32_t* its, std::uint64_t* cmp) {       \
+            return comerge_merge_parallel_ex_##SUF(a, av, m, b, bv, n, out, ov, out_len,        \
+                                                   workers, o, rep, bs, its, cmp);              \
+        }                                                                                       \
         static int merge_pairs(const K* ak, const std::uint32_t* av, std::size_t m,            \
                                const K* bk, const std::uint32_t* bv, std::size_t n, K* ok,      \
                                std::uint32_t* ov, std::size_t out_len, std::size_t workers,     \
@@ -186,19 +195,19 @@ template <typename A, typename B, typename Out>
 merge_report run_merge_parallel(const A& a, const B& b, Out& out, std::size_t workers,
                                 merge_options opts, bool synced) {
     using K = key_of<A>;
-    if (opts.count_comparisons)
-        throw std::invalid_argument(
-            "merge_parallel: comparison counting is not available on the device");
     comerge_merge_report rep{};
+    const comerge_merge_options o{synced ? 1 : 0, opts.count_comparisons ? 1 : 0};
     std::vector<std::uint64_t> bs(workers ? workers : 1);
     std::vector<std::uint32_t> its(2 * (workers ? workers : 1));
-    check(abi<K>::merge_parallel(std::ranges::data(a), std::ranges::size(a), std::ranges::data(b),
-                                 std::ranges::size(b), std::ranges::data(out),
-                                 std::ranges::size(out), workers, synced ? 1 : 0, &rep, bs.data(),
-                                 its.data()));
+    std::uint64_t cmp = 0;
+    check(abi<K>::merge_ex(std::ranges::data(a), nullptr, std::ranges::size(a),
+                           std::ranges::data(b), nullptr, std::ranges::size(b),
+                           std::ranges::data(out), nullptr, std::ranges::size(out), workers, &o,
+                           &rep, bs.data(), its.data(), &cmp));
     merge_report r = to_report(rep);
     r.block_sizes.assign(bs.begin(), bs.begin() + workers);
     r.corank_iterations.assign(its.begin(), its.begin() + (synced ? workers : 2 * workers));
+    if (opts.count_comparisons) r.comparisons = cmp;
     return r;
 }
 

@@ -228,6 +228,38 @@ int comerge_merge_parallel_pairs_u64(const uint64_t* a_keys, const uint32_t* a_v
                                      uint64_t* out_keys, uint32_t* out_vals, size_t out_len,
                                      size_t workers, comerge_merge_report* report);
 
+/* merge_options (parallel.hpp:38-42) for the full-report entry points. */
+typedef struct comerge_merge_options {
+    int synced;             /* merge_parallel_synced semantics (parallel.hpp:323-336)  */
+    int count_comparisons;  /* merge_options::count_comparisons: fill *comparisons      */
+} comerge_merge_options;
+
+/* merge_parallel / merge_parallel_synced with every report field, keys only
+ * (payload pointers NULL) or keys + uint32 payloads (all three non-NULL).
+ * With opts->count_comparisons, *comparisons receives the reference's total
+ * (parallel.hpp:270-280): Algorithm 1's comparisons at every co-rank its
+ * workers make plus every block's merge_into (merge.hpp:18-33), computed
+ * exactly from the block windows (one binary search per block).  opts may be
+ * NULL (unsynced, no counting). */
+int comerge_merge_parallel_ex_i32(const int32_t* a, const uint32_t* a_vals, size_t m,
+                                  const int32_t* b, const uint32_t* b_vals, size_t n,
+                                  int32_t* out, uint32_t* out_vals, size_t out_len,
+                                  size_t workers, const comerge_merge_options* opts,
+                                  comerge_merge_report* report, uint64_t* block_sizes,
+                                  uint32_t* corank_iterations, uint64_t* comparisons);
+int comerge_merge_parallel_ex_u32(const uint32_t* a, const uint32_t* a_vals, size_t m,
+                                  const uint32_t* b, const uint32_t* b_vals, size_t n,
+                                  uint32_t* out, uint32_t* out_vals, size_t out_len,
+                                  size_t workers, const comerge_merge_options* opts,
+                                  comerge_merge_report* report, uint64_t* block_sizes,
+                                  uint32_t* corank_iterations, uint64_t* comparisons);
+int comerge_merge_parallel_ex_u64(const uint64_t* a, const uint32_t* a_vals, size_t m,
+                                  const uint64_t* b, const uint32_t* b_vals, size_t n,
+                                  uint64_t* out, uint32_t* out_vals, size_t out_len,
+                                  size_t workers, const comerge_merge_options* opts,
+                                  comerge_merge_report* report, uint64_t* block_sizes,
+                                  uint32_t* corank_iterations, uint64_t* comparisons);
+
 /* comerge::co_rank(target, a, b, less, stats) (corank.hpp:128-133); host or
  * device pointers; iterations / comparisons may be NULL. */
 int comerge_co_rank_i32(uint64_t target, const int32_t* a, size_t m, const int32_t* b, size_t n,

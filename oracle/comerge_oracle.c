@@ -169,6 +169,19 @@ uint64_t oracle_multiset_checksum(int kind, const void* keys, uint64_t len) {
             if (outv) outv[o] = bv[y];                                                         \
             out[o++] = b[y];                                                                   \
         }                                                                                      \
+    }                                                                                          \
+    /* the same loop with counting_compare (parallel.hpp:253-256): the number */               \
+    /* of less() calls, i.e. loop passes before one side runs out */                           \
+    static uint64_t merge_count_##SUFFIX(const K* a, uint64_t m, const K* b, uint64_t n) {     \
+        uint64_t x = 0, y = 0, c = 0;                                                          \
+        while (x < m && y < n) {                                                               \
+            ++c;                                                                               \
+            if (b[y] < a[x])                                                                   \
+                ++y;                                                                           \
+            else                                                                               \
+                ++x;                                                                           \
+        }                                                                                      \
+        return c;                                                                              \
     }
 
 DEFINE_TYPED(i32, int32_t)
@@ -210,6 +223,64 @@ void oracle_merge_into(int kind, const void* a, const uint32_t* av, uint64_t m, 
     case ORACLE_U32: merge_into_u32(a, av, m, b, bv, n, out, outv); break;
     case ORACLE_U64: merge_into_u64(a, av, m, b, bv, n, out, outv); break;
     }
+}
+
+/* merge_report with count_comparisons (parallel.hpp:180-282, simulated
+ * mode): per worker r, co_rank both block ends (unsynced) or its begin only
+ * (synced: the end is the next worker's begin, parallel.hpp:209-219), then the
+ * counted merge of its block.  Writes block_sizes[workers],
+ * iterations[2*workers or workers] and the total comparisons (any may be NULL). */
+int oracle_merge_report(int kind, const void* a, uint64_t m, const void* b, uint64_t n,
+                        uint64_t workers, int synced, uint64_t* block_sizes,
+                        uint32_t* iterations, uint64_t* comparisons) {
+    if (check_total_length(m, n)) return ORACLE_E_LENGTH;
+    if (workers == 0) return ORACLE_E_INVALID;
+    const size_t s = key_size(kind);
+    const char* ca = (const char*)a;
+    const char* cb = (const char*)b;
+    const uint64_t total = m + n;
+    uint64_t sum = 0;
+    for (uint64_t r = 0; r < workers; ++r) {
+        uint64_t lo, hi, j0, k0, j1, k1;
+        uint32_t it0 = 0, c0 = 0, it1 = 0, c1 = 0;
+        oracle_partition_output(total, workers, r, &lo);
+        oracle_partition_output(total, workers, r + 1, &hi);
+        oracle_co_rank(kind, lo, a, m, b, n, &j0, &k0, &it0, &c0);
+        if (!synced || r + 1 < workers) {
+            oracle_co_rank(kind, hi, a, m, b, n, &j1, &k1, &it1, &c1);
+        } else {
+            j1 = m;
+            k1 = n;
+        }
+        if (synced) c1 = 0; /* the next worker's begin co-rank: counted there */
+        uint64_t kc = 0;
+        switch (kind) {
+        case ORACLE_I32:
+            kc = merge_count_i32((const int32_t*)(ca + j0 * s), j1 - j0,
+                                 (const int32_t*)(cb + k0 * s), k1 - k0);
+            break;
+        case ORACLE_U32:
+            kc = merge_count_u32((const uint32_t*)(ca + j0 * s), j1 - j0,
+                                 (const uint32_t*)(cb + k0 * s), k1 - k0);
+            break;
+        default:
+            kc = merge_count_u64((const uint64_t*)(ca + j0 * s), j1 - j0,
+                                 (const uint64_t*)(cb + k0 * s), k1 - k0);
+            break;
+        }
+        sum += (uint64_t)c0 + c1 + kc;
+        if (block_sizes) block_sizes[r] = hi - lo;
+        if (iterations) {
+            if (synced) {
+                iterations[r] = it0;
+            } else {
+                iterations[2 * r] = it0;
+                iterations[2 * r + 1] = it1;
+            }
+        }
+    }
+    if (comparisons) *comparisons = sum;
+    return ORACLE_OK;
 }
 
 /* ------------------------------------------- merge sort (test oracle only) */

@@ -61,6 +61,8 @@ class Port:
                                               C.c_int, _p, _p]
         lib.oracle_merge_segmented.argtypes = [C.c_int, _p, _p, _p, _p, _u64, _p, C.c_int]
         lib.oracle_merge_sort.argtypes = [C.c_int, _p, _u64, _p]
+        lib.oracle_merge_report.argtypes = [C.c_int, _p, _u64, _p, _u64, _u64, C.c_int, _p, _p,
+                                            C.POINTER(_u64)]
         lib.oracle_generate_sorted.argtypes = [C.c_int, _u64, _u64, _u64, _u64, _p]
         lib.oracle_generate_sorted.restype = None
         lib.oracle_generate_raw.argtypes = [_u64, _u64, _u64, _u64, _p]
@@ -112,6 +114,16 @@ class Port:
                                              nseg, ptr(out), threads)
         _raise(rc, "merge_segmented: offsets must be nondecreasing")
         return out
+
+    def merge_report(self, a, b, workers, synced=False):
+        """(block_sizes, corank_iterations, comparisons) of merge_parallel."""
+        bs = np.zeros(max(workers, 1), dtype=np.uint64)
+        its = np.zeros((1 if synced else 2) * max(workers, 1), dtype=np.uint32)
+        cmp = _u64(0)
+        rc = self.lib.oracle_merge_report(kind_of(a), ptr(a), len(a), ptr(b), len(b), workers,
+                                          int(synced), ptr(bs), ptr(its), C.byref(cmp))
+        _raise(rc, "merge_parallel: worker count must be positive")
+        return bs, its, int(cmp.value)
 
     def merge_sort(self, keys):
         keys = np.ascontiguousarray(keys)

@@ -31,6 +31,11 @@ class MergeReport(C.Structure):
                 ("e2e_ns", _u64), ("h2d_bytes", _u64), ("d2h_bytes", _u64), ("tiles", _u64)]
 
 
+class MergeOptions(C.Structure):
+    """comerge_merge_options (include/comerge_cuda.h)."""
+    _fields_ = [("synced", C.c_int), ("count_comparisons", C.c_int)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -52,6 +57,9 @@ def _load():
             _p, _sz, _p, _sz, _p, _sz, _p, _p, _p, _p]
         getattr(lib, f"comerge_merge_parallel_{suf}").argtypes = [
             _p, _sz, _p, _sz, _p, _sz, _sz, _i, C.POINTER(MergeReport), _p, _p]
+        getattr(lib, f"comerge_merge_parallel_ex_{suf}").argtypes = [
+            _p, _p, _sz, _p, _p, _sz, _p, _p, _sz, _sz, C.POINTER(MergeOptions),
+            C.POINTER(MergeReport), _p, _p, C.POINTER(_u64)]
         getattr(lib, f"comerge_merge_parallel_pairs_{suf}").argtypes = [
             _p, _p, _sz, _p, _p, _sz, _p, _p, _sz, _sz, C.POINTER(MergeReport)]
         getattr(lib, f"comerge_co_rank_{suf}").argtypes = [

@@ -237,7 +237,9 @@ class MergeReport:
 class MergeOptions:
     """comerge::merge_options (parallel.hpp:39-42).  `mode` is accepted for
     API compatibility; the device schedule does not depend on it.
-    `count_comparisons` is not supported on the device (raises)."""
+    `count_comparisons` fills MergeReport.comparisons with the reference's
+    total (co-ranks + every block's merge_into), computed exactly from the
+    block windows."""
     mode: str = "threads"
     count_comparisons: bool = False
 
@@ -246,22 +248,25 @@ def _merge_parallel(who, a, b, out, workers, opts, synced):
     suf = _suffix(a)
     if _suffix(b) != suf or _suffix(out) != suf:
         raise TypeError(f"{who}: a, b and out must share one dtype")
-    if opts is not None and opts.count_comparisons:
-        raise ValueError(f"{who}: comparison counting is not available on the device")
+    count = bool(opts is not None and opts.count_comparisons)
     if workers < 0:
         raise ValueError("merge_parallel: worker count must be positive")
     rep = N.MergeReport()
     bs = np.zeros(max(workers, 1), np.uint64)
     its = np.zeros(2 * max(workers, 1), np.uint32)
+    cmp = C.c_uint64(0)
+    mo = N.MergeOptions(int(synced), int(count))
     if _is_torch(out) and out.is_cuda:
         torch.cuda.current_stream(out.device).synchronize()
-    N.check(getattr(N.lib, f"comerge_merge_parallel_{suf}")(
-        _ptr(a), _len(a), _ptr(b), _len(b), _ptr(out), _len(out), workers, int(synced),
-        C.byref(rep), C.c_void_p(bs.ctypes.data), C.c_void_p(its.ctypes.data)))
+    N.check(getattr(N.lib, f"comerge_merge_parallel_ex_{suf}")(
+        _ptr(a), None, _len(a), _ptr(b), None, _len(b), _ptr(out), None, _len(out), workers,
+        C.byref(mo), C.byref(rep), C.c_void_p(bs.ctypes.data), C.c_void_p(its.ctypes.data),
+        C.byref(cmp)))
     return MergeReport(
         m=rep.m, n=rep.n, workers=rep.workers, wall_ns=rep.wall_ns,
         block_sizes=[int(x) for x in bs[:workers]],
         corank_iterations=[int(x) for x in its[:(workers if synced else 2 * workers)]],
+        comparisons=int(cmp.value) if count else None,
         e2e_ns=rep.e2e_ns, h2d_bytes=rep.h2d_bytes, d2h_bytes=rep.d2h_bytes, tiles=rep.tiles)
 
 

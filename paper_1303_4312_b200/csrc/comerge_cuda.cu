@@ -399,6 +399,18 @@ int merge_segmented_device(const K* a, const uint64_t* a_off, size_t m, const K*
     return check_launch("comerge: segmented merge launch");
 }
 
+// merge_comparisons of every worker block (report bookkeeping, one thread each)
+template <typename K>
+__global__ void block_comparisons_kernel(const K* __restrict__ a, const K* __restrict__ b,
+                                         const uint64_t* __restrict__ ranks,
+                                         const uint64_t* __restrict__ js, uint64_t workers,
+                                         uint64_t* __restrict__ out) {
+    const uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= workers) return;
+    out[r] = merge_comparisons(a, js[r], js[r + 1], b, ranks[r] - js[r], ranks[r + 1] - js[r + 1],
+                               [](const K* p) { return ldg_key(p); });
+}
+
 template <typename K>
 int co_rank_batch_device(const uint64_t* ranks, size_t count, const K* a, size_t m, const K* b,
                          size_t n, uint64_t* out_j, uint32_t* out_it, uint32_t* out_cmp,
@@ -683,11 +695,69 @@ int merge_host_pipeline(const K* a, const uint32_t* av, uint64_t m, const K* b,
     return COMERGE_OK;
 }
 
+// The reference's merge_report bookkeeping (parallel.hpp:262-281) from the
+// co-ranks of every worker-block boundary r = 0..workers: block sizes, the
+// co_rank_stats iterations (begin and end per worker; synced: begin only,
+// :269-275) and, when counting, the total comparisons -- every co-rank's
+// (Algorithm 1's own count) plus every block's merge_into (merge_comparisons,
+// corank.cuh: exact, no counted merge needed).
+struct block_report {
+    std::vector<uint64_t> ranks, js, merge_cmps;
+    std::vector<uint32_t> its, cmps;
+    void emit(size_t workers, int synced, uint64_t* block_sizes, uint32_t* iters,
+              uint64_t* comparisons) const {
+        if (block_sizes)
+            for (size_t r = 0; r < workers; ++r) block_sizes[r] = ranks[r + 1] - ranks[r];
+        if (iters) {
+            for (size_t r = 0; r < workers; ++r) {
+                if (synced) {
+                    iters[r] = its[r];
+                } else {
+                    iters[2 * r] = its[r];
+                    iters[2 * r + 1] = its[r + 1];
+                }
+            }
+        }
+        if (comparisons) {
+            uint64_t total = 0;
+            for (size_t r = 0; r < workers; ++r)
+                total += cmps[r] + (synced ? 0 : cmps[r + 1]) + merge_cmps[r];
+            *comparisons = total;
+        }
+    }
+};
+
+// ... with Algorithm 1 over host-resident inputs
+template <typename K>
+void host_block_report(const K* a, size_t m, const K* b, size_t n, size_t workers, bool count,
+                       block_report& br) {
+    const uint64_t total = uint64_t(m) + n;
+    br.ranks.resize(workers + 1);
+    br.js.resize(workers + 1);
+    br.its.resize(workers + 1);
+    br.cmps.resize(workers + 1);
+    auto rd = [](const K* p) { return *p; };
+    for (size_t r = 0; r <= workers; ++r) {
+        partition_output_impl(total, workers, r, &br.ranks[r]);
+        corank_stats st{};
+        br.js[r] = co_rank_alg1(br.ranks[r], a, m, b, n, rd, &st);
+        br.its[r] = st.iterations;
+        br.cmps[r] = st.comparisons;
+    }
+    if (count) {
+        br.merge_cmps.resize(workers);
+        for (size_t r = 0; r < workers; ++r)
+            br.merge_cmps[r] = merge_comparisons(a, br.js[r], br.js[r + 1], b,
+                                                 br.ranks[r] - br.js[r],
+                                                 br.ranks[r + 1] - br.js[r + 1], rd);
+    }
+}
+
 template <typename K, bool HAS_V>
 int merge_parallel_sync(const K* a, const uint32_t* av, size_t m, const K* b, const uint32_t* bv,
                         size_t n, K* out, uint32_t* outv, size_t out_len, size_t workers,
                         int synced, comerge_merge_report* rep, uint64_t* block_sizes,
-                        uint32_t* corank_iterations) {
+                        uint32_t* corank_iterations, uint64_t* comparisons = nullptr) {
     const char* who = synced ? "merge_parallel_synced" : "merge_parallel";
     // checked_output (parallel.hpp:284-295), then workers (:185-186)
     if (m > SIZE_MAX - n)
@@ -708,7 +778,8 @@ int merge_parallel_sync(const K* a, const uint32_t* av, size_t m, const K* b, co
         return bytes == 0 || is_pinned_host(p) || is_device_ptr(p);
     };
     const bool any_host = !is_device_ptr(a) || !is_device_ptr(b) || !is_device_ptr(out);
-    if (total >= (uint64_t(1) << 20) && any_host && g_host_mode == 1 &&
+    const bool host_in = !is_device_ptr(a) && !is_device_ptr(b);
+    if (total >= (uint64_t(1) << 20) && any_host && host_in && g_host_mode == 1 &&
         pinned_or_dev(a, m * sizeof(K)) && pinned_or_dev(b, n * sizeof(K)) &&
         pinned_or_dev(out, total * sizeof(K)) &&
         (!HAS_V || (pinned_or_dev(av, m * 4) && pinned_or_dev(bv, n * 4) &&
@@ -720,22 +791,9 @@ int merge_parallel_sync(const K* a, const uint32_t* av, size_t m, const K* b, co
         cudaEventRecord(e2e.b, s);
         const cudaError_t e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) return cuda_fail(e, "comerge: zero-copy merge");
-        std::vector<uint64_t> ranks(workers + 1);
-        for (size_t r = 0; r <= workers; ++r) partition_output_impl(total, workers, r, &ranks[r]);
-        if (block_sizes)
-            for (size_t r = 0; r < workers; ++r) block_sizes[r] = ranks[r + 1] - ranks[r];
-        if (corank_iterations) {
-            for (size_t r = 0; r <= workers; ++r) {
-                corank_stats st{};
-                co_rank_alg1(ranks[r], a, m, b, n, [](const K* p) { return *p; }, &st);
-                if (synced) {
-                    if (r < workers) corank_iterations[r] = st.iterations;
-                } else {
-                    if (r < workers) corank_iterations[2 * r] = st.iterations;
-                    if (r > 0) corank_iterations[2 * r - 1] = st.iterations;
-                }
-            }
-        }
+        block_report br;
+        host_block_report(a, m, b, n, workers, comparisons != nullptr, br);
+        br.emit(workers, synced, block_sizes, corank_iterations, comparisons);
         if (rep) {
             const uint64_t eb = sizeof(K) + (HAS_V ? 4 : 0);
             rep->m = m;
@@ -760,24 +818,9 @@ int merge_parallel_sync(const K* a, const uint32_t* av, size_t m, const K* b, co
                                                    &merge_ns))
             return rc;
         const auto w1 = std::chrono::steady_clock::now();
-        std::vector<uint64_t> ranks(workers + 1);
-        for (size_t r = 0; r <= workers; ++r) partition_output_impl(total, workers, r, &ranks[r]);
-        if (block_sizes)
-            for (size_t r = 0; r < workers; ++r) block_sizes[r] = ranks[r + 1] - ranks[r];
-        if (corank_iterations) {
-            // the reference's co_rank_stats of every block boundary (parallel.hpp:273-275),
-            // Algorithm 1 over the host-resident inputs (report bookkeeping only)
-            for (size_t r = 0; r <= workers; ++r) {
-                corank_stats st{};
-                co_rank_alg1(ranks[r], a, m, b, n, [](const K* p) { return *p; }, &st);
-                if (synced) {
-                    if (r < workers) corank_iterations[r] = st.iterations;
-                } else {
-                    if (r < workers) corank_iterations[2 * r] = st.iterations;
-                    if (r > 0) corank_iterations[2 * r - 1] = st.iterations;
-                }
-            }
-        }
+        block_report br;  // Algorithm 1 over the host-resident inputs (bookkeeping only)
+        host_block_report(a, m, b, n, workers, comparisons != nullptr, br);
+        br.emit(workers, synced, block_sizes, corank_iterations, comparisons);
         if (rep) {
             rep->m = m;
             rep->n = n;
@@ -814,44 +857,49 @@ int merge_parallel_sync(const K* a, const uint32_t* av, size_t m, const K* b, co
                                     nullptr, 0, s);
         if (rc) return rc;
         cudaEventRecord(dev.b, s);
-        // report: co-rank both ends of every reference worker block with
+        // report: co-rank every reference worker-block boundary with
         // Algorithm 1 on the device (parallel.hpp:201-207, :273-275)
         const size_t nq = workers + 1;
-        std::vector<uint64_t> ranks(nq), js(nq);
-        std::vector<uint32_t> its(nq);
-        for (size_t r = 0; r <= workers; ++r) partition_output_impl(total, workers, r, &ranks[r]);
-        const bool want_iters = corank_iterations != nullptr;
-        if (want_iters) {
-            staged dr, dj, dit;
-            if ((rc = dr.in(ranks.data(), nq * 8, s, nullptr))) return rc;
-            if ((rc = dj.out_alloc(js.data(), nq * 8, s))) return rc;
-            if ((rc = dit.out_alloc(its.data(), nq * 4, s))) return rc;
+        block_report br;
+        br.ranks.resize(nq);
+        br.js.resize(nq);
+        br.its.resize(nq);
+        br.cmps.resize(nq);
+        for (size_t r = 0; r <= workers; ++r) partition_output_impl(total, workers, r, &br.ranks[r]);
+        const bool count = comparisons != nullptr;
+        if (corank_iterations || count) {
+            staged dr, dj, dit, dcmp, dmc;
+            if ((rc = dr.in(br.ranks.data(), nq * 8, s, nullptr))) return rc;
+            if ((rc = dj.out_alloc(br.js.data(), nq * 8, s))) return rc;
+            if ((rc = dit.out_alloc(br.its.data(), nq * 4, s))) return rc;
+            if ((rc = dcmp.out_alloc(br.cmps.data(), nq * 4, s))) return rc;
             if ((rc = co_rank_batch_device<K>(static_cast<const uint64_t*>(dr.dev), nq,
                                               static_cast<const K*>(da.dev), m,
                                               static_cast<const K*>(db.dev), n,
                                               static_cast<uint64_t*>(dj.dev),
-                                              static_cast<uint32_t*>(dit.dev), nullptr, s)))
+                                              static_cast<uint32_t*>(dit.dev),
+                                              static_cast<uint32_t*>(dcmp.dev), s)))
                 return rc;
-            if ((rc = dit.back(its.data(), nq * 4, nullptr))) return rc;
+            if (count) {
+                br.merge_cmps.resize(workers);
+                if ((rc = dmc.out_alloc(br.merge_cmps.data(), workers * 8, s))) return rc;
+                block_comparisons_kernel<K><<<unsigned(div_up(workers, 128)), 128, 0, s>>>(
+                    static_cast<const K*>(da.dev), static_cast<const K*>(db.dev),
+                    static_cast<const uint64_t*>(dr.dev), static_cast<const uint64_t*>(dj.dev),
+                    workers, static_cast<uint64_t*>(dmc.dev));
+                if ((rc = check_launch("comerge: block comparisons launch"))) return rc;
+                if ((rc = dmc.back(br.merge_cmps.data(), workers * 8, nullptr))) return rc;
+            }
+            if ((rc = dit.back(br.its.data(), nq * 4, nullptr))) return rc;
+            if ((rc = dcmp.back(br.cmps.data(), nq * 4, nullptr))) return rc;
+            if ((rc = dj.back(br.js.data(), nq * 8, nullptr))) return rc;
         }
         if ((rc = dout.back(out, total * sizeof(K), &d2h))) return rc;
         if (HAS_V && (rc = doutv.back(outv, total * 4, &d2h))) return rc;
         cudaEventRecord(e2e.b, s);
         const cudaError_t e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) return cuda_fail(e, "comerge: merge_parallel");
-        if (block_sizes)
-            for (size_t r = 0; r < workers; ++r) block_sizes[r] = ranks[r + 1] - ranks[r];
-        if (want_iters) {
-            // unsynced: begin/end per worker; synced: begin only (:269-275)
-            for (size_t r = 0; r < workers; ++r) {
-                if (synced) {
-                    corank_iterations[r] = its[r];
-                } else {
-                    corank_iterations[2 * r] = its[r];
-                    corank_iterations[2 * r + 1] = its[r + 1];
-                }
-            }
-        }
+        br.emit(workers, synced, block_sizes, corank_iterations, comparisons);
     }
     if (rep) {
         rep->m = m;
@@ -1021,6 +1069,27 @@ size_t comerge_cuda_segmented_workspace_bytes(size_t total, size_t, int key_kind
         return merge_parallel_sync<K, false>(a, nullptr, m, b, nullptr, n, out, nullptr,         \
                                              out_len, workers, synced, report, block_sizes,      \
                                              corank_iterations);                                 \
+    }                                                                                            \
+    int comerge_merge_parallel_ex_##SUF(const K* a, const uint32_t* av, size_t m, const K* b,    \
+                                        const uint32_t* bv, size_t n, K* out, uint32_t* outv,    \
+                                        size_t out_len, size_t workers,                          \
+                                        const comerge_merge_options* opts,                       \
+                                        comerge_merge_report* report, uint64_t* block_sizes,     \
+                                        uint32_t* corank_iterations, uint64_t* comparisons) {    \
+        const int synced = opts ? opts->synced : 0;                                              \
+        uint64_t* cmp = opts && opts->count_comparisons ? comparisons : nullptr;                 \
+        if (opts && opts->count_comparisons && !comparisons)                                     \
+            return fail(COMERGE_E_INVALID, "merge_parallel: count_comparisons needs an output"); \
+        if (av || bv || outv) {                                                                  \
+            if (!(av || m == 0) || !(bv || n == 0) || !(outv || m + n == 0))                     \
+                return fail(COMERGE_E_INVALID, "merge_parallel: payloads need all three arrays"); \
+            return merge_parallel_sync<K, true>(a, av, m, b, bv, n, out, outv, out_len, workers, \
+                                                synced, report, block_sizes, corank_iterations,  \
+                                                cmp);                                            \
+        }                                                                                        \
+        return merge_parallel_sync<K, false>(a, nullptr, m, b, nullptr, n, out, nullptr,         \
+                                             out_len, workers, synced, report, block_sizes,      \
+                                             corank_iterations, cmp);                            \
     }                                                                                            \
     int comerge_merge_parallel_pairs_##SUF(const K* ak, const uint32_t* av, size_t m,            \
                                            const K* bk, const uint32_t* bv, size_t n, K* ok,     \

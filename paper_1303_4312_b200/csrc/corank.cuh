@@ -71,6 +71,39 @@ __host__ __device__ __forceinline__ uint64_t co_rank_alg1(uint64_t target, const
     return take_a;
 }
 
+// Key comparisons the reference's serial merge (merge.hpp:18-33) makes on the
+// windows A[j0, j1), B[k0, k1): its loop compares once per output until one
+// side is exhausted.  B runs out first iff B's last key < A's last key (ties
+// go to A); the loop then also took every A key <= B_last, else every B key
+// < A_last -- one binary search instead of a counted merge.
+template <typename K, typename Read>
+__host__ __device__ __forceinline__ uint64_t merge_comparisons(const K* a, uint64_t j0, uint64_t j1,
+                                                               const K* b, uint64_t k0, uint64_t k1,
+                                                               Read rd) {
+    if (j1 == j0 || k1 == k0) return 0;
+    const K al = rd(a + j1 - 1), bl = rd(b + k1 - 1);
+    if (bl < al) {
+        uint64_t lo = j0, hi = j1;  // first A key > B_last
+        while (lo < hi) {
+            const uint64_t mid = lo + (hi - lo) / 2;
+            if (bl < rd(a + mid))
+                hi = mid;
+            else
+                lo = mid + 1;
+        }
+        return (k1 - k0) + (lo - j0);
+    }
+    uint64_t lo = k0, hi = k1;  // first B key >= A_last
+    while (lo < hi) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (rd(b + mid) < al)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return (j1 - j0) + (lo - k0);
+}
+
 // Largest j in [max(0,i-n), min(i,m)] with !P(j): the Lemma-1 split.
 template <typename K, typename Index, typename Read>
 __host__ __device__ __forceinline__ Index co_rank_split(Index i, const K* a, Index m, const K* b,

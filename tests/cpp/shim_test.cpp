@@ -134,6 +134,40 @@ static void kats() {
     }
 }
 
+// merge_options::count_comparisons (parallel.hpp:41, :253-280): absent unless
+// requested (parallel_test.cpp:186); when requested, the reference's total --
+// here recomputed the reference's way: Algorithm 1's comparisons at both ends
+// of every block plus a counted two-finger merge of every block.
+static void comparisons() {
+    std::mt19937_64 rng(11);
+    keys a(3000), b(2000);
+    for (auto& x : a) x = rng() % 50;
+    for (auto& x : b) x = rng() % 50;
+    std::sort(a.begin(), a.end());
+    std::sort(b.begin(), b.end());
+    keys out(5000);
+    CHECK(!cm::merge_parallel(a, b, out, 7).comparisons.has_value());
+    for (std::size_t w : {std::size_t{1}, std::size_t{7}, std::size_t{64}}) {
+        cm::merge_options opts;
+        opts.count_comparisons = true;
+        const auto rep = cm::merge_parallel(a, b, out, w, {}, opts);
+        std::uint64_t expect = 0;
+        for (std::size_t r = 0; r < w; ++r) {
+            const auto lo = cm::partition_output(5000, w, r), hi = cm::partition_output(5000, w, r + 1);
+            cm::co_rank_stats s0, s1;
+            const auto c0 = cm::co_rank(lo, a, b, {}, &s0), c1 = cm::co_rank(hi, a, b, {}, &s1);
+            std::size_t x = c0.a, y = c0.b;
+            std::uint64_t kc = 0;
+            while (x < c1.a && y < c1.b) {
+                ++kc;
+                if (b[y] < a[x]) ++y; else ++x;
+            }
+            expect += s0.comparisons + s1.comparisons + kc;
+        }
+        CHECK(rep.comparisons.has_value() && *rep.comparisons == expect);
+    }
+}
+
 template <typename K>
 static void sweep(std::uint64_t seed) {
     std::mt19937_64 rng(seed);
@@ -177,6 +211,7 @@ static void sweep(std::uint64_t seed) {
 
 int main() {
     kats();
+    comparisons();
     sweep<std::int32_t>(1);
     sweep<std::uint32_t>(2);
     sweep<std::uint64_t>(3);

@@ -137,6 +137,28 @@ def main():
     fx["checksum__keys"] = keys
     fx["checksum__value"] = np.array([ref.checksum(keys)], np.uint64)
 
+    # 8. merge_options::count_comparisons (parallel.hpp:41, :253-280): the
+    #    reference's total comparison count for several worker counts, both
+    #    modes (simulated, so deterministic), duplicate-heavy and skewed inputs.
+    crng = np.random.default_rng(20261019)
+    cshapes = [(0, 9, 4), (9, 0, 4), (1, 1, 1), (500, 700, 3), (2000, 37, 0), (37, 2000, 0),
+               (1500, 1500, 1), (4096, 4095, 64)]
+    workers_set = [1, 2, 3, 7, 16, 100]
+    for name, dt in DTYPES.items():
+        for c, (m, n, alphabet) in enumerate(cshapes):
+            a, b = sorted_keys(crng, dt, m, alphabet), sorted_keys(crng, dt, n, alphabet)
+            counts = np.zeros((len(workers_set), 2), np.uint64)
+            for wi, w in enumerate(workers_set):
+                for synced in (0, 1):
+                    _, rep, _, _ = ref.merge_parallel(a, b, w, simulated=True, synced=bool(synced),
+                                                      count=True)
+                    assert rep.has_comparisons
+                    counts[wi, synced] = rep.comparisons
+            fx[f"cmp__{name}__{c}__a"] = a
+            fx[f"cmp__{name}__{c}__b"] = b
+            fx[f"cmp__{name}__{c}__counts"] = counts
+    fx["cmp__workers"] = np.array(workers_set, np.uint64)
+
     np.savez_compressed(OUT, **fx)
     print(f"wrote {OUT}: {len(fx)} arrays, {os.path.getsize(OUT)} bytes")
 

@@ -468,3 +468,49 @@ def test_sort_large_properties(cuda):
     torch.cuda.synchronize()
     assert tk.count_unsorted(out) == 0
     assert tk.checksum(out) == tk.checksum(keys)
+
+
+# ------------------------------------------- merge report: comparisons
+# merge_options::count_comparisons (parallel.hpp:41, :253-280) against the
+# reference's own totals (tests/golden section 8) and the oracle's report.
+
+@pytest.mark.parametrize("where", ["host", "device"])
+def test_comparison_counts_match_reference(cuda, port, golden, where):
+    from paper_1303_4312_b200.comerge import MergeOptions
+    ws = [int(x) for x in golden["cmp__workers"]]
+    opts = MergeOptions(count_comparisons=True)
+    for name in ("i32", "u32", "u64"):
+        for c in range(8):
+            a, b = golden[f"cmp__{name}__{c}__a"], golden[f"cmp__{name}__{c}__b"]
+            counts = golden[f"cmp__{name}__{c}__counts"]
+            for wi, w in enumerate(ws):
+                for synced in (False, True):
+                    if where == "host":
+                        aa, bb = a, b
+                        out = np.empty(len(a) + len(b), a.dtype)
+                    else:
+                        aa, bb = dev(a, cuda), dev(b, cuda)
+                        out = torch.empty(len(a) + len(b), dtype=TDT[a.dtype], device=cuda)
+                    fn = P().merge_parallel_synced if synced else P().merge_parallel
+                    rep = fn(aa, bb, out, w, opts=opts)
+                    assert rep.comparisons == int(counts[wi, int(synced)]), (name, c, w, synced)
+                    bs, its, _ = port.merge_report(a, b, w, synced)
+                    assert rep.block_sizes == [int(x) for x in bs[:w]]
+                    assert rep.corank_iterations == [int(x) for x in its]
+                    got = out if where == "host" else host(out)
+                    assert np.array_equal(got, port.merge(a, b))
+
+
+def test_comparison_counts_large_host_pipeline(cuda, port):
+    """The chunked host pipeline (>= 2^20 elements) reports the same counts."""
+    from paper_1303_4312_b200.comerge import MergeOptions
+    rng = np.random.default_rng(9)
+    a = np.sort(rng.integers(0, 64, 700_000).astype(np.int32))
+    b = np.sort(rng.integers(0, 64, 600_000).astype(np.int32))
+    out = np.empty(len(a) + len(b), np.int32)
+    for w, synced in ((1, False), (16, False), (16, True), (1000, True)):
+        fn = P().merge_parallel_synced if synced else P().merge_parallel
+        rep = fn(a, b, out, w, opts=MergeOptions(count_comparisons=True))
+        _, _, total = port.merge_report(a, b, w, synced)
+        assert rep.comparisons == total
+    assert np.array_equal(out, port.merge(a, b))

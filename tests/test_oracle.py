@@ -255,3 +255,16 @@ def test_oracle_merge_sort_is_stable_sort(port):
         for n in (0, 1, 2, 3, 31, 1000, 4097):
             k = rng.integers(0, 40, n).astype(dt)
             assert np.array_equal(port.merge_sort(k), np.sort(k, kind="stable"))
+
+
+def test_oracle_comparison_counts_match_reference(port, golden):
+    """merge_options::count_comparisons totals (reference, tests/golden, section 8)."""
+    ws = [int(x) for x in golden["cmp__workers"]]
+    for name in ("i32", "u32", "u64"):
+        for c in range(8):
+            a, b = golden[f"cmp__{name}__{c}__a"], golden[f"cmp__{name}__{c}__b"]
+            counts = golden[f"cmp__{name}__{c}__counts"]
+            for wi, w in enumerate(ws):
+                for synced in (0, 1):
+                    _, _, total = port.merge_report(a, b, w, bool(synced))
+                    assert total == int(counts[wi, synced]), (name, c, w, synced)
