@@ -12,8 +12,17 @@ HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/comerge_cuda.h include/comerge_cud
 OBJS := $(patsubst $(PKG)/csrc/%.cu,$(PKG)/lib/%.o,$(SRCS))
 
 SHIM_TEST := tests/cpp/shim_test
+CLI := bin/comerge_cuda
 
-all: $(LIB) oracle $(SHIM_TEST)
+all: $(LIB) oracle $(SHIM_TEST) $(CLI)
+
+# the reference's command line tool with device merges (cli/)
+$(CLI): cli/comerge_cuda.cpp cli/keyfile.hpp include/comerge/cuda.hpp include/comerge_cuda.h \
+        include/comerge_cuda_testkit.h $(LIB)
+	@mkdir -p bin
+	g++ -std=c++20 -O2 -Wall -Wextra -Iinclude -Icli -I/usr/local/cuda/include -o $@ $< \
+	    -L$(PKG)/lib -lcomerge_cuda -L/usr/local/cuda/lib64 -lcudart \
+	    -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib' -Wl,-rpath,/usr/local/cuda/lib64
 
 # C++ drop-in shim test (include/comerge/cuda.hpp over the C ABI)
 $(SHIM_TEST): tests/cpp/shim_test.cpp include/comerge/cuda.hpp include/comerge_cuda.h $(LIB)
@@ -32,7 +41,7 @@ oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -f $(PKG)/lib/*.o $(PKG)/lib/*.so $(PKG)/lib/*.ptxas.txt $(SHIM_TEST)
+	rm -f $(PKG)/lib/*.o $(PKG)/lib/*.so $(PKG)/lib/*.ptxas.txt $(SHIM_TEST) $(CLI)
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean

@@ -159,6 +159,21 @@ def main():
             fx[f"cmp__{name}__{c}__counts"] = counts
     fx["cmp__workers"] = np.array(workers_set, np.uint64)
 
+    # 9. what the reference CLI's `bench` measures (experiment.cpp:49-121):
+    #    for every distribution (generate.cpp), seed 5, m = n = 1000, the
+    #    comparison count of p = 1, 2, 4 and the generated inputs' checksums.
+    dists = [("uniform", 0, 0), ("all-equal", 1, 0), ("few-distinct:16", 2, 16),
+             ("disjoint", 3, 0), ("interleaved", 4, 0), ("organ-pipe", 5, 0), ("runs:32", 6, 32)]
+    for token, kind, param in dists:
+        a, b = ref.generate(kind, 5, param, 1000, 1000)
+        counts = []
+        for w in (1, 2, 4):
+            _, rep, _, _ = ref.merge_parallel(a, b, w, simulated=True, count=True)
+            counts.append(rep.comparisons)
+        fx[f"clibench__{token}__counts"] = np.array(counts, np.uint64)
+        fx[f"clibench__{token}__checksum"] = np.array([ref.checksum(a), ref.checksum(b)],
+                                                      np.uint64)
+
     np.savez_compressed(OUT, **fx)
     print(f"wrote {OUT}: {len(fx)} arrays, {os.path.getsize(OUT)} bytes")
 
