@@ -167,6 +167,10 @@ struct abi;
             return comerge_merge_parallel_pairs_##SUF(ak, av, m, bk, bv, n, ok, ov, out_len,    \
                                                       workers, rep);                            \
         }                                                                                       \
+        static int plan(const K* a, std::size_t m, const K* b, std::size_t n, std::size_t w,    \
+                        std::uint64_t* blocks) {                                                \
+            return comerge_plan_##SUF(a, m, b, n, w, blocks);                                   \
+        }                                                                                       \
         static int co_rank(std::uint64_t t, const K* a, std::size_t m, const K* b,             \
                            std::size_t n, std::uint64_t* j, std::uint64_t* k,                   \
                            std::uint32_t* it, std::uint32_t* cmp) {                             \
@@ -304,21 +308,26 @@ merge_report merge_parallel_pairs(const A& a_keys, std::span<const std::uint32_t
     return detail::to_report(rep);
 }
 
-/// Central per-worker assignment (two independent co-ranks per block).
+/// Central per-worker assignment (two independent co-ranks per block), all
+/// co-ranks in one batched device launch.
 template <detail::key_range A, detail::key_range B>
     requires std::same_as<detail::key_of<A>, detail::key_of<B>>
-merge_plan plan(const A& a, const B& b, std::size_t workers, std::less<> less = {}) {
+merge_plan plan(const A& a, const B& b, std::size_t workers, std::less<> = {}) {
+    using K = detail::key_of<A>;
     if (workers == 0) throw std::invalid_argument("plan: worker count must be positive");
-    const std::size_t total = std::ranges::size(a) + std::ranges::size(b);
+    std::vector<std::uint64_t> raw(7 * workers);
+    detail::check(detail::abi<K>::plan(std::ranges::data(a), std::ranges::size(a),
+                                       std::ranges::data(b), std::ranges::size(b), workers,
+                                       raw.data()));
     merge_plan p;
     p.workers = workers;
-    std::vector<co_ranks> ends(workers + 1);
-    for (std::size_t r = 0; r <= workers; ++r)
-        ends[r] = co_rank(partition_output(total, workers, r), a, b, less);
-    for (std::size_t r = 0; r < workers; ++r)
-        p.blocks.push_back({r, partition_output(total, workers, r),
-                            partition_output(total, workers, r + 1), ends[r].a, ends[r + 1].a,
-                            ends[r].b, ends[r + 1].b});
+    for (std::size_t r = 0; r < workers; ++r) {
+        const std::uint64_t* o = raw.data() + 7 * r;
+        p.blocks.push_back({static_cast<std::size_t>(o[0]), static_cast<rank_t>(o[1]),
+                            static_cast<rank_t>(o[2]), static_cast<std::size_t>(o[3]),
+                            static_cast<std::size_t>(o[4]), static_cast<std::size_t>(o[5]),
+                            static_cast<std::size_t>(o[6])});
+    }
     return p;
 }
 

@@ -260,6 +260,17 @@ int comerge_merge_parallel_ex_u64(const uint64_t* a, const uint32_t* a_vals, siz
                                   comerge_merge_report* report, uint64_t* block_sizes,
                                   uint32_t* corank_iterations, uint64_t* comparisons);
 
+/* comerge::plan(a, b, workers) (parallel.hpp:94-115): blocks[7*r .. 7*r+6] =
+ * {worker, out_begin, out_end, a_begin, a_end, b_begin, b_end} for every
+ * worker r (block_assignment, parallel.hpp:70-84).  Host or device inputs,
+ * staged once; all co-ranks in one batched device launch. */
+int comerge_plan_i32(const int32_t* a, size_t m, const int32_t* b, size_t n, size_t workers,
+                     uint64_t* blocks);
+int comerge_plan_u32(const uint32_t* a, size_t m, const uint32_t* b, size_t n, size_t workers,
+                     uint64_t* blocks);
+int comerge_plan_u64(const uint64_t* a, size_t m, const uint64_t* b, size_t n, size_t workers,
+                     uint64_t* blocks);
+
 /* comerge::co_rank(target, a, b, less, stats) (corank.hpp:128-133); host or
  * device pointers; iterations / comparisons may be NULL. */
 int comerge_co_rank_i32(uint64_t target, const int32_t* a, size_t m, const int32_t* b, size_t n,

@@ -62,6 +62,7 @@ def _load():
             C.POINTER(MergeReport), _p, _p, C.POINTER(_u64)]
         getattr(lib, f"comerge_merge_parallel_pairs_{suf}").argtypes = [
             _p, _p, _sz, _p, _p, _sz, _p, _p, _sz, _sz, C.POINTER(MergeReport)]
+        getattr(lib, f"comerge_plan_{suf}").argtypes = [_p, _sz, _p, _sz, _sz, _p]
         getattr(lib, f"comerge_co_rank_{suf}").argtypes = [
             _u64, _p, _sz, _p, _sz, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(C.c_uint32),
             C.POINTER(C.c_uint32)]

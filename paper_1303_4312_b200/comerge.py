@@ -309,19 +309,15 @@ def plan(a, b, workers: int):
     independent co-ranks per block, computed in one device batch."""
     if workers <= 0:
         raise ValueError("plan: worker count must be positive")
-    total = _len(a) + _len(b)
-    bounds = [partition_output(total, workers, r) for r in range(workers + 1)]
+    suf = _suffix(a)
+    if _suffix(b) != suf:
+        raise TypeError("plan: a and b must share one dtype")
+    raw = np.zeros(7 * workers, np.uint64)
     if _is_torch(a) and a.is_cuda:
-        ranks = torch.tensor(bounds, dtype=torch.uint64, device=a.device)
-        js = co_rank_batch(ranks, a, b).cpu().numpy().astype(np.uint64)
-    else:
-        js = [co_rank(i, a, b)[0] for i in bounds]
-    blocks = []
-    for r in range(workers):
-        lo, hi = bounds[r], bounds[r + 1]
-        ja, jb = int(js[r]), int(js[r + 1])
-        blocks.append(BlockAssignment(r, lo, hi, ja, jb, lo - ja, hi - jb))
-    return blocks
+        torch.cuda.current_stream(a.device).synchronize()
+    N.check(getattr(N.lib, f"comerge_plan_{suf}")(_ptr(a), _len(a), _ptr(b), _len(b), workers,
+                                                   C.c_void_p(raw.ctypes.data)))
+    return [BlockAssignment(*(int(x) for x in raw[7 * r:7 * r + 7])) for r in range(workers)]
 
 
 def merge_pairs(a_keys, a_vals, b_keys, b_vals, out_keys=None, out_vals=None, workspace=None):

@@ -952,6 +952,49 @@ int co_rank_sync(uint64_t target, const K* a, size_t m, const K* b, size_t n, ui
     return COMERGE_OK;
 }
 
+// comerge::plan (parallel.hpp:94-115): both co-ranks of every block from one
+// batched Algorithm-1 launch over inputs staged once (host or device).
+template <typename K>
+int plan_sync(const K* a, size_t m, const K* b, size_t n, size_t workers, uint64_t* blocks) {
+    if (m > SIZE_MAX - n)
+        return fail(COMERGE_E_LENGTH, "comerge: combined input length exceeds index range");
+    if (workers == 0) return fail(COMERGE_E_INVALID, "plan: worker count must be positive");
+    if (!blocks) return fail(COMERGE_E_INVALID, "plan: null result pointer");
+    if ((m && !a) || (n && !b)) return fail(COMERGE_E_INVALID, "plan: null input");
+    const uint64_t total = uint64_t(m) + n;
+    const size_t nq = workers + 1;
+    std::vector<uint64_t> ranks(nq), js(nq);
+    for (size_t r = 0; r <= workers; ++r) partition_output_impl(total, workers, r, &ranks[r]);
+    cudaStream_t s = sync_stream();
+    int rc;
+    {
+        staged da, db, dr, dj;
+        if ((rc = da.in(a, m * sizeof(K), s, nullptr))) return rc;
+        if ((rc = db.in(b, n * sizeof(K), s, nullptr))) return rc;
+        if ((rc = dr.in(ranks.data(), nq * 8, s, nullptr))) return rc;
+        if ((rc = dj.out_alloc(js.data(), nq * 8, s))) return rc;
+        if ((rc = co_rank_batch_device<K>(static_cast<const uint64_t*>(dr.dev), nq,
+                                          static_cast<const K*>(da.dev), m,
+                                          static_cast<const K*>(db.dev), n,
+                                          static_cast<uint64_t*>(dj.dev), nullptr, nullptr, s)))
+            return rc;
+        if ((rc = dj.back(js.data(), nq * 8, nullptr))) return rc;
+        const cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return cuda_fail(e, "comerge: plan");
+    }
+    for (size_t r = 0; r < workers; ++r) {
+        uint64_t* o = blocks + 7 * r;  // block_assignment, parallel.hpp:70-84
+        o[0] = r;
+        o[1] = ranks[r];
+        o[2] = ranks[r + 1];
+        o[3] = js[r];
+        o[4] = js[r + 1];
+        o[5] = ranks[r] - js[r];
+        o[6] = ranks[r + 1] - js[r + 1];
+    }
+    return COMERGE_OK;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------ merge sort
@@ -1097,6 +1140,10 @@ size_t comerge_cuda_segmented_workspace_bytes(size_t total, size_t, int key_kind
                                            comerge_merge_report* report) {                       \
         return merge_parallel_sync<K, true>(ak, av, m, bk, bv, n, ok, ov, out_len, workers, 0,   \
                                             report, nullptr, nullptr);                           \
+    }                                                                                            \
+    int comerge_plan_##SUF(const K* a, size_t m, const K* b, size_t n, size_t workers,          \
+                           uint64_t* blocks) {                                                   \
+        return plan_sync<K>(a, m, b, n, workers, blocks);                                        \
     }                                                                                            \
     int comerge_co_rank_##SUF(uint64_t target, const K* a, size_t m, const K* b, size_t n,       \
                               uint64_t* j, uint64_t* k, uint32_t* iterations,                    \
