@@ -99,9 +99,10 @@ struct pipe_layout {
     static constexpr int VW = HAS_V ? ((T + 16 + VT + 2) + 3) / 4 * 4 : 0;
     static constexpr size_t kStageKeys = (size_t(KW) * sizeof(K) + 127) / 128 * 128;
     static constexpr size_t kStageVals = (size_t(VW) * 4 + 127) / 128 * 128;
-    // segmented batches: the tile's segment offsets {aoff, boff}[s0 .. s0+SEGCAP)
+    // segmented batches: the tile's segment-end table (window-relative
+    // x1 | y1 << 16 of segments s0 .. s0+SEGCAP-1), written by the producer warp
     static constexpr int SEGCAP = 128;
-    static constexpr size_t kStageOffs = SEG ? size_t(2 * SEGCAP) * 8 : 0;
+    static constexpr size_t kStageOffs = SEG ? size_t(SEGCAP) * 4 : 0;
     static constexpr size_t kStage = kStageKeys + kStageVals + kStageOffs;
     static constexpr size_t oStages = 0;
     static constexpr size_t oBars = oStages + NST * kStage;
@@ -110,11 +111,8 @@ struct pipe_layout {
     static constexpr size_t oScratch = oDesc + size_t(NB) * 64;    // 40 x u64
     static constexpr size_t oMisc = oScratch + 40 * 8;
     static constexpr size_t kMisc = 64;
-    // segmented batches: window-relative ends of the current tile's segments
-    // (x1 | y1 << 16), built by the consumers once per tile
-    static constexpr size_t oSegEnd = oMisc + kMisc;
     static_assert(!SEG || KW < 65536, "segment ends are packed as 16-bit window offsets");
-    static constexpr size_t kSmem = oSegEnd + (SEG ? size_t(SEGCAP) * 4 : 0);
+    static constexpr size_t kSmem = oMisc + kMisc;
 };
 
 constexpr int kMaxPipeGrid = 512;
@@ -578,7 +576,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
     }
     if (tid == 0) {
         for (int s = 0; s < NST; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], SEG ? 2 : 1);  // SEG: + the producer warp's segment table
             mbar_init(&empty[s], 1);
             mbar_init(&staged[s], 1);
         }
@@ -866,7 +864,9 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
 
     if (warp == W_PROD) {
         // ------------------------------------------------------ producer
-        if (lane != 0) return;
+        // lane 0 stages the windows; for segmented batches the whole warp also
+        // writes the tile's segment-end table (the full barrier's 2nd arrival)
+        if (!SEG && lane != 0) return;
         const uint64_t policy = policy_evict_first();
         unsigned long long starve = 0;  // ns spent waiting for descriptors
         for (uint32_t s = 0;; ++s) {
@@ -882,15 +882,45 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             const uint64_t i0 = d[0];
             uint64_t* mt = meta + 8 * st;
             if (i0 == ~uint64_t(0)) {
-                mt[3] = uint64_t(1) << 63;  // done
-                mbar_arrive(&full[st]);
-                if (args.trace) args.trace[8 * c + 6] = starve;
+                if (lane == 0) {
+                    mt[3] = uint64_t(1) << 63;  // done
+                    mbar_arrive(&full[st]);
+                    if (SEG) mbar_arrive(&full[st]);
+                    if (args.trace) args.trace[8 * c + 6] = starve;
+                }
                 break;
             }
             // copy the whole descriptor out before its ring slot is released
             const uint64_t j0 = d[1], j1 = d[2], i1 = d[3], seg0 = d[4], seg1 = d[5];
-            __threadfence_block();
-            *issued = s + 1;
+            if constexpr (SEG) __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                *issued = s + 1;
+            }
+            if constexpr (SEG) {  // segment-end table (merge_thread_segends)
+                const uint64_t nse = seg1 - seg0 + 1;
+                uint32_t* se = reinterpret_cast<uint32_t*>(smem + L::oStages + size_t(st) * L::kStage +
+                                                           L::kStageKeys + L::kStageVals);
+                if (nse <= uint64_t(L::SEGCAP)) {
+                    const uint64_t k0 = i0 - j0, alen = j1 - j0, blen = (i1 - j1) - k0;
+                    for (uint64_t q = lane; q < nse; q += 32) {
+                        uint64_t ae, be;
+                        if constexpr (SEG == 2) {
+                            ae = run_off(seg0 + q + 1, args.run_len, m);
+                            be = run_off(seg0 + q + 1, args.run_len, n);
+                        } else {
+                            ae = ldg_u64(args.aoff + seg0 + q + 1);
+                            be = ldg_u64(args.boff + seg0 + q + 1);
+                        }
+                        const uint32_t x1 = ae > j0 ? uint32_t(ae - j0 < alen ? ae - j0 : alen) : 0u;
+                        const uint32_t y1 = be > k0 ? uint32_t(be - k0 < blen ? be - k0 : blen) : 0u;
+                        se[q] = x1 | (y1 << 16);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&full[st]);  // table written (release)
+                if (lane != 0) continue;
+            }
 #ifdef COMERGE_DEBUG_CHECKS
             if (!(j0 <= j1 && i0 <= i1 && i1 - i0 <= uint64_t(T) && i0 >= j0 && i1 >= j1 &&
                   i1 - j1 >= i0 - j0 && j1 <= m && i1 - j1 <= n && seg0 <= seg1 &&
@@ -930,27 +960,8 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             mt[2] = (uint64_t(a_len) << 32) | b_len;
             mt[3] = (uint64_t(a_off) << 48) | (uint64_t(b_base) << 24) | (uint64_t(b_off) << 8) |
                     uint64_t(av_off);
-            uint32_t ob = 0;
-            if constexpr (SEG) {
-                // the tile's segment offsets s0 .. s1+1 (16-byte aligned superset)
-                const uint64_t olo = seg0 - (seg0 & 1), ohi = seg1 + 2;
-                uint64_t* so = reinterpret_cast<uint64_t*>(stage + L::kStageKeys + L::kStageVals);
-                if (RL) {
-                    mt[6] = ~uint64_t(0);  // implicit offsets
-                } else if (ohi - olo + 1 <= uint64_t(L::SEGCAP)) {
-                    const uint32_t oa = stage_copy_plan(args.aoff, args.nseg + 1, olo, ohi, so, 2);
-                    const uint32_t obb =
-                        stage_copy_plan(args.boff, args.nseg + 1, olo, ohi, so + L::SEGCAP, 2);
-                    ob = oa + obb;
-                    mt[6] = olo + 1;  // staged (0 = read from global)
-                    mbar_arrive_expect_tx(&full[st], ab + bb + ob);
-                    if (oa) tma_load_1d(so, args.aoff + olo, oa, &full[st], policy);
-                    if (obb) tma_load_1d(so + L::SEGCAP, args.boff + olo, obb, &full[st], policy);
-                } else {
-                    mt[6] = 0;
-                }
-            }
-            if (ob == 0) mbar_arrive_expect_tx(&full[st], ab + bb + avb + bvb);
+            if constexpr (SEG) mt[6] = seg1 - seg0 + 1 <= uint64_t(L::SEGCAP) ? 1 : 0;  // table?
+            mbar_arrive_expect_tx(&full[st], ab + bb + avb + bvb);
             if (RL) {
                 stage_runs(a, m + n, j0, j1, RL, 0, sk, VECE, true, &full[st], policy);
                 stage_runs(b, m + n, k0, k1, RL, 1, sk + b_base, VECE, true, &full[st], policy);
@@ -1006,28 +1017,11 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             if (SEG == 2 && s_lo == s_hi) {  // merge pass, one segment: a plain merge
                 merge_thread<K, VT, false>(sk + a_off, a_len, sk + b_base + b_off, b_len, diag,
                                            keys, src);
-            } else if (mt[6]) {  // offsets staged: build the segment-end table, then merge
-                const uint64_t* so =
-                    reinterpret_cast<const uint64_t*>(stage + L::kStageKeys + L::kStageVals);
-                uint32_t* se = reinterpret_cast<uint32_t*>(smem + L::oSegEnd);
-                const int nse = int(s_hi - s_lo) + 1;
-                if (tid < nse) {
-                    uint64_t ae, be;
-                    if (SEG == 2) {  // merge pass: implicit offsets
-                        ae = run_off(s_lo + uint64_t(tid) + 1, args.run_len, args.m);
-                        be = run_off(s_lo + uint64_t(tid) + 1, args.run_len, args.n);
-                    } else {
-                        const uint64_t x = s_lo + uint64_t(tid) + 1 - (mt[6] - 1);
-                        ae = so[x];
-                        be = so[L::SEGCAP + x];
-                    }
-                    const uint64_t j0 = i0 - k0;
-                    const uint32_t x1 = ae > j0 ? uint32_t(min(ae - j0, uint64_t(a_len))) : 0u;
-                    const uint32_t y1 = be > k0 ? uint32_t(min(be - k0, uint64_t(b_len))) : 0u;
-                    se[tid] = x1 | (y1 << 16);
-                }
-                named_bar_sync(1, NC);
-                merge_thread_segends<K, VT>(sk + a_off, sk + b_base + b_off, diag, se, nse, keys);
+            } else if (mt[6]) {  // the producer's segment-end table
+                const uint32_t* se = reinterpret_cast<const uint32_t*>(stage + L::kStageKeys +
+                                                                       L::kStageVals);
+                merge_thread_segends<K, VT>(sk + a_off, sk + b_base + b_off, diag, se,
+                                            int(s_hi - s_lo) + 1, keys);
             } else {
                 const seg_offsets off{args.aoff, args.boff, 0, false};
                 merge_thread_seg<K, VT>(sk + a_off, a_len, sk + b_base + b_off, b_len, diag, i0,
