@@ -495,15 +495,18 @@ __device__ __forceinline__ void merge_thread_segends(const K* sA, const K* sB, i
     int ia = x0 + l, ib = y0 + dl - l;
     K ka = sA[ia], kb = sB[ib];
     K ka1 = sA[ia + 1], kb1 = sB[ib + 1];
+    int rem = (x1 - ia) + (y1 - ib);  // outputs left in the current segment
 #pragma unroll
     for (int v = 0; v < VT; ++v) {
-        if (ia >= x1 && ib >= y1 && k < nse - 1) {  // next segment (rare)
+        if (rem == 0 && k < nse - 1) {  // next non-empty segment (rare)
             do {
                 e1 = se[++k];
                 x1 = int(e1 & 0xffffu);
                 y1 = int(e1 >> 16);
-            } while (ia >= x1 && ib >= y1 && k < nse - 1);
+                rem = (x1 - ia) + (y1 - ib);
+            } while (rem == 0 && k < nse - 1);
         }
+        --rem;
         const bool take_b = ib < y1 && (ia >= x1 || kb < ka);
         keys[v] = take_b ? kb : ka;
         if (take_b) {
