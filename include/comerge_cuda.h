@@ -160,6 +160,19 @@ int comerge_cuda_sort_keys_u32(const uint32_t* keys, size_t n, uint32_t* out, vo
                                size_t ws_bytes, comerge_stream_t stream);
 int comerge_cuda_sort_keys_u64(const uint64_t* keys, size_t n, uint64_t* out, void* ws,
                                size_t ws_bytes, comerge_stream_t stream);
+/* Stable key-value merge sort: the uint32 payload moves with its key, equal
+ * keys keep their input order (std::stable_sort of {key, val} by key).  Out
+ * arrays may equal the inputs. */
+size_t comerge_cuda_sort_pairs_workspace_bytes(size_t n, int key_kind);
+int comerge_cuda_sort_pairs_i32(const int32_t* keys, const uint32_t* vals, size_t n,
+                                int32_t* out_keys, uint32_t* out_vals, void* ws, size_t ws_bytes,
+                                comerge_stream_t stream);
+int comerge_cuda_sort_pairs_u32(const uint32_t* keys, const uint32_t* vals, size_t n,
+                                uint32_t* out_keys, uint32_t* out_vals, void* ws, size_t ws_bytes,
+                                comerge_stream_t stream);
+int comerge_cuda_sort_pairs_u64(const uint64_t* keys, const uint32_t* vals, size_t n,
+                                uint64_t* out_keys, uint32_t* out_vals, void* ws, size_t ws_bytes,
+                                comerge_stream_t stream);
 
 /* Batched co-rank (Algorithm 1 exactly, corank.hpp:72-121): for each
  * ranks[q] (device array) writes j (k = ranks[q] - j) and, if the pointers

@@ -312,6 +312,45 @@ int oracle_merge_sort(int kind, const void* in, uint64_t n, void* out) {
     return 0;
 }
 
+int oracle_merge_sort_pairs(int kind, const void* in, const uint32_t* in_v, uint64_t n,
+                            void* out, uint32_t* out_v) {
+    const size_t s = key_size(kind);
+    char* x = (char*)malloc(n ? n * s : 1);
+    char* y = (char*)malloc(n ? n * s : 1);
+    uint32_t* xv = (uint32_t*)malloc(n ? n * 4 : 1);
+    uint32_t* yv = (uint32_t*)malloc(n ? n * 4 : 1);
+    if (!x || !y || !xv || !yv) {
+        free(x);
+        free(y);
+        free(xv);
+        free(yv);
+        return -1;
+    }
+    memcpy(x, in, n * s);
+    memcpy(xv, in_v, n * 4);
+    for (uint64_t w = 1; w < n; w *= 2) {
+        for (uint64_t lo = 0; lo < n; lo += 2 * w) {
+            const uint64_t mid = lo + w < n ? lo + w : n;
+            const uint64_t hi = lo + 2 * w < n ? lo + 2 * w : n;
+            oracle_merge_into(kind, x + lo * s, xv + lo, mid - lo, x + mid * s, xv + mid, hi - mid,
+                              y + lo * s, yv + lo);
+        }
+        char* t = x;
+        x = y;
+        y = t;
+        uint32_t* tv = xv;
+        xv = yv;
+        yv = tv;
+    }
+    memcpy(out, x, n * s);
+    memcpy(out_v, xv, n * 4);
+    free(x);
+    free(y);
+    free(xv);
+    free(yv);
+    return 0;
+}
+
 /* ---------------------------------------------- Algorithm 2 (parallel.hpp) */
 
 typedef struct {

@@ -61,6 +61,7 @@ class Port:
                                               C.c_int, _p, _p]
         lib.oracle_merge_segmented.argtypes = [C.c_int, _p, _p, _p, _p, _u64, _p, C.c_int]
         lib.oracle_merge_sort.argtypes = [C.c_int, _p, _u64, _p]
+        lib.oracle_merge_sort_pairs.argtypes = [C.c_int, _p, _p, _u64, _p, _p]
         lib.oracle_merge_report.argtypes = [C.c_int, _p, _u64, _p, _u64, _u64, C.c_int, _p, _p,
                                             C.POINTER(_u64)]
         lib.oracle_generate_sorted.argtypes = [C.c_int, _u64, _u64, _u64, _u64, _p]
@@ -132,6 +133,16 @@ class Port:
         if rc:
             raise MemoryError("oracle_merge_sort: allocation failed")
         return out
+
+    def merge_sort_pairs(self, keys, vals):
+        keys = np.ascontiguousarray(keys)
+        vals = np.ascontiguousarray(vals, dtype=np.uint32)
+        ok, ov = np.empty_like(keys), np.empty_like(vals)
+        rc = self.lib.oracle_merge_sort_pairs(kind_of(keys), ptr(keys), ptr(vals), len(keys),
+                                              ptr(ok), ptr(ov))
+        if rc:
+            raise MemoryError("oracle_merge_sort_pairs: allocation failed")
+        return ok, ov
 
     def generate_sorted(self, dtype, seed, lane, length, width):
         out = np.empty(length, dtype=dtype)

@@ -7,10 +7,11 @@ the reference API (see ``comerge``).
 from .comerge import (BlockAssignment, ComparisonCounter, CoRankStats, MergeOptions,  # noqa: F401
                       MergeReport, co_rank, co_rank_batch, co_rank_counted, merge_pairs,
                       merge_parallel, merge_parallel_synced, merge_segmented, partition_output,
-                      plan, set_kernel_path, sort, sort_workspace_bytes, stable_merge,
+                      plan, set_kernel_path, sort, sort_pairs, sort_pairs_workspace_bytes,
+                      sort_workspace_bytes, stable_merge,
                       workspace_bytes)
 
 __all__ = ["co_rank", "co_rank_counted", "co_rank_batch", "stable_merge", "partition_output",
            "plan", "merge_parallel", "merge_parallel_synced", "merge_pairs", "merge_segmented",
-           "sort", "sort_workspace_bytes", "set_kernel_path", "workspace_bytes",
+           "sort", "sort_workspace_bytes", "sort_pairs", "sort_pairs_workspace_bytes", "set_kernel_path", "workspace_bytes",
            "MergeReport", "MergeOptions", "CoRankStats", "ComparisonCounter", "BlockAssignment"]

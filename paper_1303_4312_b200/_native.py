@@ -68,8 +68,12 @@ def _load():
             C.POINTER(C.c_uint32)]
     lib.comerge_cuda_sort_workspace_bytes.argtypes = [_sz, _i]
     lib.comerge_cuda_sort_workspace_bytes.restype = _sz
+    lib.comerge_cuda_sort_pairs_workspace_bytes.argtypes = [_sz, _i]
+    lib.comerge_cuda_sort_pairs_workspace_bytes.restype = _sz
     for suf in ("i32", "u32", "u64"):
         getattr(lib, f"comerge_cuda_sort_keys_{suf}").argtypes = [_p, _sz, _p, _p, _sz, _p]
+        getattr(lib, f"comerge_cuda_sort_pairs_{suf}").argtypes = [_p, _p, _sz, _p, _p, _p, _sz,
+                                                                   _p]
     for suf in ("i32", "u32"):
         getattr(lib, f"comerge_cuda_merge_segmented_{suf}").argtypes = [
             _p, _p, _sz, _p, _p, _sz, _sz, _p, _p, _sz, _p]

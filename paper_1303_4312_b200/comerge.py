@@ -385,3 +385,33 @@ def sort(keys, out=None, workspace=None):
         _ptr(keys), _len(keys), _ptr(out), wsp, wsb, _stream(keys)))
     return out
 
+
+def sort_pairs(keys, vals, out_keys=None, out_vals=None, workspace=None):
+    """Stable key-value merge sort of device tensors (uint32 payloads move
+    with their keys; equal keys keep their input order)."""
+    if not (_is_torch(keys) and keys.is_cuda):
+        raise TypeError("sort_pairs: keys must be a CUDA tensor (there is no host path)")
+    suf = _suffix(keys)
+    if _len(vals) != _len(keys):
+        raise ValueError("sort_pairs: payload length must equal key length")
+    if out_keys is None:
+        out_keys = _empty_like_merge(keys, _len(keys))
+    if out_vals is None:
+        out_vals = _empty_like_merge(vals, _len(vals))
+    if _len(out_keys) != _len(keys) or _len(out_vals) != _len(keys):
+        raise ValueError("sort_pairs: output length must equal the input length")
+    if workspace is None:
+        wsp, wsb = None, 0
+    else:
+        wsp, wsb = _ws(workspace)
+    N.check(getattr(N.lib, f"comerge_cuda_sort_pairs_{suf}")(
+        _ptr(keys), _ptr(vals), _len(keys), _ptr(out_keys), _ptr(out_vals), wsp, wsb,
+        _stream(keys)))
+    return out_keys, out_vals
+
+
+def sort_pairs_workspace_bytes(n, dtype):
+    name = str(dtype).replace("torch.", "") if torch is not None and isinstance(dtype, torch.dtype) \
+        else np.dtype(dtype).name
+    return int(N.lib.comerge_cuda_sort_pairs_workspace_bytes(int(n), _KIND[_SUFFIX[name]]))
+

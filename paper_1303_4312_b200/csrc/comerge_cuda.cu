@@ -1014,6 +1014,72 @@ size_t sort_ws_bytes(size_t n) {
 }
 
 template <typename K>
+size_t sort_pairs_ws_bytes(size_t n) {
+    if (n == 0) return 0;
+    const size_t buf = round256(n * sizeof(K)) + round256(n * 4);
+    const size_t tail = round256(32 * (div_up(n, pipe_layout<K, true, 2>::T) + 2));
+    return 2 * buf + tail;
+}
+
+// Stable key-value merge sort: as sort_device, the payload moving with its key.
+template <typename K>
+int sort_pairs_device(const K* keys, const uint32_t* vals, size_t n, K* out, uint32_t* out_v,
+                      void* ws, size_t ws_bytes, cudaStream_t s) {
+    if (n && (!keys || !vals || !out || !out_v))
+        return fail(COMERGE_E_INVALID, "sort_pairs: null pointer");
+    if (n == 0) return COMERGE_OK;
+    if (n > (size_t(1) << 40)) return fail(COMERGE_E_LENGTH, "sort_pairs: more than 2^40 elements");
+    if ((keys != out && overlaps(keys, n * sizeof(K), out, n * sizeof(K))) ||
+        (vals != out_v && overlaps(vals, n * 4, out_v, n * 4)) ||
+        overlaps(out, n * sizeof(K), out_v, n * 4))
+        return fail(COMERGE_E_INVALID, "sort_pairs: outputs must not partially overlap the inputs or each other");
+    constexpr uint64_t R = sort_pairs_cfg<K>::R;
+    const uint64_t nblocks = div_up(n, R);
+    uint32_t passes = 0;
+    while ((R << passes) < n) ++passes;
+    if (passes == 0) {
+        block_sort_pairs_kernel<K><<<unsigned(nblocks), sort_pairs_cfg<K>::NT, 0, s>>>(
+            keys, vals, out, out_v, n);
+        return check_launch("comerge: block sort launch");
+    }
+    scratch sc;
+    if (int rc = sc.acquire(ws, ws_bytes, sort_pairs_ws_bytes<K>(n), s)) return rc;
+    unsigned char* w = static_cast<unsigned char*>(sc.ptr);
+    const size_t kb = round256(n * sizeof(K)), vb = round256(n * 4);
+    K* tk[2] = {reinterpret_cast<K*>(w), reinterpret_cast<K*>(w + kb + vb)};
+    uint32_t* tv[2] = {reinterpret_cast<uint32_t*>(w + kb),
+                       reinterpret_cast<uint32_t*>(w + 2 * kb + vb)};
+    unsigned char* tail = w + 2 * (kb + vb);
+    const size_t tail_bytes = sort_pairs_ws_bytes<K>(n) - 2 * (kb + vb);
+    const bool direct = aligned16(out) && aligned16(out_v);
+    K* bk[2] = {direct ? out : tk[1], tk[0]};
+    uint32_t* bv[2] = {direct ? out_v : tv[1], tv[0]};
+    K* ck = bk[passes & 1];
+    uint32_t* cv = bv[passes & 1];
+    block_sort_pairs_kernel<K><<<unsigned(nblocks), sort_pairs_cfg<K>::NT, 0, s>>>(keys, vals, ck,
+                                                                                  cv, n);
+    if (int rc = check_launch("comerge: block sort launch")) return rc;
+    uint64_t L = R;
+    for (uint32_t p = 0; p < passes; ++p, L *= 2) {
+        K* dk = bk[(passes - p - 1) & 1];
+        uint32_t* dv = bv[(passes - p - 1) & 1];
+        const uint64_t full = n / (2 * L), rem = n % (2 * L);
+        const uint64_t ma = full * L + (rem < L ? rem : L), mb = n - ma;
+        if (int rc = launch_pipe<K, true, 2>(ck, cv, ma, ck, cv, mb, dk, dv, nullptr, nullptr,
+                                             div_up(n, 2 * L), tail, tail_bytes, s, L))
+            return rc;
+        ck = dk;
+        cv = dv;
+    }
+    if (ck != out) {
+        cudaError_t e = cudaMemcpyAsync(out, ck, n * sizeof(K), cudaMemcpyDeviceToDevice, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(out_v, cv, n * 4, cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) return cuda_fail(e, "comerge: sort result copy");
+    }
+    return COMERGE_OK;
+}
+
+template <typename K>
 int sort_device(const K* keys, size_t n, K* out, void* ws, size_t ws_bytes, cudaStream_t s) {
     if (n && (!keys || !out)) return fail(COMERGE_E_INVALID, "sort: null pointer");
     if (n == 0) return COMERGE_OK;
@@ -1175,6 +1241,25 @@ int comerge_cuda_merge_segmented_u32(const uint32_t* a, const uint64_t* a_off, s
 
 size_t comerge_cuda_sort_workspace_bytes(size_t n, int key_kind) {
     return key_kind == COMERGE_KEY_U64 ? sort_ws_bytes<uint64_t>(n) : sort_ws_bytes<uint32_t>(n);
+}
+size_t comerge_cuda_sort_pairs_workspace_bytes(size_t n, int key_kind) {
+    return key_kind == COMERGE_KEY_U64 ? sort_pairs_ws_bytes<uint64_t>(n)
+                                       : sort_pairs_ws_bytes<uint32_t>(n);
+}
+int comerge_cuda_sort_pairs_i32(const int32_t* keys, const uint32_t* vals, size_t n,
+                                int32_t* out_keys, uint32_t* out_vals, void* ws, size_t ws_bytes,
+                                comerge_stream_t stream) {
+    return sort_pairs_device<int32_t>(keys, vals, n, out_keys, out_vals, ws, ws_bytes, stream);
+}
+int comerge_cuda_sort_pairs_u32(const uint32_t* keys, const uint32_t* vals, size_t n,
+                                uint32_t* out_keys, uint32_t* out_vals, void* ws, size_t ws_bytes,
+                                comerge_stream_t stream) {
+    return sort_pairs_device<uint32_t>(keys, vals, n, out_keys, out_vals, ws, ws_bytes, stream);
+}
+int comerge_cuda_sort_pairs_u64(const uint64_t* keys, const uint32_t* vals, size_t n,
+                                uint64_t* out_keys, uint32_t* out_vals, void* ws, size_t ws_bytes,
+                                comerge_stream_t stream) {
+    return sort_pairs_device<uint64_t>(keys, vals, n, out_keys, out_vals, ws, ws_bytes, stream);
 }
 int comerge_cuda_sort_keys_i32(const int32_t* keys, size_t n, int32_t* out, void* ws,
                                size_t ws_bytes, comerge_stream_t stream) {

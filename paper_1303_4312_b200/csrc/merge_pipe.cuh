@@ -464,10 +464,10 @@ __device__ __forceinline__ void merge_thread_seg(const K* sA, int a_len, const K
 // (a_len, b_len)).  A segment's windows start where the previous one's end,
 // so a segment change only moves the limits x1 / y1: the per-step cost over
 // merge_thread is one test, and the rare change is two shared loads.
-template <typename K, int VT>
+template <typename K, int VT, bool TRACK = false>
 __device__ __forceinline__ void merge_thread_segends(const K* sA, const K* sB, int diag,
                                                      const uint32_t* se, int nse,
-                                                     K (&keys)[VT]) {
+                                                     K (&keys)[VT], uint32_t (&src)[VT]) {
     int lo = 0, hi = nse - 1;  // first segment whose window part ends past diag
     while (lo < hi) {
         const int mid = (lo + hi) >> 1;
@@ -509,6 +509,7 @@ __device__ __forceinline__ void merge_thread_segends(const K* sA, const K* sB, i
         --rem;
         const bool take_b = ib < y1 && (ia >= x1 || kb < ka);
         keys[v] = take_b ? kb : ka;
+        if constexpr (TRACK) src[v] = take_b ? (uint32_t(ib) | 0x80000000u) : uint32_t(ia);
         if (take_b) {
             ++ib;
             kb = kb1;
@@ -531,7 +532,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
     constexpr int NST = L::NST;
     constexpr int VECE = L::VECE;
     constexpr int NB = L::NB;
-    static_assert(!(SEG && HAS_V), "segmented batches are keys-only");
+    static_assert(!(SEG == 1 && HAS_V), "explicit-offset segmented batches are keys-only");
 
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::oBars);
@@ -955,8 +956,11 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             if constexpr (HAS_V) {
                 av_off = uint32_t(j0 % 4);
                 bv_base = (av_off + a_len + 3) / 4 * 4;
-                avb = stage_copy_plan(args.av, m, j0, j1, sv, 4);
-                bvb = stage_copy_plan(args.bv, n, k0, k1, sv + bv_base, 4);
+                avb = RL ? stage_runs(args.av, m + n, j0, j1, RL, 0, sv, 4, false, nullptr, 0)
+                         : stage_copy_plan(args.av, m, j0, j1, sv, 4);
+                bvb = RL ? stage_runs(args.bv, m + n, k0, k1, RL, 1, sv + bv_base, 4, false,
+                                      nullptr, 0)
+                         : stage_copy_plan(args.bv, n, k0, k1, sv + bv_base, 4);
             }
             mt[0] = i0;
             mt[1] = k0;
@@ -973,9 +977,15 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
                 if (bb) tma_load_1d(sk + b_base, b + (k0 - k0 % VECE), bb, &full[st], policy);
             }
             if constexpr (HAS_V) {
-                if (avb) tma_load_1d(sv, args.av + (j0 - j0 % 4), avb, &full[st], policy);
-                if (bvb)
-                    tma_load_1d(sv + bv_base, args.bv + (k0 - k0 % 4), bvb, &full[st], policy);
+                if (RL) {
+                    stage_runs(args.av, m + n, j0, j1, RL, 0, sv, 4, true, &full[st], policy);
+                    stage_runs(args.bv, m + n, k0, k1, RL, 1, sv + bv_base, 4, true, &full[st],
+                               policy);
+                } else {
+                    if (avb) tma_load_1d(sv, args.av + (j0 - j0 % 4), avb, &full[st], policy);
+                    if (bvb)
+                        tma_load_1d(sv + bv_base, args.bv + (k0 - k0 % 4), bvb, &full[st], policy);
+                }
             }
         }
         return;
@@ -1018,17 +1028,19 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             const uint64_t k0 = mt[1];
             const uint64_t s_lo = mt[4], s_hi = mt[5];
             if (SEG == 2 && s_lo == s_hi) {  // merge pass, one segment: a plain merge
-                merge_thread<K, VT, false>(sk + a_off, a_len, sk + b_base + b_off, b_len, diag,
+                merge_thread<K, VT, HAS_V>(sk + a_off, a_len, sk + b_base + b_off, b_len, diag,
                                            keys, src);
             } else if (mt[6]) {  // the producer's segment-end table
                 const uint32_t* se = reinterpret_cast<const uint32_t*>(stage + L::kStageKeys +
                                                                        L::kStageVals);
-                merge_thread_segends<K, VT>(sk + a_off, sk + b_base + b_off, diag, se,
-                                            int(s_hi - s_lo) + 1, keys);
-            } else {
+                merge_thread_segends<K, VT, HAS_V>(sk + a_off, sk + b_base + b_off, diag, se,
+                                                   int(s_hi - s_lo) + 1, keys, src);
+            } else if constexpr (!HAS_V) {
                 const seg_offsets off{args.aoff, args.boff, 0, false};
                 merge_thread_seg<K, VT>(sk + a_off, a_len, sk + b_base + b_off, b_len, diag, i0,
                                         i0 - k0, k0, s_lo, s_hi, off, keys);
+            } else {
+                __trap();  // merge passes have at most a few segments per tile
             }
         } else {
             merge_thread<K, VT, HAS_V>(sk + a_off, a_len, sk + b_base + b_off, b_len, diag, keys,

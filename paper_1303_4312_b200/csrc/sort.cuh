@@ -97,4 +97,98 @@ __global__ void __launch_bounds__(sort_cfg<K>::NT)
     for (int x = t; x < cnt; x += NT) out[base + x] = s[spad(x)];
 }
 
+// Key-value variant: the uint32 payload moves with its key (VT = 8, runs of
+// 4096 pairs, 2048 for 64-bit keys; keys and payloads in two padded shared
+// arrays within the 48 KB static limit).
+template <typename K>
+struct sort_pairs_cfg {
+    static constexpr int NT = sizeof(K) == 8 ? 256 : 512;
+    static constexpr int VT = 8;
+    static constexpr int R = NT * VT;
+};
+
+template <typename K>
+__global__ void __launch_bounds__(sort_pairs_cfg<K>::NT)
+    block_sort_pairs_kernel(const K* __restrict__ in, const uint32_t* __restrict__ in_v,
+                            K* __restrict__ out, uint32_t* __restrict__ out_v, uint64_t n) {
+    constexpr int NT = sort_pairs_cfg<K>::NT, VT = sort_pairs_cfg<K>::VT,
+                  R = sort_pairs_cfg<K>::R;
+    __shared__ K s[R + R / 32 + 4];
+    __shared__ uint32_t sv[R + R / 32 + 4];
+    const uint64_t base = uint64_t(blockIdx.x) * R;
+    const int cnt = n - base < uint64_t(R) ? int(n - base) : R;
+    const int t = threadIdx.x;
+    const K pad = std::numeric_limits<K>::max();
+    for (int x = t; x < R; x += NT) {
+        s[spad(x)] = x < cnt ? in[base + x] : pad;
+        sv[spad(x)] = x < cnt ? in_v[base + x] : 0u;
+    }
+    __syncthreads();
+    K k[VT];
+    uint32_t p[VT];
+#pragma unroll
+    for (int v = 0; v < VT; ++v) {
+        k[v] = s[spad(t * VT + v)];
+        p[v] = sv[spad(t * VT + v)];
+    }
+#pragma unroll
+    for (int pass = 0; pass < VT; ++pass) {
+#pragma unroll
+        for (int v = pass & 1; v + 1 < VT; v += 2) {
+            if (k[v + 1] < k[v]) {  // strict: equal keys keep their order
+                const K x = k[v];
+                k[v] = k[v + 1];
+                k[v + 1] = x;
+                const uint32_t y = p[v];
+                p[v] = p[v + 1];
+                p[v + 1] = y;
+            }
+        }
+    }
+    for (int w = VT; w < R; w *= 2) {
+        __syncthreads();
+#pragma unroll
+        for (int v = 0; v < VT; ++v) {
+            s[spad(t * VT + v)] = k[v];
+            sv[spad(t * VT + v)] = p[v];
+        }
+        __syncthreads();
+        const int d = t * VT;
+        const int a0 = d / (2 * w) * (2 * w), b0 = a0 + w;
+        const int diag = d - a0;
+        int lo = diag > w ? diag - w : 0, hi = diag < w ? diag : w;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s[spad(b0 + diag - mid)] < s[spad(a0 + mid - 1)])
+                hi = mid - 1;
+            else
+                lo = mid;
+        }
+        int ia = lo, ib = diag - lo;
+        K ka = s[spad(a0 + ia)], kb = s[spad(b0 + ib)];
+#pragma unroll
+        for (int v = 0; v < VT; ++v) {
+            const bool take_b = ib < w && (ia >= w || kb < ka);
+            k[v] = take_b ? kb : ka;
+            p[v] = sv[spad(take_b ? b0 + ib : a0 + ia)];
+            ia += take_b ? 0 : 1;
+            ib += take_b ? 1 : 0;
+            const K nx = s[spad(take_b ? b0 + ib : a0 + ia)];
+            ka = take_b ? ka : nx;
+            kb = take_b ? nx : kb;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int v = 0; v < VT; ++v) {
+        s[spad(t * VT + v)] = k[v];
+        sv[spad(t * VT + v)] = p[v];
+    }
+    __syncthreads();
+    for (int x = t; x < cnt; x += NT) {
+        out[base + x] = s[spad(x)];
+        out_v[base + x] = sv[spad(x)];
+    }
+}
+
 }  // namespace comerge_b200

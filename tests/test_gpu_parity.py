@@ -514,3 +514,36 @@ def test_comparison_counts_large_host_pipeline(cuda, port):
         _, _, total = port.merge_report(a, b, w, synced)
         assert rep.comparisons == total
     assert np.array_equal(out, port.merge(a, b))
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.uint32, np.uint64])
+def test_sort_pairs_stability_against_oracle(cuda, port, dt):
+    """Key-value sort: payload = input index, so stability is visible."""
+    R = 4096 if np.dtype(dt).itemsize == 4 else 2048
+    rng = np.random.default_rng(8)
+    for n in (0, 1, 9, R - 1, R, R + 1, 2 * R + 3, 5 * R + 7, 100_003, 1 << 20):
+        for alphabet in (2, 1000, None):
+            if alphabet is None:
+                info = np.iinfo(dt)
+                k = rng.integers(info.min, info.max, n, dtype=dt, endpoint=True)
+            else:
+                k = rng.integers(0, alphabet, n).astype(dt)
+            v = rng.permutation(n).astype(np.uint32)
+            ok, ov = P().sort_pairs(dev(k, cuda), dev(v, cuda))
+            ek, ev = port.merge_sort_pairs(k, v)
+            assert np.array_equal(host(ok), ek) and np.array_equal(host(ov), ev), (dt, n, alphabet)
+
+
+def test_sort_pairs_in_place_and_misaligned(cuda, port):
+    n = 123_457
+    rng = np.random.default_rng(10)
+    k = rng.integers(0, 50, n).astype(np.int32)
+    v = np.arange(n, dtype=np.uint32)
+    tk, tv = dev(k, cuda), dev(v, cuda)
+    P().sort_pairs(tk, tv, out_keys=tk, out_vals=tv)
+    ek, ev = port.merge_sort_pairs(k, v)
+    assert np.array_equal(host(tk), ek) and np.array_equal(host(tv), ev)
+    bk = torch.empty(n + 1, dtype=torch.int32, device=cuda)
+    bv = torch.empty(n + 3, dtype=torch.uint32, device=cuda)
+    ok, ov = P().sort_pairs(dev(k, cuda), dev(v, cuda), out_keys=bk[1:], out_vals=bv[3:])
+    assert np.array_equal(host(ok), ek) and np.array_equal(host(ov), ev)

@@ -268,3 +268,14 @@ def test_oracle_comparison_counts_match_reference(port, golden):
                 for synced in (0, 1):
                     _, _, total = port.merge_report(a, b, w, bool(synced))
                     assert total == int(counts[wi, synced]), (name, c, w, synced)
+
+
+def test_oracle_merge_sort_pairs_is_stable(port):
+    rng = np.random.default_rng(3)
+    for dt in (np.int32, np.uint64):
+        for n in (0, 1, 7, 1000, 4097):
+            k = rng.integers(0, 9, n).astype(dt)
+            v = np.arange(n, dtype=np.uint32)
+            ok, ov = port.merge_sort_pairs(k, v)
+            idx = np.argsort(k, kind="stable")
+            assert np.array_equal(ok, k[idx]) and np.array_equal(ov, v[idx])
