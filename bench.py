@@ -490,6 +490,48 @@ def reference_arm(args):
         dist.destroy_process_group()
 
 
+def sort_extras(device, reps=5):
+    """SURVEY 8f row 1 (not a BASELINE config): the stable merge sorts on
+    2^26 int32 keys (uniform 31-bit, seeded) with and without uint32 payloads,
+    median device time (events, L2 flushed before each rep)."""
+    import torch
+    import paper_1303_4312_b200 as P
+    import paper_1303_4312_b200._native as N
+    n = 1 << 26
+    raw = torch.empty(n, dtype=torch.int64, device=device)
+    N.check(N.lib.comerge_testkit_generate_raw(SEED, 0, n, 1 << 31, raw.data_ptr(), None), True)
+    k = raw.to(torch.int32)
+    del raw
+    v = torch.arange(n, dtype=torch.int32, device=device).view(torch.uint32)
+    ok, ov = torch.empty_like(k), torch.empty_like(v)
+    ws = torch.empty(max(P.sort_workspace_bytes(n, torch.int32),
+                         P.sort_pairs_workspace_bytes(n, torch.int32)), dtype=torch.uint8,
+                     device=device)
+    flush = torch.empty(512 * 2**20 // 4, dtype=torch.int32, device=device)
+
+    def med(fn):
+        ts = []
+        for r in range(reps + 2):
+            flush.fill_(r)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            if r >= 2:
+                ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
+
+    t_keys = med(lambda: P.sort(k, out=ok, workspace=ws))
+    t_pairs = med(lambda: P.sort_pairs(k, v, out_keys=ok, out_vals=ov, workspace=ws))
+    out = {"workload": "2^26 int32 keys, uniform [0, 2^31), seeded; stable merge sort",
+           "keys_ms": t_keys, "keys_per_s": n / (t_keys * 1e-3),
+           "pairs_ms": t_pairs, "pairs_per_s": n / (t_pairs * 1e-3)}
+    del k, v, ok, ov, ws, flush
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -540,6 +582,7 @@ def main():
             del r
             torch.cuda.empty_cache()
 
+    sorts = None if args.only_headline else sort_extras(device)
     e2e = None if args.no_e2e or rank != 0 else e2e_measure(cfg, res["inp"], min(args.steps, 5), 1)
     cpu = None if args.no_cpu or rank != 0 else cpu_baseline(cfg, res["inp"])
     if rank == 0:
@@ -559,7 +602,7 @@ def main():
                           step_gbs=head["step_gbs"], frac_of_8tbs=head["frac_of_8tbs"]),
             cpu_baseline=cpu, e2e=e2e, clocks=res["clocks"],
             gpu_launches=args.steps * head["launches_per_step"],
-            configs=per_config)
+            configs=per_config, sorts=sorts)
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
