@@ -19,7 +19,8 @@ extern "C" {
 int comerge_testkit_generate_sorted(int key_kind, uint64_t seed, uint64_t lane, size_t len,
                                     uint64_t width, void* out, comerge_stream_t stream);
 
-/* Unsorted accepted draws (uint64) of stream(seed, lane), in stream order. */
+/* Unsorted accepted draws (uint64) of stream(seed, lane), in stream order.
+ * The seeded generators take at most 2^31 - 2^20 draws per call. */
 int comerge_testkit_generate_raw(uint64_t seed, uint64_t lane, size_t len, uint64_t width,
                                  uint64_t* out, comerge_stream_t stream);
 
@@ -29,6 +30,11 @@ int comerge_testkit_generate_raw(uint64_t seed, uint64_t lane, size_t len, uint6
 int comerge_testkit_generate_runs(int key_kind, uint64_t seed, uint64_t lane,
                                   const uint64_t* offsets, size_t nseg, size_t total,
                                   uint64_t width, void* out, comerge_stream_t stream);
+
+/* out[i] = (i + offset) / run_len as the key kind: sorted runs of equal keys
+ * (inputs of any size without a sort, for the 64-bit-index tests). */
+int comerge_testkit_fill_runs(int key_kind, size_t len, uint64_t run_len, uint64_t offset,
+                              void* out, comerge_stream_t stream);
 
 /* out[i] = i | tag  (payloads: A tag 0, B tag 1u<<31). */
 int comerge_testkit_iota(uint32_t* out, size_t len, uint32_t tag, comerge_stream_t stream);

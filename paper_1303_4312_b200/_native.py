@@ -93,6 +93,7 @@ def _load():
     lib.comerge_partition_output.argtypes = [_u64, _u64, _u64, C.POINTER(_u64)]
     lib.comerge_testkit_generate_sorted.argtypes = [_i, _u64, _u64, _sz, _u64, _p, _p]
     lib.comerge_testkit_iota.argtypes = [_p, _sz, C.c_uint32, _p]
+    lib.comerge_testkit_fill_runs.argtypes = [_i, _sz, _u64, _u64, _p, _p]
     lib.comerge_testkit_verify_pairs.argtypes = [_i, _p, _sz, _p, _sz, _p, _p, _p, _p]
     lib.comerge_testkit_checksum.argtypes = [_i, _p, _sz, _p, _p]
     lib.comerge_testkit_count_unsorted.argtypes = [_i, _p, _sz, _p, _p]

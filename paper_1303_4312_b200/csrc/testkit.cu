@@ -53,6 +53,14 @@ __global__ void narrow_kernel(const uint64_t* __restrict__ in, uint64_t len, K* 
     if (t < len) out[t] = K(uint32_t(in[t]));
 }
 
+// out[i] = (i + offset) / run_len: sorted keys in runs of equal values
+template <typename K>
+__global__ void fill_runs_kernel(K* out, uint64_t len, uint64_t run_len, uint64_t offset) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        out[i] = K((i + offset) / run_len);
+}
+
 __global__ void iota_kernel(uint32_t* out, uint64_t len, uint32_t tag) {
     const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t < len) out[t] = uint32_t(t) | tag;
@@ -135,6 +143,10 @@ unsigned grid_for(uint64_t n, unsigned threads) {
 int draw_accepted(uint64_t seed, uint64_t lane, size_t len, uint64_t width, uint64_t** out,
                   cudaStream_t s) {
     *out = nullptr;
+    if (len > (uint64_t(1) << 31) - (uint64_t(1) << 20)) {  // CUB selects count in int
+        g_tk_error = "testkit: at most 2^31 - 2^20 draws per call";
+        return COMERGE_E_LENGTH;
+    }
     const uint64_t state0 = mix64(seed) ^ mix64(lane + 1);
     const uint64_t limit = width ? width * (UINT64_MAX / width) : 0;
     const long double p_rej =
@@ -289,6 +301,26 @@ int comerge_testkit_generate_runs(int key_kind, uint64_t seed, uint64_t lane,
                                        static_cast<uint32_t*>(out), stream);
     }
     return COMERGE_E_INVALID;
+}
+
+int comerge_testkit_fill_runs(int key_kind, size_t len, uint64_t run_len, uint64_t offset,
+                              void* out, comerge_stream_t stream) {
+    if (len == 0) return COMERGE_OK;
+    if (run_len == 0) return tk_fail(cudaErrorInvalidValue, "testkit: run length 0");
+    const unsigned g = grid_for(len, 256);
+    switch (key_kind) {
+    case COMERGE_KEY_I32:
+        fill_runs_kernel<int32_t><<<g, 256, 0, stream>>>(static_cast<int32_t*>(out), len, run_len, offset);
+        break;
+    case COMERGE_KEY_U32:
+        fill_runs_kernel<uint32_t><<<g, 256, 0, stream>>>(static_cast<uint32_t*>(out), len, run_len, offset);
+        break;
+    default:
+        fill_runs_kernel<uint64_t><<<g, 256, 0, stream>>>(static_cast<uint64_t*>(out), len, run_len, offset);
+        break;
+    }
+    const cudaError_t e = cudaGetLastError();
+    return e ? tk_fail(e, "testkit: fill_runs") : COMERGE_OK;
 }
 
 int comerge_testkit_iota(uint32_t* out, size_t len, uint32_t tag, comerge_stream_t stream) {

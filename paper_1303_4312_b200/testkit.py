@@ -49,6 +49,16 @@ def generate_runs(dtype, seed: int, lane: int, offsets, width: int):
     return out
 
 
+def fill_runs(length: int, run_len: int, dtype, offset: int = 0, device="cuda"):
+    """Sorted keys (i + offset) // run_len of `dtype` on the device."""
+    out = torch.empty(length, dtype=dtype, device=device)
+    if length:
+        N.check(N.lib.comerge_testkit_fill_runs(_KIND[dtype], length, run_len, offset,
+                                                 C.c_void_p(out.data_ptr()),
+                                                 _stream(out.device)), testkit=True)
+    return out
+
+
 def iota(length: int, tag: int, device="cuda"):
     """uint32 payloads i | tag (A: tag 0, B: tag 1<<31)."""
     out = torch.empty(length, dtype=torch.uint32, device=device)

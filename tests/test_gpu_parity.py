@@ -547,3 +547,90 @@ def test_sort_pairs_in_place_and_misaligned(cuda, port):
     bv = torch.empty(n + 3, dtype=torch.uint32, device=cuda)
     ok, ov = P().sort_pairs(dev(k, cuda), dev(v, cuda), out_keys=bk[1:], out_vals=bv[3:])
     assert np.array_equal(host(ok), ek) and np.array_equal(host(ov), ev)
+
+
+# ------------------------------------------- 64-bit sizes (> 2^32 elements)
+# The API indexes with size_t (up to 2^40); these runs cross 2^32 in the
+# output (and in one input) so every 32-bit truncation would show.  Inputs are
+# sorted runs of equal keys made on the device; properties are size-independent
+# (sortedness + multiset checksum fix a keys-only merge / sort uniquely; the
+# tagged check fixes a key-value merge).
+
+def _free_gb():
+    free, _ = torch.cuda.mem_get_info()
+    return free / 2**30
+
+
+def test_max_size_keys_merge_crosses_2_32(cuda):
+    from paper_1303_4312_b200 import testkit as tk
+    m, n = (1 << 32) + 5, (1 << 31) + 3
+    if _free_gb() < 60:
+        pytest.skip("needs ~52 GB of device memory")
+    a = tk.fill_runs(m, 3, torch.int32)
+    b = tk.fill_runs(n, 2, torch.int32, offset=1)
+    out = P().stable_merge(a, b)
+    torch.cuda.synchronize()
+    assert tk.count_unsorted(out) == 0
+    assert tk.checksum(out) == (tk.checksum(a) + tk.checksum(b)) % 2**64
+    # the boundary at output rank 2^32 + 1: Algorithm 1 on the device agrees with
+    # the closed form (A run of 3 equal keys, B run of 2, B offset by 1)
+    i = (1 << 32) + 1
+    j, k = P().co_rank(i, a, b)
+    assert j + k == i and 0 <= j <= m and 0 <= k <= n
+    if j > 0 and k < n:
+        assert not (int(b[k]) < int(a[j - 1]))
+    if k > 0 and j < m:
+        assert int(b[k - 1]) < int(a[j])
+    del a, b, out
+    torch.cuda.empty_cache()
+
+
+def test_max_size_pairs_merge_crosses_2_32(cuda):
+    """A = K runs of 3 equal keys, B = K runs of 5 (same key range), payloads
+    = raw input indices: the stable merge is known in closed form -- output
+    8k..8k+2 are A's 3k..3k+2, 8k+3..8k+7 are B's 5k..5k+4 -- and is checked
+    position by position (in chunks) across 2^32."""
+    from paper_1303_4312_b200 import testkit as tk
+    K = (1 << 29) + 8
+    m, n = 3 * K, 5 * K  # total 8K > 2^32; payload indices < 2^32
+    if _free_gb() < 80:
+        pytest.skip("needs ~70 GB of device memory")
+    a = tk.fill_runs(m, 3, torch.int32)
+    b = tk.fill_runs(n, 5, torch.int32)
+    av, bv = tk.iota(m, 0), tk.iota(n, 0)
+    ok, ov = P().merge_pairs(a, av, b, bv)
+    torch.cuda.synchronize()
+    del a, b, av, bv
+    total = m + n
+    step = 1 << 28
+    for p0 in range(0, total, step):
+        p = torch.arange(p0, min(p0 + step, total), dtype=torch.int64, device=cuda)
+        k, r = p // 8, p % 8
+        exp_pay = torch.where(r < 3, 3 * k + r, 5 * k + r - 3)
+        assert torch.equal(ok[p0:p0 + len(p)].to(torch.int64), k), p0
+        got = ov[p0:p0 + len(p)].view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+        assert torch.equal(got, exp_pay), p0
+    del ok, ov
+    torch.cuda.empty_cache()
+
+
+def test_max_size_sort_crosses_2_32(cuda):
+    from paper_1303_4312_b200 import testkit as tk
+    n = (1 << 32) + 17
+    if _free_gb() < 80:
+        pytest.skip("needs ~70 GB of device memory")
+    # scrambled keys (a multiplicative hash of the index; the testkit's
+    # generator draws at most 2^31 per call)
+    keys = torch.empty(n, dtype=torch.int32, device=cuda)
+    step = 1 << 28
+    for p0 in range(0, n, step):
+        p = torch.arange(p0, min(p0 + step, n), dtype=torch.int64, device=cuda)
+        keys[p0:p0 + len(p)] = ((p * 0x9E3779B1) >> 7 & 0x7FFFFFFF).to(torch.int32)
+    del p
+    torch.cuda.empty_cache()
+    out = P().sort(keys)
+    torch.cuda.synchronize()
+    assert tk.count_unsorted(out) == 0
+    assert tk.checksum(out) == tk.checksum(keys)
+    del keys, out
+    torch.cuda.empty_cache()
