@@ -71,7 +71,7 @@ void comerge_cuda_set_path(int path);
  * + merge launches), 2 = ring-streaming kernel (one launch), 3 = tile
  * pipeline (one launch), 4 = segmented tile kernel (partition + merge),
  * 5 = segmented tile pipeline (one launch), 6 = merge pass of the sort
- * (tile pipeline over runs), 0 = none yet. */
+ * (tile pipeline over runs), 7 = pieced-input range merge, 0 = none yet. */
 int comerge_cuda_last_path(void);
 /* Host-buffer strategy of the synchronous entry points on this thread
  * (testing / benchmarking): 0 = chunked pipeline (default: output chunks
@@ -272,6 +272,31 @@ int comerge_merge_parallel_ex_u64(const uint64_t* a, const uint32_t* a_vals, siz
                                   size_t workers, const comerge_merge_options* opts,
                                   comerge_merge_report* report, uint64_t* block_sizes,
                                   uint32_t* corank_iterations, uint64_t* comparisons);
+
+/* Output ranks [out_begin, out_end) of the stable merge of A and B into
+ * out[0, out_end - out_begin), where A (B) is the concatenation of na (nb) <= 8
+ * device arrays -- e.g. every GPU's piece of a distributed input, peer
+ * pointers mapped over NVLink (CUDA IPC): the multi-GPU split of Algorithm 2,
+ * one launch per GPU for its own output range, no data-path collective.
+ * Pieces and out 16-byte aligned; every piece but the last a multiple of 16
+ * bytes.  Piece pointer / length arrays are host memory.  Workspace: the
+ * tail slots of the pipeline (comerge_cuda_merge_workspace_bytes(m, n, ...)
+ * is enough), NULL = library pool. */
+int comerge_cuda_merge_keys_pieces_i32(const int32_t* const* a_pieces, const uint64_t* a_lens,
+                                       int na, const int32_t* const* b_pieces,
+                                       const uint64_t* b_lens, int nb, uint64_t out_begin,
+                                       uint64_t out_end, int32_t* out, void* ws, size_t ws_bytes,
+                                       comerge_stream_t stream);
+int comerge_cuda_merge_keys_pieces_u32(const uint32_t* const* a_pieces, const uint64_t* a_lens,
+                                       int na, const uint32_t* const* b_pieces,
+                                       const uint64_t* b_lens, int nb, uint64_t out_begin,
+                                       uint64_t out_end, uint32_t* out, void* ws, size_t ws_bytes,
+                                       comerge_stream_t stream);
+int comerge_cuda_merge_keys_pieces_u64(const uint64_t* const* a_pieces, const uint64_t* a_lens,
+                                       int na, const uint64_t* const* b_pieces,
+                                       const uint64_t* b_lens, int nb, uint64_t out_begin,
+                                       uint64_t out_end, uint64_t* out, void* ws, size_t ws_bytes,
+                                       comerge_stream_t stream);
 
 /* comerge::plan(a, b, workers) (parallel.hpp:94-115): blocks[7*r .. 7*r+6] =
  * {worker, out_begin, out_end, a_begin, a_end, b_begin, b_end} for every

@@ -415,3 +415,30 @@ def sort_pairs_workspace_bytes(n, dtype):
         else np.dtype(dtype).name
     return int(N.lib.comerge_cuda_sort_pairs_workspace_bytes(int(n), _KIND[_SUFFIX[name]]))
 
+
+def merge_pieces(a_pieces, b_pieces, out_begin: int, out_end: int, out=None, workspace=None):
+    """Output ranks [out_begin, out_end) of stable_merge(cat(a_pieces),
+    cat(b_pieces)) in one device launch, without concatenating: the pieces may
+    live on other GPUs (peer tensors opened over CUDA IPC / NVLink).  Every
+    piece but the last must hold a multiple of 16 bytes; all 16-byte aligned."""
+    if not a_pieces or not b_pieces or len(a_pieces) > 8 or len(b_pieces) > 8:
+        raise ValueError("merge_pieces: 1 to 8 pieces per input")
+    suf = _suffix(a_pieces[0])
+    for t in list(a_pieces) + list(b_pieces):
+        if not (_is_torch(t) and t.is_cuda) or _suffix(t) != suf:
+            raise TypeError("merge_pieces: pieces must be CUDA tensors of one key dtype")
+    if out is None:
+        out = torch.empty(out_end - out_begin, dtype=a_pieces[0].dtype,
+                          device=torch.cuda.current_device())
+    if _len(out) != out_end - out_begin:
+        raise ValueError("merge_pieces: output length must equal out_end - out_begin")
+    ap = (C.c_void_p * len(a_pieces))(*[t.data_ptr() if t.numel() else 0 for t in a_pieces])
+    bp = (C.c_void_p * len(b_pieces))(*[t.data_ptr() if t.numel() else 0 for t in b_pieces])
+    al = (C.c_uint64 * len(a_pieces))(*[t.numel() for t in a_pieces])
+    bl = (C.c_uint64 * len(b_pieces))(*[t.numel() for t in b_pieces])
+    wsp, wsb = _ws(workspace)
+    N.check(getattr(N.lib, f"comerge_cuda_merge_keys_pieces_{suf}")(
+        ap, al, len(a_pieces), bp, bl, len(b_pieces), out_begin, out_end, _ptr(out), wsp, wsb,
+        _stream(out)))
+    return out
+

@@ -237,13 +237,27 @@ int check_merge_args(const char* who, const K* a, size_t m, const K* b, size_t n
 
 // Launch the persistent tile pipeline (merge_pipe.cuh) for a plain merge or a
 // segmented batch (aoff/boff/nseg).  Scratch: the dynamic-tail state.
+// Pieced inputs (SEG == 3) and output ranges for launch_pipe.
+struct pipe_pieces {
+    uint32_t na = 0, nb = 0;
+    const void* pa[kMaxPieces] = {};
+    const void* pb[kMaxPieces] = {};
+    uint64_t a_start[kMaxPieces + 1] = {};
+    uint64_t b_start[kMaxPieces + 1] = {};
+    uint64_t out_base = 0, out_end = 0;
+};
+
 template <typename K, bool HAS_V, int SEG>
 int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const uint32_t* bv,
                 uint64_t n, K* out, uint32_t* outv, const uint64_t* aoff, const uint64_t* boff,
-                uint64_t nseg, void* ws, size_t ws_bytes, cudaStream_t s, uint64_t run_len = 0) {
+                uint64_t nseg, void* ws, size_t ws_bytes, cudaStream_t s, uint64_t run_len = 0,
+                const pipe_pieces* pieces = nullptr) {
     using PL = pipe_layout<K, HAS_V, SEG>;
     const uint64_t total = m + n;
-    const uint64_t ptiles = div_up(total, PL::T);
+    const uint64_t out_base = pieces ? pieces->out_base : 0;
+    const uint64_t out_end = pieces ? pieces->out_end : total;
+    const uint64_t ptiles = div_up(out_end - out_base, PL::T);
+    if (ptiles == 0) return COMERGE_OK;
     int limit = pipe_grid_limit<K, HAS_V, SEG>();
     if (limit > kMaxPipeGrid) limit = kMaxPipeGrid;
     const uint32_t grid = uint32_t(ptiles < uint64_t(limit) ? ptiles : uint64_t(limit));
@@ -261,6 +275,20 @@ int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const ui
     args.boff = boff;
     args.nseg = nseg;
     args.run_len = run_len;
+    args.out_base = out_base;
+    args.out_end = out_end;
+    if (pieces) {
+        args.npa = pieces->na;
+        args.npb = pieces->nb;
+        for (uint32_t q = 0; q < kMaxPieces; ++q) {
+            args.pa[q] = pieces->pa[q];
+            args.pb[q] = pieces->pb[q];
+        }
+        for (uint32_t q = 0; q <= kMaxPieces; ++q) {
+            args.pa_start[q] = pieces->a_start[q];
+            args.pb_start[q] = pieces->b_start[q];
+        }
+    }
     args.trace = g_trace;
     // equal static split of 70% of the tiles + a dynamic tail of 30%: the tail
     // absorbs the start-up skew (~10 us between the first and last CTA to
@@ -303,7 +331,7 @@ int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const ui
     if (args.sched_ahead < args.sched_cap) args.sched_ahead = args.sched_cap;
     if (g_tune_flags & 256) args.store_evict_first = 1;
     if (g_tune_flags & 512) args.store_evict_first = 0;
-    g_last_path = SEG == 2 ? 6 : (SEG ? 5 : 3);
+    g_last_path = SEG == 3 ? 7 : (SEG == 2 ? 6 : (SEG ? 5 : 3));
     mark_before(s);
     merge_pipe_kernel<K, HAS_V, SEG><<<grid, PL::kThreads, PL::kSmem, s>>>(args);
     mark_after(s);
@@ -359,6 +387,51 @@ int merge_device(const K* a, const uint32_t* av, size_t m, const K* b, const uin
         a, av, m, b, bv, n, out, outv, bj, flags);
     mark_after(s);
     return check_launch("comerge: merge launch");
+}
+
+// Output ranks [out_begin, out_end) of the stable merge of A and B, each
+// given as up to kMaxPieces device arrays (a multi-GPU split: rank r passes
+// every GPU's piece -- peer pointers over NVLink -- and its own output range;
+// Algorithm 2 with one worker per GPU).
+template <typename K>
+int merge_pieces_device(const K* const* ap, const uint64_t* alen, int na, const K* const* bp,
+                        const uint64_t* blen, int nb, uint64_t out_begin, uint64_t out_end,
+                        K* out, void* ws, size_t ws_bytes, cudaStream_t s) {
+    if (na < 1 || nb < 1 || na > kMaxPieces || nb > kMaxPieces || !ap || !bp || !alen || !blen)
+        return fail(COMERGE_E_INVALID, "merge_pieces: 1 to 8 pieces per input");
+    constexpr uint64_t vece = 16 / sizeof(K);
+    pipe_pieces pc;
+    pc.na = uint32_t(na);
+    pc.nb = uint32_t(nb);
+    uint64_t m = 0, n = 0;
+    for (int q = 0; q < na; ++q) {
+        if (alen[q] && (!ap[q] || !aligned16(ap[q])))
+            return fail(COMERGE_E_INVALID, "merge_pieces: pieces must be 16-byte aligned device arrays");
+        if (q + 1 < na && alen[q] % vece)
+            return fail(COMERGE_E_INVALID, "merge_pieces: every piece but the last must be a multiple of 16 bytes");
+        pc.pa[q] = ap[q];
+        pc.a_start[q] = m;
+        m += alen[q];
+    }
+    for (int q = 0; q < nb; ++q) {
+        if (blen[q] && (!bp[q] || !aligned16(bp[q])))
+            return fail(COMERGE_E_INVALID, "merge_pieces: pieces must be 16-byte aligned device arrays");
+        if (q + 1 < nb && blen[q] % vece)
+            return fail(COMERGE_E_INVALID, "merge_pieces: every piece but the last must be a multiple of 16 bytes");
+        pc.pb[q] = bp[q];
+        pc.b_start[q] = n;
+        n += blen[q];
+    }
+    for (int q = na; q <= kMaxPieces; ++q) pc.a_start[q] = m;
+    for (int q = nb; q <= kMaxPieces; ++q) pc.b_start[q] = n;
+    if (out_begin > out_end || out_end > m + n)
+        return fail(COMERGE_E_RANGE, "merge_pieces: output range exceeds m+n");
+    if (out_end > out_begin && (!out || !aligned16(out)))
+        return fail(COMERGE_E_INVALID, "merge_pieces: output must be a 16-byte aligned device array");
+    pc.out_base = out_begin;
+    pc.out_end = out_end;
+    return launch_pipe<K, false, 3>(nullptr, nullptr, m, nullptr, nullptr, n, out, nullptr,
+                                    nullptr, nullptr, 0, ws, ws_bytes, s, 0, &pc);
 }
 
 template <typename K>
@@ -1209,6 +1282,14 @@ size_t comerge_cuda_segmented_workspace_bytes(size_t total, size_t, int key_kind
                                            comerge_merge_report* report) {                       \
         return merge_parallel_sync<K, true>(ak, av, m, bk, bv, n, ok, ov, out_len, workers, 0,   \
                                             report, nullptr, nullptr);                           \
+    }                                                                                            \
+    int comerge_cuda_merge_keys_pieces_##SUF(const K* const* a_pieces, const uint64_t* a_lens,  \
+                                             int na, const K* const* b_pieces,                   \
+                                             const uint64_t* b_lens, int nb, uint64_t out_begin, \
+                                             uint64_t out_end, K* out, void* ws,                 \
+                                             size_t ws_bytes, comerge_stream_t stream) {         \
+        return merge_pieces_device<K>(a_pieces, a_lens, na, b_pieces, b_lens, nb, out_begin,    \
+                                      out_end, out, ws, ws_bytes, stream);                       \
     }                                                                                            \
     int comerge_plan_##SUF(const K* a, size_t m, const K* b, size_t n, size_t workers,          \
                            uint64_t* blocks) {                                                   \

@@ -82,7 +82,8 @@ struct pipe_cfg<uint64_t, true> {
 };
 
 // SEG: 0 plain merge, 1 segmented batch (explicit offsets), 2 merge pass
-// (runs of run_len, implicit offsets; sort.cuh)
+// (runs of run_len, implicit offsets; sort.cuh), 3 plain merge of inputs
+// held as pieces in several device arrays (a multi-GPU split, peer memory)
 template <typename K, bool HAS_V, int SEG = 0>
 struct pipe_layout {
     using C = pipe_cfg<K, HAS_V>;
@@ -102,7 +103,8 @@ struct pipe_layout {
     // segmented batches: the tile's segment-end table (window-relative
     // x1 | y1 << 16 of segments s0 .. s0+SEGCAP-1), written by the producer warp
     static constexpr int SEGCAP = 128;
-    static constexpr size_t kStageOffs = SEG ? size_t(SEGCAP) * 4 : 0;
+    static constexpr bool kSeg = SEG == 1 || SEG == 2;  // segmented modes
+    static constexpr size_t kStageOffs = kSeg ? size_t(SEGCAP) * 4 : 0;
     static constexpr size_t kStage = kStageKeys + kStageVals + kStageOffs;
     static constexpr size_t oStages = 0;
     static constexpr size_t oBars = oStages + NST * kStage;
@@ -111,11 +113,12 @@ struct pipe_layout {
     static constexpr size_t oScratch = oDesc + size_t(NB) * 64;    // 40 x u64
     static constexpr size_t oMisc = oScratch + 40 * 8;
     static constexpr size_t kMisc = 64;
-    static_assert(!SEG || KW < 65536, "segment ends are packed as 16-bit window offsets");
+    static_assert(!kSeg || KW < 65536, "segment ends are packed as 16-bit window offsets");
     static constexpr size_t kSmem = oMisc + kMisc;
 };
 
 constexpr int kMaxPipeGrid = 512;
+constexpr int kMaxPieces = 8;  // SEG == 3: pieces per input (one per GPU of a node)
 
 struct pipe_args {
     const void* a;
@@ -146,6 +149,17 @@ struct pipe_args {
     // boff(s) = min(s*L, n), A index x at element x + (x/L)*L, B index y at
     // y + (y/L + 1)*L; aoff / boff are NULL.  0 = explicit offsets.
     uint64_t run_len;
+    // output range: this launch merges output ranks [out_base, out_end) of the
+    // whole merge into out[0, out_end - out_base) (whole merges: 0, m + n)
+    uint64_t out_base, out_end;
+    // SEG == 3: input A (B) is npa (npb) pieces, piece q = global indices
+    // [pa_start[q], pa_start[q+1]) at pa[q] (any device pointer, e.g. a peer
+    // GPU's buffer mapped over NVLink); starts are multiples of 16 bytes
+    uint32_t npa, npb;
+    const void* pa[kMaxPieces];
+    const void* pb[kMaxPieces];
+    uint64_t pa_start[kMaxPieces + 1];
+    uint64_t pb_start[kMaxPieces + 1];
 };
 
 // Lane-group (P+1)-ary search for the largest q in [lo, hi] with !pred(q),
@@ -263,6 +277,47 @@ __device__ __forceinline__ uint64_t run_off(uint64_t s, uint64_t L, uint64_t len
 __device__ __forceinline__ uint64_t run_pos_a(uint64_t x, uint64_t L) { return x + (x / L) * L; }
 __device__ __forceinline__ uint64_t run_pos_b(uint64_t y, uint64_t L) { return y + (y / L + 1) * L; }
 
+// SEG == 3: element x of a pieced input (linear scan: at most kMaxPieces)
+template <typename K>
+__device__ __forceinline__ K piece_probe(const void* const* p, const uint64_t* st, uint32_t np,
+                                         uint64_t x) {
+    uint32_t q = 0;
+    while (q + 1 < np && st[q + 1] <= x) ++q;
+    return probe_elem(static_cast<const K*>(p[q]) + (x - st[q]));
+}
+
+// SEG == 3: stage the window [x0, x1) of a pieced input (dst <-> index
+// x0 - x0 % vece) as one TMA copy per piece it touches; issue == false: plan
+// only (scalar tails copied, bytes returned) -- as stage_runs.
+template <typename E>
+__device__ __forceinline__ uint32_t stage_pieces(const void* const* p, const uint64_t* st,
+                                                 uint32_t np, uint64_t x0, uint64_t x1, E* dst,
+                                                 int vece, bool issue, uint64_t* bar,
+                                                 uint64_t policy) {
+    uint32_t total = 0;
+    const uint64_t base = x0 - x0 % vece;
+    for (uint32_t q = 0; q < np; ++q) {
+        const uint64_t lo = x0 > st[q] ? x0 : st[q];
+        const uint64_t hi = x1 < st[q + 1] ? x1 : st[q + 1];
+        if (lo >= hi) continue;
+        const E* src = static_cast<const E*>(p[q]);
+        const uint64_t plen = st[q + 1] - st[q];
+        E* d = dst + ((lo - lo % vece) - base);
+        if (!issue) {
+            total += stage_copy_plan(src, plen, lo - st[q], hi - st[q], d, vece);
+        } else {
+            const uint64_t l = lo - st[q], l_al = l - l % vece;
+            uint64_t h_al = (hi - st[q] + vece - 1) / vece * vece;
+            const uint64_t len_al = plen - plen % vece;
+            if (h_al > plen) h_al = len_al > l_al ? len_al : l_al;
+            const uint32_t bytes = uint32_t((h_al - l_al) * sizeof(E));
+            if (bytes) tma_load_1d(d, src + l_al, bytes, bar, policy);
+            total += bytes;
+        }
+    }
+    return total;
+}
+
 // A tile boundary: co-rank j of output rank i and, for segmented batches, the
 // segment s that holds it (largest s with aoff[s] + boff[s] <= i).
 struct boundary {
@@ -281,8 +336,18 @@ __device__ __forceinline__ boundary find_boundary(const pipe_args& args, uint64_
                                                   uint32_t* rounds) {
     const K* __restrict__ a = static_cast<const K*>(args.a);
     const K* __restrict__ b = static_cast<const K*>(args.b);
-    if constexpr (!SEG) {
+    if constexpr (SEG == 0) {
         return {group_search<K>(i, jlo, jhi, P, a, b, rounds), 0};
+    } else if constexpr (SEG == 3) {
+        uint64_t lo = jlo, hi = jhi;
+        const uint64_t j = group_search_pred(
+            lo, hi, P,
+            [&](uint64_t q) {
+                return piece_probe<K>(args.pb, args.pb_start, args.npb, i - q) <
+                       piece_probe<K>(args.pa, args.pa_start, args.npa, q - 1);
+            },
+            rounds);
+        return {j, 0};
     } else {
         if constexpr (SEG == 2) {  // merge pass: pair s holds output ranks [2sL, 2sL + 2L)
             const uint64_t L = args.run_len;
@@ -533,6 +598,8 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
     constexpr int VECE = L::VECE;
     constexpr int NB = L::NB;
     static_assert(!(SEG == 1 && HAS_V), "explicit-offset segmented batches are keys-only");
+    constexpr bool SEGM = L::kSeg;
+    static_assert(!(SEG == 3 && HAS_V), "pieced inputs are keys-only");
 
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::oBars);
@@ -553,9 +620,10 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
     const uint32_t G = gridDim.x, c = blockIdx.x;
     const uint64_t NS = args.static_tiles;
 
+    const uint64_t out_base = args.out_base, out_end = args.out_end;
     auto diag_of = [=](uint64_t t) {  // output rank of tile boundary t
-        const uint64_t d = t * uint64_t(T);
-        return d < total ? d : total;
+        const uint64_t d = out_base + t * uint64_t(T);
+        return d < out_end ? d : out_end;
     };
     auto full_bracket = [=](uint64_t i, uint64_t& lo, uint64_t& hi) {
         lo = i > n ? i - n : 0;
@@ -580,7 +648,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
     }
     if (tid == 0) {
         for (int s = 0; s < NST; ++s) {
-            mbar_init(&full[s], SEG ? 2 : 1);  // SEG: + the producer warp's segment table
+            mbar_init(&full[s], SEGM ? 2 : 1);  // segmented: + the producer warp's table
             mbar_init(&empty[s], 1);
             mbar_init(&staged[s], 1);
         }
@@ -604,7 +672,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
     // large plain merges: the scheduler narrows the start's bracket to one tile,
     // hands it to the consumer warps (named barrier 2), and both finish their
     // searches concurrently (boundary w is in [lo, hi + (i_w - i_0)])
-    const bool split_start = !SEG && !args.eager_start && known > 0 && !(args.flags & 1u);
+    const bool split_start = SEG == 0 && !args.eager_start && known > 0 && !(args.flags & 1u);
     constexpr int kSplitBar = 32 * (L::kCW + 1);
     if (warp == W_SCHED) {
         if (te0 > ts0) {
@@ -612,7 +680,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             uint64_t lo, hi;
             full_bracket(i, lo, hi);
             boundary bd{0, 0};
-            if constexpr (!SEG) {
+            if constexpr (SEG == 0) {
                 if (split_start) {
                     group_narrow<K>(i, lo, hi, 32, a, b, uint64_t(T));
                     if (lane == 0) {
@@ -673,7 +741,8 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         // ------------------------------------------------------ tail warp
         // co-rank the tail boundaries q = c, c+G, ... (in passes of up to 32,
         // lane groups, full-diagonal brackets) and publish them
-        const uint64_t nq = NT - NS;  // slots 0 .. nq-1 (boundary NT is trivial)
+        // slots 0 .. nq-1; boundary NT is trivial for a whole merge, else co-ranked too
+        const uint64_t nq = NT > NS ? NT - NS + (out_end < total ? 1 : 0) : 0;
         for (uint64_t q0 = c; q0 < nq; q0 += 32 * uint64_t(G)) {
             uint64_t left = (nq - q0 + G - 1) / G;
             const int k = int(left < 32 ? left : 32);
@@ -786,8 +855,8 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
                 for (int e = 0; e < 2; ++e) {
                     const uint64_t qq = q + e;
                     const uint64_t i = diag_of(NS + qq);
-                    boundary bd{m, SEG ? args.nseg - 1 : 0};  // the last boundary is (m, n)
-                    bool ok = NS + qq == NT;
+                    boundary bd{m, SEGM ? args.nseg - 1 : 0};  // the last boundary is (m, n)
+                    bool ok = NS + qq == NT && out_end == total;
                     if (!ok) {
                         const uint64_t* slot = args.tail + 4 + 4 * qq;
                         uint64_t tag, pad;
@@ -837,7 +906,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             mbar_wait_sleepy(&staged[st], uint32_t((s / NST) & 1), 2000);
             const uint64_t* mt = meta + 8 * st;
             if (mt[3] >> 63) break;  // end of work
-            const uint64_t i0 = mt[0];
+            const uint64_t i0 = mt[0] - out_base;  // position in out
             const uint64_t lens = mt[2];
             const int len = int(lens >> 32) + int(lens & 0xffffffffu);
             unsigned char* stage = smem + L::oStages + size_t(st) * L::kStage;
@@ -870,7 +939,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         // ------------------------------------------------------ producer
         // lane 0 stages the windows; for segmented batches the whole warp also
         // writes the tile's segment-end table (the full barrier's 2nd arrival)
-        if (!SEG && lane != 0) return;
+        if (!SEGM && lane != 0) return;
         const uint64_t policy = policy_evict_first();
         unsigned long long starve = 0;  // ns spent waiting for descriptors
         for (uint32_t s = 0;; ++s) {
@@ -889,19 +958,19 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
                 if (lane == 0) {
                     mt[3] = uint64_t(1) << 63;  // done
                     mbar_arrive(&full[st]);
-                    if (SEG) mbar_arrive(&full[st]);
+                    if (SEGM) mbar_arrive(&full[st]);
                     if (args.trace) args.trace[8 * c + 6] = starve;
                 }
                 break;
             }
             // copy the whole descriptor out before its ring slot is released
             const uint64_t j0 = d[1], j1 = d[2], i1 = d[3], seg0 = d[4], seg1 = d[5];
-            if constexpr (SEG) __syncwarp();
+            if constexpr (SEGM) __syncwarp();
             if (lane == 0) {
                 __threadfence_block();
                 *issued = s + 1;
             }
-            if constexpr (SEG) {  // segment-end table (merge_thread_segends)
+            if constexpr (SEGM) {  // segment-end table (merge_thread_segends)
                 const uint64_t nse = seg1 - seg0 + 1;
                 uint32_t* se = reinterpret_cast<uint32_t*>(smem + L::oStages + size_t(st) * L::kStage +
                                                            L::kStageKeys + L::kStageVals);
@@ -928,7 +997,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
 #ifdef COMERGE_DEBUG_CHECKS
             if (!(j0 <= j1 && i0 <= i1 && i1 - i0 <= uint64_t(T) && i0 >= j0 && i1 >= j1 &&
                   i1 - j1 >= i0 - j0 && j1 <= m && i1 - j1 <= n && seg0 <= seg1 &&
-                  (!SEG || seg1 < args.nseg))) {
+                  (!SEGM || seg1 < args.nseg))) {
                 printf("comerge: bad tile descriptor cta %u s %u: i0 %llu i1 %llu j0 %llu j1 %llu "
                        "s0 %llu s1 %llu\n", c, s, (unsigned long long)i0, (unsigned long long)i1,
                        (unsigned long long)j0, (unsigned long long)j1,
@@ -947,11 +1016,18 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             const uint32_t b_base = (a_off + a_len + VECE - 1) / VECE * VECE;
             const uint32_t b_off = uint32_t(k0 % VECE);
             const uint64_t RL = SEG == 2 ? args.run_len : 0;  // merge pass (see pipe_args)
-            const uint32_t ab = RL ? stage_runs(a, m + n, j0, j1, RL, 0, sk, VECE, false, nullptr, 0)
-                                   : stage_copy_plan(a, m, j0, j1, sk, VECE);
-            const uint32_t bb = RL ? stage_runs(b, m + n, k0, k1, RL, 1, sk + b_base, VECE, false,
-                                                nullptr, 0)
-                                   : stage_copy_plan(b, n, k0, k1, sk + b_base, VECE);
+            uint32_t ab, bb;
+            if constexpr (SEG == 3) {
+                ab = stage_pieces(args.pa, args.pa_start, args.npa, j0, j1, sk, VECE, false,
+                                  nullptr, 0);
+                bb = stage_pieces(args.pb, args.pb_start, args.npb, k0, k1, sk + b_base, VECE,
+                                  false, nullptr, 0);
+            } else {
+                ab = RL ? stage_runs(a, m + n, j0, j1, RL, 0, sk, VECE, false, nullptr, 0)
+                        : stage_copy_plan(a, m, j0, j1, sk, VECE);
+                bb = RL ? stage_runs(b, m + n, k0, k1, RL, 1, sk + b_base, VECE, false, nullptr, 0)
+                        : stage_copy_plan(b, n, k0, k1, sk + b_base, VECE);
+            }
             uint32_t avb = 0, bvb = 0, av_off = 0, bv_base = 0;
             if constexpr (HAS_V) {
                 av_off = uint32_t(j0 % 4);
@@ -967,9 +1043,14 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             mt[2] = (uint64_t(a_len) << 32) | b_len;
             mt[3] = (uint64_t(a_off) << 48) | (uint64_t(b_base) << 24) | (uint64_t(b_off) << 8) |
                     uint64_t(av_off);
-            if constexpr (SEG) mt[6] = seg1 - seg0 + 1 <= uint64_t(L::SEGCAP) ? 1 : 0;  // table?
+            if constexpr (SEGM) mt[6] = seg1 - seg0 + 1 <= uint64_t(L::SEGCAP) ? 1 : 0;  // table?
             mbar_arrive_expect_tx(&full[st], ab + bb + avb + bvb);
-            if (RL) {
+            if constexpr (SEG == 3) {
+                stage_pieces(args.pa, args.pa_start, args.npa, j0, j1, sk, VECE, true, &full[st],
+                             policy);
+                stage_pieces(args.pb, args.pb_start, args.npb, k0, k1, sk + b_base, VECE, true,
+                             &full[st], policy);
+            } else if (RL) {
                 stage_runs(a, m + n, j0, j1, RL, 0, sk, VECE, true, &full[st], policy);
                 stage_runs(b, m + n, k0, k1, RL, 1, sk + b_base, VECE, true, &full[st], policy);
             } else {
@@ -1024,7 +1105,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         K keys[VT];
         uint32_t src[VT];
         const unsigned long long p0 = args.trace && tid == 0 ? globaltimer_ns() : 0;
-        if constexpr (SEG) {
+        if constexpr (SEGM) {
             const uint64_t k0 = mt[1];
             const uint64_t s_lo = mt[4], s_hi = mt[5];
             if (SEG == 2 && s_lo == s_hi) {  // merge pass, one segment: a plain merge

@@ -634,3 +634,74 @@ def test_max_size_sort_crosses_2_32(cuda):
     assert tk.checksum(out) == tk.checksum(keys)
     del keys, out
     torch.cuda.empty_cache()
+
+
+# ------------------------------------- pieced inputs / multi-GPU split (8f-4)
+
+@pytest.mark.parametrize("dt", [np.int32, np.uint64])
+def test_merge_pieces_ranges_against_oracle(cuda, port, dt):
+    """A and B cut into pieces (no concatenation), any output range."""
+    rng = np.random.default_rng(12)
+    a, b = _draw(rng, dt, 400_004, 60), _draw(rng, dt, 333_332, 60)
+    expect = port.merge(a, b)
+    total = len(a) + len(b)
+    vece = 16 // np.dtype(dt).itemsize
+    for cuts_a, cuts_b in (([], []), ([100_000], [4 * vece]), ([0, 200_000, 200_000 + vece], [333_328]),
+                           ([40_000 * k for k in range(1, 8)], [47_616 * k for k in range(1, 7)])):
+        pa = [dev(x, cuda) for x in np.split(a, cuts_a)]
+        pb = [dev(x, cuda) for x in np.split(b, cuts_b)]
+        for lo, hi in ((0, total), (0, 0), (12345, 500_000), (total - 7, total), (1, total - 1)):
+            out = P().merge_pieces(pa, pb, lo, hi)
+            torch.cuda.synchronize()
+            assert np.array_equal(host(out), expect[lo:hi]), (len(pa), len(pb), lo, hi)
+    # a piece that is not a 16-byte multiple (and not last) is rejected
+    with pytest.raises(ValueError):
+        P().merge_pieces([dev(a[:3], cuda), dev(a[3:], cuda)], [dev(b, cuda)], 0, total)
+
+
+def _ipc_worker(rank, world, port, q):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)  # one GPU here: the ranks share it (IPC works the same)
+        from paper_1303_4312_b200.shard import merge_distributed
+        rng = np.random.default_rng(99)  # every rank draws the same full inputs...
+        a = np.sort(rng.integers(0, 1000, 600_000)).astype(np.int32)
+        b = np.sort(rng.integers(0, 1000, 500_008)).astype(np.int32)
+        ca = [0, 250_000, 600_000] if world == 2 else None
+        cb = [0, 300_000, 500_008] if world == 2 else None
+        # ...and keeps only its own piece on the device
+        la = torch.from_numpy(a[ca[rank]:ca[rank + 1]]).cuda()
+        lb = torch.from_numpy(b[cb[rank]:cb[rank + 1]]).cuda()
+        lo, out = merge_distributed(la, lb)
+        parts = [None] * world
+        dist.all_gather_object(parts, (lo, out.cpu().numpy().tobytes()))
+        if rank == 0:
+            from oracle.py import Port
+            got = np.concatenate([np.frombuffer(p[1], np.int32) for p in sorted(parts)])
+            q.put(bool(np.array_equal(got, Port().merge(a, b))))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_merge_distributed_ipc_world2(cuda):
+    """Two processes, each holding one piece of A and of B; each merges its
+    output range reading the other's piece through a CUDA IPC mapping."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs)
+    assert q.get(timeout=5) is True
