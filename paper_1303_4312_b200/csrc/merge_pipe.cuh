@@ -443,19 +443,13 @@ struct pipe_min_blocks<int32_t, true> {
 // Segmented consumer merge: VT outputs from window diagonal `diag` of a tile
 // whose windows hold A[j0, j0+a_len) and B[k0, k0+b_len) of a batch of
 // independent pairs; s_lo..s_hi bound the segments the tile touches.
-// Segment offsets of a tile: staged in shared memory when the tile touches
-// few segments (so = first staged index), else read from global memory.
+// Segment offsets in global memory (the fallback for tiles touching more
+// than SEGCAP segments, where no segment-end table is built).
 struct seg_offsets {
-    const uint64_t* ao;  // aoff (global) or its staged copy (shared)
+    const uint64_t* ao;
     const uint64_t* bo;
-    uint64_t base;       // index of ao[0] / bo[0]
-    bool shared;
-    __device__ __forceinline__ uint64_t a(uint64_t s) const {
-        return shared ? ao[s - base] : ldg_u64(ao + s);
-    }
-    __device__ __forceinline__ uint64_t b(uint64_t s) const {
-        return shared ? bo[s - base] : ldg_u64(bo + s);
-    }
+    __device__ __forceinline__ uint64_t a(uint64_t s) const { return ldg_u64(ao + s); }
+    __device__ __forceinline__ uint64_t b(uint64_t s) const { return ldg_u64(bo + s); }
 };
 
 // Segmented consumer merge: VT outputs from window diagonal `diag` of a tile
@@ -1073,8 +1067,6 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
     }
 
     // ---------------------------------------------------------- consumers
-    K* __restrict__ out = static_cast<K*>(args.out);
-    uint32_t* __restrict__ outv = args.outv;
     unsigned long long data_wait = 0;  // ns consumers waited for stage data
     unsigned long long ph[4] = {0, 0, 0, 0};  // trace: merge, barrier 1, staging+barrier 2, store
     for (uint32_t s = 0;; ++s) {
@@ -1117,7 +1109,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
                 merge_thread_segends<K, VT, HAS_V>(sk + a_off, sk + b_base + b_off, diag, se,
                                                    int(s_hi - s_lo) + 1, keys, src);
             } else if constexpr (!HAS_V) {
-                const seg_offsets off{args.aoff, args.boff, 0, false};
+                const seg_offsets off{args.aoff, args.boff};
                 merge_thread_seg<K, VT>(sk + a_off, a_len, sk + b_base + b_off, b_len, diag, i0,
                                         i0 - k0, k0, s_lo, s_hi, off, keys);
             } else {
