@@ -57,6 +57,10 @@ EXTRA = {
                desc="diagnostic: int32 keys only, m=n=2^26, uniform [0,2^31)"),
     "X2": dict(kind="pairs", dtype="int32", m=2**26, n=2**26, width=2**31,
                desc="diagnostic: int32 keys + payload, m=n=2^26, uniform [0,2^31)"),
+    "X3": dict(kind="segmented", dtype="int32", nseg=2**20, maxlen=64, width=2**20,
+               desc="diagnostic: segmented batch of 2^20 small pairs, m_s,n_s in [1,64]"),
+    "X4": dict(kind="segmented", dtype="int32", nseg=2**21, maxlen=16, width=2**20,
+               desc="diagnostic: segmented batch of 2^21 tiny pairs, m_s,n_s in [1,16]"),
 }
 HEADLINE = "C2"
 SEED = 5

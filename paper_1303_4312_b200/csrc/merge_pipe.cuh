@@ -102,7 +102,7 @@ struct pipe_layout {
     static constexpr size_t kStageVals = (size_t(VW) * 4 + 127) / 128 * 128;
     // segmented batches: the tile's segment-end table (window-relative
     // x1 | y1 << 16 of segments s0 .. s0+SEGCAP-1), written by the producer warp
-    static constexpr int SEGCAP = 128;
+    static constexpr int SEGCAP = 512;
     static constexpr bool kSeg = SEG == 1 || SEG == 2;  // segmented modes
     static constexpr size_t kStageOffs = kSeg ? size_t(SEGCAP) * 4 : 0;
     static constexpr size_t kStage = kStageKeys + kStageVals + kStageOffs;

@@ -21,6 +21,7 @@ def main():
     import torch
     import bench
     import paper_1303_4312_b200._native as N
+    bench.CONFIGS.update(bench.EXTRA)
     dev = torch.device("cuda:0")
     flags = [int(x) for x in args.flags.split(",")]
     res = {f: [] for f in flags}
