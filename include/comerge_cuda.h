@@ -298,6 +298,33 @@ int comerge_cuda_merge_keys_pieces_u64(const uint64_t* const* a_pieces, const ui
                                        uint64_t out_end, uint64_t* out, void* ws, size_t ws_bytes,
                                        comerge_stream_t stream);
 
+/* Key-value form: payload pieces cut like their key pieces; every piece but
+ * the last a multiple of 4 elements and of 16 bytes of keys. */
+int comerge_cuda_merge_pairs_pieces_i32(const int32_t* const* a_pieces,
+                                        const uint32_t* const* a_val_pieces,
+                                        const uint64_t* a_lens, int na,
+                                        const int32_t* const* b_pieces,
+                                        const uint32_t* const* b_val_pieces,
+                                        const uint64_t* b_lens, int nb, uint64_t out_begin,
+                                        uint64_t out_end, int32_t* out_keys, uint32_t* out_vals,
+                                        void* ws, size_t ws_bytes, comerge_stream_t stream);
+int comerge_cuda_merge_pairs_pieces_u32(const uint32_t* const* a_pieces,
+                                        const uint32_t* const* a_val_pieces,
+                                        const uint64_t* a_lens, int na,
+                                        const uint32_t* const* b_pieces,
+                                        const uint32_t* const* b_val_pieces,
+                                        const uint64_t* b_lens, int nb, uint64_t out_begin,
+                                        uint64_t out_end, uint32_t* out_keys, uint32_t* out_vals,
+                                        void* ws, size_t ws_bytes, comerge_stream_t stream);
+int comerge_cuda_merge_pairs_pieces_u64(const uint64_t* const* a_pieces,
+                                        const uint32_t* const* a_val_pieces,
+                                        const uint64_t* a_lens, int na,
+                                        const uint64_t* const* b_pieces,
+                                        const uint32_t* const* b_val_pieces,
+                                        const uint64_t* b_lens, int nb, uint64_t out_begin,
+                                        uint64_t out_end, uint64_t* out_keys, uint32_t* out_vals,
+                                        void* ws, size_t ws_bytes, comerge_stream_t stream);
+
 /* comerge::plan(a, b, workers) (parallel.hpp:94-115): blocks[7*r .. 7*r+6] =
  * {worker, out_begin, out_end, a_begin, a_end, b_begin, b_end} for every
  * worker r (block_assignment, parallel.hpp:70-84).  Host or device inputs,

@@ -65,6 +65,8 @@ def _load():
         getattr(lib, f"comerge_plan_{suf}").argtypes = [_p, _sz, _p, _sz, _sz, _p]
         getattr(lib, f"comerge_cuda_merge_keys_pieces_{suf}").argtypes = [
             _p, _p, _i, _p, _p, _i, _u64, _u64, _p, _p, _sz, _p]
+        getattr(lib, f"comerge_cuda_merge_pairs_pieces_{suf}").argtypes = [
+            _p, _p, _p, _i, _p, _p, _p, _i, _u64, _u64, _p, _p, _p, _sz, _p]
         getattr(lib, f"comerge_co_rank_{suf}").argtypes = [
             _u64, _p, _sz, _p, _sz, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(C.c_uint32),
             C.POINTER(C.c_uint32)]

@@ -416,29 +416,48 @@ def sort_pairs_workspace_bytes(n, dtype):
     return int(N.lib.comerge_cuda_sort_pairs_workspace_bytes(int(n), _KIND[_SUFFIX[name]]))
 
 
-def merge_pieces(a_pieces, b_pieces, out_begin: int, out_end: int, out=None, workspace=None):
+def merge_pieces(a_pieces, b_pieces, out_begin: int, out_end: int, out=None, workspace=None,
+                 a_val_pieces=None, b_val_pieces=None, out_vals=None):
     """Output ranks [out_begin, out_end) of stable_merge(cat(a_pieces),
     cat(b_pieces)) in one device launch, without concatenating: the pieces may
     live on other GPUs (peer tensors opened over CUDA IPC / NVLink).  Every
-    piece but the last must hold a multiple of 16 bytes; all 16-byte aligned."""
+    piece but the last must hold a multiple of 16 bytes (and, with uint32
+    payload pieces cut like their keys, a multiple of 4 elements); all 16-byte
+    aligned.  Returns out (keys) or (out, out_vals)."""
     if not a_pieces or not b_pieces or len(a_pieces) > 8 or len(b_pieces) > 8:
         raise ValueError("merge_pieces: 1 to 8 pieces per input")
+    pairs = a_val_pieces is not None or b_val_pieces is not None
+    if pairs and (a_val_pieces is None or b_val_pieces is None or
+                  len(a_val_pieces) != len(a_pieces) or len(b_val_pieces) != len(b_pieces)):
+        raise ValueError("merge_pieces: one payload piece per key piece")
     suf = _suffix(a_pieces[0])
     for t in list(a_pieces) + list(b_pieces):
         if not (_is_torch(t) and t.is_cuda) or _suffix(t) != suf:
             raise TypeError("merge_pieces: pieces must be CUDA tensors of one key dtype")
+    dev_ = torch.cuda.current_device()
     if out is None:
-        out = torch.empty(out_end - out_begin, dtype=a_pieces[0].dtype,
-                          device=torch.cuda.current_device())
+        out = torch.empty(out_end - out_begin, dtype=a_pieces[0].dtype, device=dev_)
     if _len(out) != out_end - out_begin:
         raise ValueError("merge_pieces: output length must equal out_end - out_begin")
-    ap = (C.c_void_p * len(a_pieces))(*[t.data_ptr() if t.numel() else 0 for t in a_pieces])
-    bp = (C.c_void_p * len(b_pieces))(*[t.data_ptr() if t.numel() else 0 for t in b_pieces])
+
+    def ptrs(ts):
+        return (C.c_void_p * len(ts))(*[t.data_ptr() if t.numel() else 0 for t in ts])
+
     al = (C.c_uint64 * len(a_pieces))(*[t.numel() for t in a_pieces])
     bl = (C.c_uint64 * len(b_pieces))(*[t.numel() for t in b_pieces])
     wsp, wsb = _ws(workspace)
-    N.check(getattr(N.lib, f"comerge_cuda_merge_keys_pieces_{suf}")(
-        ap, al, len(a_pieces), bp, bl, len(b_pieces), out_begin, out_end, _ptr(out), wsp, wsb,
-        _stream(out)))
-    return out
-
+    if not pairs:
+        N.check(getattr(N.lib, f"comerge_cuda_merge_keys_pieces_{suf}")(
+            ptrs(a_pieces), al, len(a_pieces), ptrs(b_pieces), bl, len(b_pieces), out_begin,
+            out_end, _ptr(out), wsp, wsb, _stream(out)))
+        return out
+    for v, k in zip(list(a_val_pieces) + list(b_val_pieces), list(a_pieces) + list(b_pieces)):
+        if _len(v) != _len(k):
+            raise ValueError("merge_pieces: payload length must equal key length")
+    if out_vals is None:
+        out_vals = torch.empty(out_end - out_begin, dtype=torch.uint32, device=dev_)
+    N.check(getattr(N.lib, f"comerge_cuda_merge_pairs_pieces_{suf}")(
+        ptrs(a_pieces), ptrs(a_val_pieces), al, len(a_pieces), ptrs(b_pieces),
+        ptrs(b_val_pieces), bl, len(b_pieces), out_begin, out_end, _ptr(out), _ptr(out_vals),
+        wsp, wsb, _stream(out)))
+    return out, out_vals

@@ -242,6 +242,8 @@ struct pipe_pieces {
     uint32_t na = 0, nb = 0;
     const void* pa[kMaxPieces] = {};
     const void* pb[kMaxPieces] = {};
+    const uint32_t* pav[kMaxPieces] = {};
+    const uint32_t* pbv[kMaxPieces] = {};
     uint64_t a_start[kMaxPieces + 1] = {};
     uint64_t b_start[kMaxPieces + 1] = {};
     uint64_t out_base = 0, out_end = 0;
@@ -283,6 +285,8 @@ int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const ui
         for (uint32_t q = 0; q < kMaxPieces; ++q) {
             args.pa[q] = pieces->pa[q];
             args.pb[q] = pieces->pb[q];
+            args.pav[q] = pieces->pav[q];
+            args.pbv[q] = pieces->pbv[q];
         }
         for (uint32_t q = 0; q <= kMaxPieces; ++q) {
             args.pa_start[q] = pieces->a_start[q];
@@ -393,45 +397,49 @@ int merge_device(const K* a, const uint32_t* av, size_t m, const K* b, const uin
 // given as up to kMaxPieces device arrays (a multi-GPU split: rank r passes
 // every GPU's piece -- peer pointers over NVLink -- and its own output range;
 // Algorithm 2 with one worker per GPU).
-template <typename K>
-int merge_pieces_device(const K* const* ap, const uint64_t* alen, int na, const K* const* bp,
+template <typename K, bool HAS_V>
+int merge_pieces_device(const K* const* ap, const uint32_t* const* apv, const uint64_t* alen,
+                        int na, const K* const* bp, const uint32_t* const* bpv,
                         const uint64_t* blen, int nb, uint64_t out_begin, uint64_t out_end,
-                        K* out, void* ws, size_t ws_bytes, cudaStream_t s) {
-    if (na < 1 || nb < 1 || na > kMaxPieces || nb > kMaxPieces || !ap || !bp || !alen || !blen)
+                        K* out, uint32_t* outv, void* ws, size_t ws_bytes, cudaStream_t s) {
+    if (na < 1 || nb < 1 || na > kMaxPieces || nb > kMaxPieces || !ap || !bp || !alen || !blen ||
+        (HAS_V && (!apv || !bpv)))
         return fail(COMERGE_E_INVALID, "merge_pieces: 1 to 8 pieces per input");
-    constexpr uint64_t vece = 16 / sizeof(K);
+    // piece cuts keep every TMA copy 16-byte aligned (keys and payloads)
+    constexpr uint64_t vece = HAS_V ? (16 / sizeof(K) > 4 ? 16 / sizeof(K) : 4) : 16 / sizeof(K);
     pipe_pieces pc;
     pc.na = uint32_t(na);
     pc.nb = uint32_t(nb);
-    uint64_t m = 0, n = 0;
-    for (int q = 0; q < na; ++q) {
-        if (alen[q] && (!ap[q] || !aligned16(ap[q])))
-            return fail(COMERGE_E_INVALID, "merge_pieces: pieces must be 16-byte aligned device arrays");
-        if (q + 1 < na && alen[q] % vece)
-            return fail(COMERGE_E_INVALID, "merge_pieces: every piece but the last must be a multiple of 16 bytes");
-        pc.pa[q] = ap[q];
-        pc.a_start[q] = m;
-        m += alen[q];
+    uint64_t len[2] = {0, 0};
+    for (int side = 0; side < 2; ++side) {
+        const int np = side ? nb : na;
+        const K* const* kp = side ? bp : ap;
+        const uint32_t* const* vp = side ? bpv : apv;
+        const uint64_t* pl = side ? blen : alen;
+        for (int q = 0; q < np; ++q) {
+            if (pl[q] && (!kp[q] || !aligned16(kp[q]) || (HAS_V && (!vp[q] || !aligned16(vp[q])))))
+                return fail(COMERGE_E_INVALID,
+                            "merge_pieces: pieces must be 16-byte aligned device arrays");
+            if (q + 1 < np && pl[q] % vece)
+                return fail(COMERGE_E_INVALID, "merge_pieces: every piece but the last must be a "
+                                               "multiple of 16 bytes (keys and payloads)");
+            (side ? pc.pb : pc.pa)[q] = kp[q];
+            if (HAS_V) (side ? pc.pbv : pc.pav)[q] = vp[q];
+            (side ? pc.b_start : pc.a_start)[q] = len[side];
+            len[side] += pl[q];
+        }
+        for (int q = np; q <= kMaxPieces; ++q) (side ? pc.b_start : pc.a_start)[q] = len[side];
     }
-    for (int q = 0; q < nb; ++q) {
-        if (blen[q] && (!bp[q] || !aligned16(bp[q])))
-            return fail(COMERGE_E_INVALID, "merge_pieces: pieces must be 16-byte aligned device arrays");
-        if (q + 1 < nb && blen[q] % vece)
-            return fail(COMERGE_E_INVALID, "merge_pieces: every piece but the last must be a multiple of 16 bytes");
-        pc.pb[q] = bp[q];
-        pc.b_start[q] = n;
-        n += blen[q];
-    }
-    for (int q = na; q <= kMaxPieces; ++q) pc.a_start[q] = m;
-    for (int q = nb; q <= kMaxPieces; ++q) pc.b_start[q] = n;
+    const uint64_t m = len[0], n = len[1];
     if (out_begin > out_end || out_end > m + n)
         return fail(COMERGE_E_RANGE, "merge_pieces: output range exceeds m+n");
-    if (out_end > out_begin && (!out || !aligned16(out)))
+    if (out_end > out_begin &&
+        (!out || !aligned16(out) || (HAS_V && (!outv || !aligned16(outv)))))
         return fail(COMERGE_E_INVALID, "merge_pieces: output must be a 16-byte aligned device array");
     pc.out_base = out_begin;
     pc.out_end = out_end;
-    return launch_pipe<K, false, 3>(nullptr, nullptr, m, nullptr, nullptr, n, out, nullptr,
-                                    nullptr, nullptr, 0, ws, ws_bytes, s, 0, &pc);
+    return launch_pipe<K, HAS_V, 3>(nullptr, nullptr, m, nullptr, nullptr, n, out, outv, nullptr,
+                                    nullptr, 0, ws, ws_bytes, s, 0, &pc);
 }
 
 template <typename K>
@@ -1288,8 +1296,18 @@ size_t comerge_cuda_segmented_workspace_bytes(size_t total, size_t, int key_kind
                                              const uint64_t* b_lens, int nb, uint64_t out_begin, \
                                              uint64_t out_end, K* out, void* ws,                 \
                                              size_t ws_bytes, comerge_stream_t stream) {         \
-        return merge_pieces_device<K>(a_pieces, a_lens, na, b_pieces, b_lens, nb, out_begin,    \
-                                      out_end, out, ws, ws_bytes, stream);                       \
+        return merge_pieces_device<K, false>(a_pieces, nullptr, a_lens, na, b_pieces, nullptr,  \
+                                             b_lens, nb, out_begin, out_end, out, nullptr, ws,   \
+                                             ws_bytes, stream);                                  \
+    }                                                                                            \
+    int comerge_cuda_merge_pairs_pieces_##SUF(                                                   \
+        const K* const* a_pieces, const uint32_t* const* a_val_pieces, const uint64_t* a_lens,  \
+        int na, const K* const* b_pieces, const uint32_t* const* b_val_pieces,                  \
+        const uint64_t* b_lens, int nb, uint64_t out_begin, uint64_t out_end, K* out_keys,       \
+        uint32_t* out_vals, void* ws, size_t ws_bytes, comerge_stream_t stream) {                \
+        return merge_pieces_device<K, true>(a_pieces, a_val_pieces, a_lens, na, b_pieces,        \
+                                            b_val_pieces, b_lens, nb, out_begin, out_end,        \
+                                            out_keys, out_vals, ws, ws_bytes, stream);           \
     }                                                                                            \
     int comerge_plan_##SUF(const K* a, size_t m, const K* b, size_t n, size_t workers,          \
                            uint64_t* blocks) {                                                   \

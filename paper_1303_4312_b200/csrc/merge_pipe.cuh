@@ -158,6 +158,8 @@ struct pipe_args {
     uint32_t npa, npb;
     const void* pa[kMaxPieces];
     const void* pb[kMaxPieces];
+    const uint32_t* pav[kMaxPieces];  // payload pieces (HAS_V), same cuts as the keys
+    const uint32_t* pbv[kMaxPieces];
     uint64_t pa_start[kMaxPieces + 1];
     uint64_t pb_start[kMaxPieces + 1];
 };
@@ -593,7 +595,6 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
     constexpr int NB = L::NB;
     static_assert(!(SEG == 1 && HAS_V), "explicit-offset segmented batches are keys-only");
     constexpr bool SEGM = L::kSeg;
-    static_assert(!(SEG == 3 && HAS_V), "pieced inputs are keys-only");
 
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::oBars);
@@ -1026,11 +1027,19 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             if constexpr (HAS_V) {
                 av_off = uint32_t(j0 % 4);
                 bv_base = (av_off + a_len + 3) / 4 * 4;
-                avb = RL ? stage_runs(args.av, m + n, j0, j1, RL, 0, sv, 4, false, nullptr, 0)
-                         : stage_copy_plan(args.av, m, j0, j1, sv, 4);
-                bvb = RL ? stage_runs(args.bv, m + n, k0, k1, RL, 1, sv + bv_base, 4, false,
-                                      nullptr, 0)
-                         : stage_copy_plan(args.bv, n, k0, k1, sv + bv_base, 4);
+                if constexpr (SEG == 3) {
+                    avb = stage_pieces(reinterpret_cast<const void* const*>(args.pav),
+                                       args.pa_start, args.npa, j0, j1, sv, 4, false, nullptr, 0);
+                    bvb = stage_pieces(reinterpret_cast<const void* const*>(args.pbv),
+                                       args.pb_start, args.npb, k0, k1, sv + bv_base, 4, false,
+                                       nullptr, 0);
+                } else {
+                    avb = RL ? stage_runs(args.av, m + n, j0, j1, RL, 0, sv, 4, false, nullptr, 0)
+                             : stage_copy_plan(args.av, m, j0, j1, sv, 4);
+                    bvb = RL ? stage_runs(args.bv, m + n, k0, k1, RL, 1, sv + bv_base, 4, false,
+                                          nullptr, 0)
+                             : stage_copy_plan(args.bv, n, k0, k1, sv + bv_base, 4);
+                }
             }
             mt[0] = i0;
             mt[1] = k0;
@@ -1051,7 +1060,12 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
                 if (ab) tma_load_1d(sk, a + (j0 - j0 % VECE), ab, &full[st], policy);
                 if (bb) tma_load_1d(sk + b_base, b + (k0 - k0 % VECE), bb, &full[st], policy);
             }
-            if constexpr (HAS_V) {
+            if constexpr (HAS_V && SEG == 3) {
+                stage_pieces(reinterpret_cast<const void* const*>(args.pav), args.pa_start,
+                             args.npa, j0, j1, sv, 4, true, &full[st], policy);
+                stage_pieces(reinterpret_cast<const void* const*>(args.pbv), args.pb_start,
+                             args.npb, k0, k1, sv + bv_base, 4, true, &full[st], policy);
+            } else if constexpr (HAS_V) {
                 if (RL) {
                     stage_runs(args.av, m + n, j0, j1, RL, 0, sv, 4, true, &full[st], policy);
                     stage_runs(args.bv, m + n, k0, k1, RL, 1, sv + bv_base, 4, true, &full[st],

@@ -54,18 +54,19 @@ def merge_shard(a, b, rank: int, world: int, out=None):
     return sh, out
 
 
-def merge_distributed(a_local, b_local, group=None):
+def merge_distributed(a_local, b_local, group=None, a_vals=None, b_vals=None):
     """Multi-GPU stable merge of a distributed input.
 
     Rank r of the process group holds the r-th contiguous piece of A and of B
-    (device tensors; every piece but the last a multiple of 16 bytes).  The
-    ranks exchange CUDA IPC handles of their pieces once (a host-side
-    all-gather of handles, no data), then each rank merges ITS output range
+    (device tensors; every piece but the last a multiple of 16 bytes, and of 4
+    elements with payloads), optionally with uint32 payload pieces.  The ranks
+    exchange CUDA IPC handles of their pieces once (a host-side all-gather of
+    handles, no data), then each rank merges ITS output range
     [floor(r*T/world), floor((r+1)*T/world)) in one kernel that co-ranks its
     tiles and streams its windows straight out of the peers' memory over
     NVLink -- Algorithm 2 with one worker per GPU, no data-path collective.
-    Returns (out_begin, out_slice).  The peer mappings are closed after a
-    barrier (every rank done reading)."""
+    Returns (out_begin, out_keys) or (out_begin, out_keys, out_vals).  The peer
+    mappings are dropped after a barrier (every rank done reading)."""
     import torch
     import torch.distributed as dist
     from torch.multiprocessing.reductions import reduce_tensor
@@ -73,27 +74,33 @@ def merge_distributed(a_local, b_local, group=None):
     from .comerge import merge_pieces
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    def share(t):  # CUDA IPC handle of the piece (None for an empty one)
-        return reduce_tensor(t) if t.numel() else None
+    pairs = a_vals is not None
 
-    mine = (share(a_local), share(b_local))
+    def share(t):  # CUDA IPC handle of a piece (None for an empty one)
+        return reduce_tensor(t) if t is not None and t.numel() else None
+
+    mine = (share(a_local), share(b_local), share(a_vals), share(b_vals))
     handles = [None] * world
     dist.all_gather_object(handles, (rank, mine, int(a_local.numel()), int(b_local.numel())),
                            group=group)
     handles.sort(key=lambda h: h[0])
-    a_pieces, b_pieces = [], []
-    for r, (ha, hb), _, _ in handles:
-        if r == rank:
-            a_pieces.append(a_local)
-            b_pieces.append(b_local)
-        else:
-            a_pieces.append(ha[0](*ha[1]) if ha else a_local[:0])
-            b_pieces.append(hb[0](*hb[1]) if hb else b_local[:0])
+    local = (a_local, b_local, a_vals, b_vals)
+    pieces = [[], [], [], []]
+    for r, hs, _, _ in handles:
+        for x in range(4 if pairs else 2):
+            if r == rank:
+                pieces[x].append(local[x])
+            else:
+                h = hs[x]
+                pieces[x].append(h[0](*h[1]) if h else local[x][:0])
     total = sum(h[2] + h[3] for h in handles)
     lo, hi = shard_ranges(total, world)[rank]
-    out = merge_pieces(a_pieces, b_pieces, lo, hi)
+    if pairs:
+        ok, ov = merge_pieces(pieces[0], pieces[1], lo, hi, a_val_pieces=pieces[2],
+                              b_val_pieces=pieces[3])
+    else:
+        ok = merge_pieces(pieces[0], pieces[1], lo, hi)
     torch.cuda.synchronize()
     dist.barrier(group=group)  # every rank is done reading its peers' pieces
-    del a_pieces, b_pieces
-    return lo, out
-
+    del pieces
+    return (lo, ok, ov) if pairs else (lo, ok)

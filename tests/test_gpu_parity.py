@@ -659,6 +659,26 @@ def test_merge_pieces_ranges_against_oracle(cuda, port, dt):
         P().merge_pieces([dev(a[:3], cuda), dev(a[3:], cuda)], [dev(b, cuda)], 0, total)
 
 
+@pytest.mark.parametrize("dt", [np.int32, np.uint64])
+def test_merge_pairs_pieces_stability(cuda, port, dt):
+    """Key-value pieces: payload pieces cut like their keys; tagged payloads
+    prove the A-before-B order across piece and range boundaries."""
+    rng = np.random.default_rng(13)
+    a, b = _draw(rng, dt, 300_008, 20), _draw(rng, dt, 250_004, 20)
+    av, bv = tagged(len(a), len(b))
+    ek, ev = port.merge(a, b, av, bv)
+    total = len(a) + len(b)
+    for cuts_a, cuts_b in (([], []), ([100_000, 200_000], [4]), ([8 * k for k in range(1, 8)], [])):
+        pa = [dev(x, cuda) for x in np.split(a, cuts_a)]
+        pav = [dev(x, cuda) for x in np.split(av, cuts_a)]
+        pb = [dev(x, cuda) for x in np.split(b, cuts_b)]
+        pbv = [dev(x, cuda) for x in np.split(bv, cuts_b)]
+        for lo, hi in ((0, total), (99_999, 400_001), (total - 5, total)):
+            ok, ov = P().merge_pieces(pa, pb, lo, hi, a_val_pieces=pav, b_val_pieces=pbv)
+            torch.cuda.synchronize()
+            assert np.array_equal(host(ok), ek[lo:hi]) and np.array_equal(host(ov), ev[lo:hi])
+
+
 def _ipc_worker(rank, world, port, q):
     import os
     import torch.distributed as dist
@@ -677,12 +697,23 @@ def _ipc_worker(rank, world, port, q):
         la = torch.from_numpy(a[ca[rank]:ca[rank + 1]]).cuda()
         lb = torch.from_numpy(b[cb[rank]:cb[rank + 1]]).cuda()
         lo, out = merge_distributed(la, lb)
+        av = np.arange(len(a), dtype=np.uint32)
+        bv = np.arange(len(b), dtype=np.uint32) | np.uint32(1 << 31)
+        lav = torch.from_numpy(av[ca[rank]:ca[rank + 1]]).cuda()
+        lbv = torch.from_numpy(bv[cb[rank]:cb[rank + 1]]).cuda()
+        lo2, ok, ov = merge_distributed(la, lb, a_vals=lav, b_vals=lbv)
         parts = [None] * world
-        dist.all_gather_object(parts, (lo, out.cpu().numpy().tobytes()))
+        dist.all_gather_object(parts, (lo, out.cpu().numpy().tobytes(), ok.cpu().numpy().tobytes(),
+                                       ov.cpu().numpy().tobytes()))
         if rank == 0:
             from oracle.py import Port
-            got = np.concatenate([np.frombuffer(p[1], np.int32) for p in sorted(parts)])
-            q.put(bool(np.array_equal(got, Port().merge(a, b))))
+            parts.sort(key=lambda p: p[0])
+            got = np.concatenate([np.frombuffer(p[1], np.int32) for p in parts])
+            gk = np.concatenate([np.frombuffer(p[2], np.int32) for p in parts])
+            gv = np.concatenate([np.frombuffer(p[3], np.uint32) for p in parts])
+            ek, ev = Port().merge(a, b, av, bv)
+            q.put(bool(np.array_equal(got, Port().merge(a, b)) and np.array_equal(gk, ek)
+                       and np.array_equal(gv, ev)))
         dist.barrier()
     finally:
         dist.destroy_process_group()
