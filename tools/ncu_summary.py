@@ -2,7 +2,8 @@
 profiles/<round>_ncu_summary.json and profiles/traffic.json (DRAM bytes read +
 written per launch, the bench's roofline.traffic).
 
-    python tools/ncu_summary.py r01 C2=gpurun_out/ncu_C2.ncu-rep C5=... """
+    python tools/ncu_summary.py r01 C2=gpurun_out/ncu_C2.ncu-rep C5=... [X=rep@k]
+(traffic.json is only updated for the BASELINE config labels C1..C5.)"""
 import csv
 import io
 import json
@@ -21,11 +22,11 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
-def raw(rep):
+def raw(rep, index=0):
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units, vals = rows[0], rows[1], rows[2 + index]
     return {h: (u, v) for h, u, v in zip(hdr, units, vals)}, vals[hdr.index("Kernel Name")]
 
 
@@ -50,7 +51,11 @@ def main():
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
     for arg in sys.argv[2:]:
         cfg, rep = arg.split("=", 1)
-        d, kname = raw(rep)
+        index = 0
+        if "@" in rep:  # report@k: the k-th kernel of a multi-kernel capture
+            rep, k = rep.rsplit("@", 1)
+            index = int(k)
+        d, kname = raw(rep, index)
         entry = {"kernel": kname, "report": os.path.basename(rep)}
         for k in KEYS:
             if k in d:
@@ -59,6 +64,8 @@ def main():
         entry["stall_reasons_pct_top6"] = stalls(d)
         summary[cfg] = entry
         try:
+            if not cfg.startswith("C"):
+                raise KeyError(cfg)
             rb = float(d["dram__bytes_read.sum"][1].replace(",", "")) * SCALE[d["dram__bytes_read.sum"][0]]
             wb = float(d["dram__bytes_write.sum"][1].replace(",", "")) * SCALE[d["dram__bytes_write.sum"][0]]
             traffic[cfg] = int(rb + wb)
