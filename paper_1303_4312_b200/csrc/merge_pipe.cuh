@@ -4,31 +4,33 @@
 // Algorithm 2 of arXiv 1303.4312 (reference
 // parallel.hpp:180-282) mapped onto a persistent grid:
 //
-//   * Work unit = an output tile of T = 256*VT elements.  Tiles are grouped in
-//     contiguous chunks; a chunk is what a reference worker does
-//     (parallel.hpp:201-207): co-rank its start and end, then merge.
-//     B200 SMs do not stream at equal rates (measured: ~25% spread between
-//     GPCs) and CTA->SM placement of a persistent grid is deterministic, so
-//     CTA c takes a contiguous static range of tiles proportional to a weight
-//     learned from the per-CTA throughput of earlier launches (reported through
-//     host-mapped memory).  The last few tiles per CTA form a dynamic tail:
-//     claimed one at a time from a global counter, their co-ranks computed in
-//     the background by a tail warp in every CTA -- this absorbs start-up
-//     jitter and any residual rate mismatch.
-//   * Scheduler warp: claims a chunk only when fewer than LOOKAHEAD tiles are
-//     queued, co-ranks its start (one 33-ary warp search over the whole
-//     diagonal) and then every later boundary of the chunk -- its end included
-//     -- bracketed by its predecessor (lane-group searches, 1, 4, 8, then 32
-//     boundaries per pass), and pushes tile descriptors (i0, j0, j1, i1) into a
-//     shared-memory ring.
+//   * Work unit = an output tile of T = 256*VT elements.  CTA c owns an equal
+//     contiguous static range of the first 70% of the tiles (a reference
+//     worker's block, parallel.hpp:201-207: co-rank its start, then every
+//     later boundary); the remaining 30% form a dynamic tail claimed one tile
+//     at a time from a global counter, their co-ranks computed in the
+//     background by a tail warp in every CTA.  The tail absorbs the start-up
+//     skew between CTAs and the ~25% spread of per-SM streaming rates
+//     (B200 GPCs differ).
+//   * Scheduler warp: co-ranks its range start (33-ary warp search over the
+//     whole diagonal, finished by the consumer warps together with the next 8
+//     boundaries), then every later boundary bracketed by its predecessor
+//     (lane-group searches, 1, 4, then 8 boundaries per pass, at most 8 tiles
+//     ahead of the producer), and pushes tile descriptors (i0, j0, j1, i1, s0,
+//     s1) into a shared-memory ring; then claims tail tiles.
 //   * Producer warp: per descriptor, waits for a free stage and TMA-loads
 //     exactly the tile's A window [j0, j1) and B window [i0-j0, i1-j1) (16-byte
 //     aligned supersets, payloads too): every input byte crosses HBM once.
+//     Segmented batches: the whole warp also writes the tile's segment-end
+//     table into the stage.
 //   * Consumers (8 warps): tile-local co-rank per VT-slot diagonal and the
 //     branch-free serial merge (merge.hpp:22-31, ties to A) of merge_tile.cuh;
 //     the merged tile is written back into the stage and handed to the store
 //     warp, which stores it with one TMA bulk store and releases the stage
 //     once the store has read it (consumers never wait on a store).
+//   * SEG selects the input model: 0 plain, 1 segmented batch, 2 merge pass
+//     of the sort (runs of run_len), 3 pieced inputs (multi-GPU split); any
+//     launch merges the output range [out_base, out_end).
 #pragma once
 
 #include <cstdint>
@@ -134,7 +136,7 @@ struct pipe_args {
     const uint64_t* boff;        // segmented batches: nseg+1 offsets into b
     uint64_t nseg;
     unsigned long long* trace;   // optional per-CTA timestamps (8 x u64 per CTA)
-    uint64_t static_tiles;       // tiles [0, static_tiles) are split statically by weight
+    uint64_t static_tiles;       // tiles [0, static_tiles) are split statically (equal shares)
     uint32_t lookahead;          // claim a tail tile when fewer than this are queued
     uint64_t* tail;              // dynamic tail workspace (16B aligned): {tag, count} + slots
     uint64_t epoch;              // per-launch tag validating tail state (no memset needed)
