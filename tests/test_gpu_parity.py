@@ -736,3 +736,83 @@ def test_merge_distributed_ipc_world2(cuda):
         p.join(timeout=300)
     assert all(p.exitcode == 0 for p in procs)
     assert q.get(timeout=5) is True
+
+
+# ------------------------------------------------- write-once coverage
+# the outputs sit inside a poisoned device buffer; every path must
+# write exactly its output range (guards untouched) and every position in it
+# (the oracle comparison), for keys, payloads, segmented batches, pieced
+# ranges and the sorts.
+
+def _guarded(n, dtype, cuda, guard=4099, poison=0x5A):
+    buf = torch.full((n + 2 * guard,), poison, dtype=torch.int64, device=cuda).to(dtype)
+    return buf, buf[guard:guard + n], guard
+
+
+def _guards_intact(buf, n, guard, poison=0x5A):
+    h = host(buf.view(torch.uint8) if buf.dtype == torch.uint64 else buf)
+    if buf.dtype == torch.uint64:
+        h = host(buf.view(torch.int64))
+    return bool((h[:guard] == poison).all() and (h[guard + n:] == poison).all())
+
+
+@pytest.mark.parametrize("guard", [4096, 4099])  # aligned (pipeline) and misaligned output
+def test_outputs_written_exactly_once(cuda, path, port, guard):
+    rng = np.random.default_rng(21)
+    for dt in (np.int32, np.uint64):
+        a, b = _draw(rng, dt, 123_457, 30), _draw(rng, dt, 98_765, 30)
+        av, bv = tagged(len(a), len(b))
+        total = len(a) + len(b)
+        # keys
+        buf, out, g = _guarded(total, TDT[np.dtype(dt)], cuda, guard)
+        P().stable_merge(dev(a, cuda), dev(b, cuda), out)
+        torch.cuda.synchronize()
+        assert _guards_intact(buf, total, g) and np.array_equal(host(out), port.merge(a, b))
+        # key-value
+        kbuf, ok, g = _guarded(total, TDT[np.dtype(dt)], cuda, guard)
+        vbuf, ov, _ = _guarded(total, torch.uint32, cuda, guard)
+        P().merge_pairs(dev(a, cuda), dev(av, cuda), dev(b, cuda), dev(bv, cuda), ok, ov)
+        torch.cuda.synchronize()
+        ek, ev = port.merge(a, b, av, bv)
+        assert _guards_intact(kbuf, total, g) and _guards_intact(vbuf, total, g)
+        assert np.array_equal(host(ok), ek) and np.array_equal(host(ov), ev)
+
+
+@pytest.mark.parametrize("guard", [4096, 4099])
+def test_outputs_written_exactly_once_other_modes(cuda, port, guard):
+    rng = np.random.default_rng(22)
+    # segmented batch (ragged, empty pairs)
+    la, lb = rng.integers(0, 700, 400), rng.integers(0, 700, 400)
+    la[::9] = 0
+    sa = np.concatenate([np.sort(rng.integers(0, 99, x)) for x in la]).astype(np.int32)
+    sb = np.concatenate([np.sort(rng.integers(0, 99, x)) for x in lb]).astype(np.int32)
+    ao = np.concatenate([[0], np.cumsum(la)]).astype(np.uint64)
+    bo = np.concatenate([[0], np.cumsum(lb)]).astype(np.uint64)
+    total = len(sa) + len(sb)
+    buf, out, g = _guarded(total, torch.int32, cuda, guard)
+    P().merge_segmented(dev(sa, cuda), dev(ao, cuda), dev(sb, cuda), dev(bo, cuda), out)
+    torch.cuda.synchronize()
+    assert _guards_intact(buf, total, g)
+    assert np.array_equal(host(out), port.merge_segmented(sa, ao, sb, bo))
+    # pieced range merge
+    a, b = _draw(rng, np.int32, 200_000, 50), _draw(rng, np.int32, 180_004, 50)
+    lo, hi = 77_777, 300_001
+    buf, out, g = _guarded(hi - lo, torch.int32, cuda, 4096)
+    P().merge_pieces([dev(a[:100_000], cuda), dev(a[100_000:], cuda)], [dev(b, cuda)], lo, hi,
+                     out=out)
+    torch.cuda.synchronize()
+    assert _guards_intact(buf, hi - lo, g) and np.array_equal(host(out), port.merge(a, b)[lo:hi])
+    # sorts (keys, pairs) into guarded outputs
+    k = rng.integers(-5000, 5000, 150_001).astype(np.int32)
+    v = np.arange(len(k), dtype=np.uint32)
+    buf, out, g = _guarded(len(k), torch.int32, cuda, guard)
+    P().sort(dev(k, cuda), out=out)
+    torch.cuda.synchronize()
+    assert _guards_intact(buf, len(k), g) and np.array_equal(host(out), port.merge_sort(k))
+    kbuf, ok, g = _guarded(len(k), torch.int32, cuda, guard)
+    vbuf, ov, _ = _guarded(len(k), torch.uint32, cuda, guard)
+    P().sort_pairs(dev(k, cuda), dev(v, cuda), out_keys=ok, out_vals=ov)
+    torch.cuda.synchronize()
+    ek, ev = port.merge_sort_pairs(k, v)
+    assert _guards_intact(kbuf, len(k), g) and _guards_intact(vbuf, len(k), g)
+    assert np.array_equal(host(ok), ek) and np.array_equal(host(ov), ev)
