@@ -195,7 +195,7 @@ size_t merge_ws_bytes(size_t m, size_t n) {
     constexpr uint64_t pt = pipe_layout<K, false>::T < pipe_layout<K, true>::T
                                 ? pipe_layout<K, false>::T
                                 : pipe_layout<K, true>::T;
-    const size_t pipe_ws = round256(32 * (div_up(total, pt) + 2));
+    const size_t pipe_ws = round256(32 * (div_up(total, pt) + 4));
     return tile_ws > pipe_ws ? tile_ws : pipe_ws;
 }
 
@@ -203,7 +203,7 @@ template <typename K>
 size_t seg_ws_bytes(size_t total) {
     if (total == 0) return 0;
     const size_t tile_ws = 2 * round256((div_up(total, seg_cfg<K>::kTile) + 1) * sizeof(uint64_t));
-    const size_t pipe_ws = round256(32 * (div_up(total, pipe_layout<K, false, 1>::T) + 2));
+    const size_t pipe_ws = round256(32 * (div_up(total, pipe_layout<K, false, 1>::T) + 4));
     return tile_ws > pipe_ws ? tile_ws : pipe_ws;
 }
 
@@ -308,7 +308,7 @@ int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const ui
     args.static_tiles = ptiles - tail_tiles;
     scratch sc;
     if (tail_tiles > 0) {
-        if (int rc = sc.acquire(ws, ws_bytes, 32 * (tail_tiles + 2), s)) return rc;
+        if (int rc = sc.acquire(ws, ws_bytes, 32 * (tail_tiles + 4), s)) return rc;
         args.tail = static_cast<uint64_t*>(sc.ptr);
         args.epoch = next_tail_epoch();
     }
@@ -1090,7 +1090,7 @@ template <typename K>
 size_t sort_ws_bytes(size_t n) {
     if (n == 0) return 0;
     const size_t buf = round256(n * sizeof(K));
-    const size_t tail = round256(32 * (div_up(n, pipe_layout<K, false, 1>::T) + 2));
+    const size_t tail = round256(32 * (div_up(n, pipe_layout<K, false, 1>::T) + 4));
     return 2 * buf + tail;
 }
 
@@ -1098,7 +1098,7 @@ template <typename K>
 size_t sort_pairs_ws_bytes(size_t n) {
     if (n == 0) return 0;
     const size_t buf = round256(n * sizeof(K)) + round256(n * 4);
-    const size_t tail = round256(32 * (div_up(n, pipe_layout<K, true, 2>::T) + 2));
+    const size_t tail = round256(32 * (div_up(n, pipe_layout<K, true, 2>::T) + 4));
     return 2 * buf + tail;
 }
 

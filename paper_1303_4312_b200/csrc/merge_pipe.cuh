@@ -388,7 +388,13 @@ __device__ __forceinline__ boundary find_boundary(const pipe_args& args, uint64_
 // ---- dynamic tail state.  The workspace is not cleared between launches;
 // every word is validated against this launch's 64-bit epoch instead:
 //   tail[0..1]     = {tag, count}: reset once per launch by a 128-bit CAS
-//   slot q (32 B)  = {j, s, hash(epoch, q, j, s), 0} at tail + 4 + 4q
+//   tail[4]        = launch counter (any initial value): every CTA claims until
+//                    it draws an index past the tail, so the launch's last claim
+//                    is number (tail tiles + CTAs - 1); that claimer bumps it
+//   slot q (32 B)  = {j, s, hash(epoch, q, j, s), 0} at tail + kTailSlots + 4q
+// The epoch is the host's per-call salt mixed with the launch counter, so it
+// changes on every launch even when a CUDA graph replays identical arguments.
+constexpr int kTailSlots = 8;  // u64 words before the first slot
 __device__ __forceinline__ uint64_t tail_hash(uint64_t epoch, uint64_t q, uint64_t j,
                                               uint64_t s) {
     uint64_t x = epoch ^ (q * 0x9e3779b97f4a7c15ULL) ^ (j + 0x632be59bd9b4e019ULL) ^
@@ -651,6 +657,14 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         }
         *pushed = 0;
         *issued = 0;
+        // this launch's tail epoch (see kTailSlots): read before the last claim
+        uint64_t e = args.epoch;
+        if (args.tail) {
+            uint64_t lc, pad;
+            ld_pair(args.tail + 4, lc, pad);
+            e ^= tail_hash(lc, 0x5eedull, 0, 0);
+        }
+        scratch[38] = e;
         mbar_fence_init();
     }
     // ---- start-up: this worker's static range [ts0, te0), an equal share of
@@ -734,6 +748,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         __syncthreads();
     }
     if (args.trace && tid == 0) args.trace[8 * c + 5] = globaltimer_ns();
+    const uint64_t epoch = scratch[38];  // written by thread 0 before the start-up barriers
     if (warp == W_TAIL) {
         // ------------------------------------------------------ tail warp
         // co-rank the tail boundaries q = c, c+G, ... (in passes of up to 32,
@@ -751,9 +766,9 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             full_bracket(i, lo, hi);
             const boundary bd = find_boundary<K, SEG>(args, i, lo, hi, 0, P, nullptr);
             if (lane % P == 0 && g < k) {
-                uint64_t* slot = args.tail + 4 + 4 * q;
+                uint64_t* slot = args.tail + kTailSlots + 4 * q;
                 st_pair(slot, bd.j, bd.s);
-                st_pair(slot + 2, tail_hash(args.epoch, q, bd.j, bd.s), 0);
+                st_pair(slot + 2, tail_hash(epoch, q, bd.j, bd.s), 0);
             }
         }
         return;
@@ -843,7 +858,11 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             for (;;) {
                 while (*pushed - *issued >= args.lookahead) __nanosleep(500);
                 uint64_t q = 0;
-                if (lane == 0) q = tail_claim(args.tail, args.epoch);
+                if (lane == 0) {
+                    q = tail_claim(args.tail, epoch);
+                    if (q == NT - NS + G - 1)  // the launch's last claim: next launch, new epoch
+                        atomicAdd(reinterpret_cast<unsigned long long*>(args.tail + 4), 1ull);
+                }
                 q = __shfl_sync(0xffffffffu, q, 0);
                 if (NS + q >= NT) break;
                 ++n_claims;
@@ -855,11 +874,11 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
                     boundary bd{m, SEGM ? args.nseg - 1 : 0};  // the last boundary is (m, n)
                     bool ok = NS + qq == NT && out_end == total;
                     if (!ok) {
-                        const uint64_t* slot = args.tail + 4 + 4 * qq;
+                        const uint64_t* slot = args.tail + kTailSlots + 4 * qq;
                         uint64_t tag, pad;
                         ld_pair(slot, bd.j, bd.s);
                         ld_pair(slot + 2, tag, pad);
-                        ok = tag == tail_hash(args.epoch, qq, bd.j, bd.s);
+                        ok = tag == tail_hash(epoch, qq, bd.j, bd.s);
                     }
                     if (!__shfl_sync(0xffffffffu, ok, 0)) {
                         uint64_t lo, hi;

@@ -816,3 +816,44 @@ def test_outputs_written_exactly_once_other_modes(cuda, port, guard):
     ek, ev = port.merge_sort_pairs(k, v)
     assert _guards_intact(kbuf, len(k), g) and _guards_intact(vbuf, len(k), g)
     assert np.array_equal(host(ok), ek) and np.array_equal(host(ov), ev)
+
+
+# ------------------------------------------------------- CUDA graph replay
+def test_cuda_graph_replay_new_inputs(cuda, port):
+    """A merge captured in a CUDA graph and replayed on new contents of the same
+    buffers: the dynamic tail's per-launch epoch comes from a device-side
+    launch counter, so identical kernel arguments never reuse stale state."""
+    rng = np.random.default_rng(31)
+    m, n = 1 << 21, (1 << 21) + 12345
+    ta = torch.empty(m, dtype=torch.int32, device=cuda)
+    tb = torch.empty(n, dtype=torch.int32, device=cuda)
+    tav = torch.arange(m, dtype=torch.int32, device=cuda).view(torch.uint32)
+    tbv = (torch.arange(n, dtype=torch.int64, device=cuda) | (1 << 31)).to(torch.int32).view(torch.uint32)
+    ok = torch.empty(m + n, dtype=torch.int32, device=cuda)
+    ov = torch.empty(m + n, dtype=torch.uint32, device=cuda)
+    ws = torch.empty(P().workspace_bytes(m, n, torch.int32, True), dtype=torch.uint8, device=cuda)
+
+    def fill(seed):
+        r = np.random.default_rng(seed)
+        a = np.sort(r.integers(0, 1 << 20, m)).astype(np.int32)
+        b = np.sort(r.integers(0, 1 << 20, n)).astype(np.int32)
+        ta.copy_(torch.from_numpy(a))
+        tb.copy_(torch.from_numpy(b))
+        return a, b
+
+    fill(0)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):  # warm-up outside capture (occupancy, attributes)
+        P().merge_pairs(ta, tav, tb, tbv, ok, ov, workspace=ws)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        P().merge_pairs(ta, tav, tb, tbv, ok, ov, workspace=ws)
+    av, bv = host(tav), host(tbv)
+    for seed in (1, 2, 3, 4):
+        a, b = fill(seed)
+        g.replay()
+        torch.cuda.synchronize()
+        ek, ev = port.merge(a, b, av, bv)
+        assert np.array_equal(host(ok), ek) and np.array_equal(host(ov), ev), seed
