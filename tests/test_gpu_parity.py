@@ -857,3 +857,19 @@ def test_cuda_graph_replay_new_inputs(cuda, port):
         torch.cuda.synchronize()
         ek, ev = port.merge(a, b, av, bv)
         assert np.array_equal(host(ok), ek) and np.array_equal(host(ov), ev), seed
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.uint64])
+def test_merge_pieces_large_range_with_dynamic_tail(cuda, port, dt):
+    """Ranges long enough for the pipeline's dynamic tail (>= 4 tiles per CTA),
+    ending before m + n: the tail's last boundary is co-ranked, not (m, n)."""
+    rng = np.random.default_rng(41)
+    m, n = 6_000_000, 5_000_004
+    a, b = _draw(rng, dt, m, 1 << 16), _draw(rng, dt, n, 1 << 16)
+    expect = port.merge_parallel(a, b, 16, threads=8)[0]
+    pa = [dev(a[:2_000_000], cuda), dev(a[2_000_000:], cuda)]
+    pb = [dev(b[:3_000_000], cuda), dev(b[3_000_000:], cuda)]
+    for lo, hi in ((1_234_567, m + n - 7), (0, m + n), (3, 10_000_001)):
+        out = P().merge_pieces(pa, pb, lo, hi)
+        torch.cuda.synchronize()
+        assert np.array_equal(host(out), expect[lo:hi]), (lo, hi)
