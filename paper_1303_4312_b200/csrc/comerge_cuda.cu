@@ -235,8 +235,6 @@ int check_merge_args(const char* who, const K* a, size_t m, const K* b, size_t n
     return COMERGE_OK;
 }
 
-// Launch the persistent tile pipeline (merge_pipe.cuh) for a plain merge or a
-// segmented batch (aoff/boff/nseg).  Scratch: the dynamic-tail state.
 // Pieced inputs (SEG == 3) and output ranges for launch_pipe.
 struct pipe_pieces {
     uint32_t na = 0, nb = 0;
@@ -249,6 +247,10 @@ struct pipe_pieces {
     uint64_t out_base = 0, out_end = 0;
 };
 
+// Launch the persistent tile pipeline (merge_pipe.cuh): a plain merge
+// (SEG 0), a segmented batch (1: aoff/boff/nseg), a merge pass of the sort (2:
+// run_len) or pieced inputs (3), over the whole output or pieces->[out_base,
+// out_end).  Scratch: the dynamic-tail state.
 template <typename K, bool HAS_V, int SEG>
 int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const uint32_t* bv,
                 uint64_t n, K* out, uint32_t* outv, const uint64_t* aoff, const uint64_t* boff,
