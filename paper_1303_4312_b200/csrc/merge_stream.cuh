@@ -125,6 +125,11 @@ __device__ __forceinline__ void tma_store_1d_hint(void* dst, const void* src, ui
                  : "memory");
 }
 
+// bulk prefetch of global memory into L2 (no completion to wait for)
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void tma_store_commit() {
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
