@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
@@ -645,72 +646,68 @@ host_streams& hstreams() {
     return hs;
 }
 
-// Key and payload windows of one chunk side go over PCIe as ONE 2-row
-// cudaMemcpy2DAsync when the two arrays are a fixed positive pitch apart on
-// both sides (measured: 6 separate copies per chunk cost ~1 ms more per C2
-// merge than 3 two-row copies; every extra copy command costs ~40 us here).
-// The device rows are laid out to match the host order (`swap`).
-struct pair_copy {
-    static size_t max_pitch() {
-        static const size_t v = [] {
-            int dev = 0, p = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&p, cudaDevAttrMaxPitch, dev);
-            return size_t(p);
-        }();
-        return v;
-    }
-    // host arrays x, y: device rows are dev (first) and dev + P (second)
-    static bool swapped(const void* x, const void* y) { return y < x; }
-    // copy `width` bytes of host rows hx, hy <-> device rows dx, dy
-    static cudaError_t run(void* dx, void* dy, const void* sx, const void* sy, size_t width,
-                           cudaMemcpyKind kind, cudaStream_t st) {
-        if (width == 0) return cudaSuccess;
-        const char *s0 = static_cast<const char*>(sx), *s1 = static_cast<const char*>(sy);
-        char *d0 = static_cast<char*>(dx), *d1 = static_cast<char*>(dy);
-        if (s1 < s0) {
-            std::swap(s0, s1);
-            std::swap(d0, d1);
-        }
-        const size_t sp = size_t(s1 - s0);
-        const bool dpos = d1 > d0;
-        const size_t dp = dpos ? size_t(d1 - d0) : 0;
-        if (dpos && sp >= width && dp >= width && sp <= max_pitch() && dp <= max_pitch()) {
-            if (cudaMemcpy2DAsync(d0, dp, s0, sp, width, 2, kind, st) == cudaSuccess)
-                return cudaSuccess;
-            cudaGetLastError();  // fall back to two copies
-        }
-        cudaError_t e = cudaMemcpyAsync(d0, s0, width, kind, st);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(d1, s1, width, kind, st);
-        return e;
-    }
-};
-
 template <typename K, bool HAS_V>
 int merge_host_pipeline(const K* a, const uint32_t* av, uint64_t m, const K* b,
                         const uint32_t* bv, uint64_t n, K* out, uint32_t* outv, uint64_t* h2d,
                         uint64_t* d2h, uint64_t* merge_ns) {
     host_streams& hs = hstreams();
     const uint64_t total = m + n;
-    // `parts` equal output chunks of at least 2^18 elements (more chunks
-    // shorten the fill / drain but every copy command costs ~4-16 us on this
-    // PCIe path: 8 measured best for C2)
+    // Copy granularity: every copy starts (and, but for an array's end, ends)
+    // on a multiple of G elements = 256 bytes of 32-bit data.  Measured on C2's
+    // shape (tools/micro/e2e_model2.cu): the same chunked copies take 6.1 ms
+    // with 256-byte aligned windows and 7.2 ms with windows a few elements off.
+    constexpr uint64_t G = 64;
     static const uint64_t parts = [] {
         const char* e = std::getenv("COMERGE_HOST_CHUNKS");  // tuning knob (benchmarking)
         const long v = e ? std::atol(e) : 0;
         return uint64_t(v > 0 ? v : 8);
     }();
-    const uint64_t chunk = std::max(div_up(total, parts), uint64_t(1) << 18);
-    const uint64_t nchunks = div_up(total, chunk);
-    std::vector<uint64_t> cuts(nchunks + 1);
-    for (uint64_t c = 0; c <= nchunks; ++c) cuts[c] = std::min(total, c * chunk);
+    // `parts` equal chunks (weights); tried and not better on C2: 6, 12 and 16
+    // chunks, smaller first / last chunks (a chunk's H2D overlaps the previous
+    // chunk's D2H, so the bytes moved with one direction idle stay ~2x the
+    // largest chunk however the sizes ramp), see DESIGN.md section 5
+    std::vector<double> w(parts, 1.0);
+    if (const char* ew = std::getenv("COMERGE_HOST_WEIGHTS")) {  // tuning knob (benchmarking)
+        w.clear();
+        for (const char* q = ew; *q;) {
+            char* end = nullptr;
+            const double x = std::strtod(q, &end);
+            if (end == q) break;
+            if (x > 0) w.push_back(x);
+            q = *end ? end + 1 : end;
+        }
+        if (w.empty()) w.push_back(1.0);
+    }
+    double wsum = 0;
+    for (double x : w) wsum += x;
+    // chunks of at least 2^18 elements (small merges: fewer, equal chunks)
+    const uint64_t min_chunk = uint64_t(1) << 18;
+    if (double(total) * w.front() / wsum < double(min_chunk)) {
+        const uint64_t k = std::max<uint64_t>(1, std::min<uint64_t>(parts, total / min_chunk));
+        w.assign(k, 1.0);
+        wsum = double(k);
+    }
+    std::vector<uint64_t> cuts(1, 0);
+    double acc = 0;
+    for (size_t q = 0; q < w.size(); ++q) {
+        acc += w[q];
+        const uint64_t c = q + 1 == w.size() ? total
+                                            : std::min(total, uint64_t(double(total) * acc / wsum) / G * G);
+        if (c > cuts.back()) cuts.push_back(c);
+    }
+    const uint64_t nchunks = cuts.size() - 1;
+    uint64_t chunk = 0;
+    for (uint64_t c = 0; c < nchunks; ++c) chunk = std::max(chunk, cuts[c + 1] - cuts[c]);
     // chunk boundaries: the Lemma-1 split of every chunk start, on host data
     std::vector<uint64_t> js(nchunks + 1);
     for (uint64_t c = 0; c <= nchunks; ++c)
         js[c] = co_rank_split<K, uint64_t>(cuts[c], a, m, b, n, [](const K* p) { return *p; });
-    // three slots of device windows (A, B, out [+ payloads]) from the pool
-    const size_t kb = chunk * sizeof(K), vb = HAS_V ? chunk * 4 : 0;
-    const size_t slot_bytes = 6 * (round256(kb) > round256(vb) ? round256(kb) : round256(vb));
+    // three slots of device windows (A, B, out [+ payloads]) from the pool;
+    // an input window is copied from its G-aligned start, so it holds up to
+    // G - 1 leading elements of the previous chunk (+ G of end round-up)
+    const uint64_t wcap = chunk + 2 * G;
+    const size_t kb = round256(wcap * sizeof(K)), vb = HAS_V ? round256(wcap * 4) : 0;
+    const size_t slot_bytes = 3 * (kb + vb);
     void* buf = nullptr;
     cudaError_t e = pool_alloc(&buf, 3 * slot_bytes, hs.comp);
     if (e != cudaSuccess) return cuda_fail(e, "comerge: host pipeline staging");
@@ -718,54 +715,74 @@ int merge_host_pipeline(const K* a, const uint32_t* av, uint64_t m, const K* b,
     cudaStreamWaitEvent(hs.h2d, hs.in_done[0], 0);
     int rc = COMERGE_OK;
     bool first = true;
+    // COMERGE_HOST_TRACE=1: per-chunk timeline on stderr (h2d start/end, merge
+    // end, d2h end, us from the first copy) -- a benchmarking aid
+    static const bool trace = std::getenv("COMERGE_HOST_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev(trace ? 4 * nchunks : 0);
+    for (auto& ev : tev) cudaEventCreate(&ev);
+    // One copy command per host array window.  The copy engines pair the two
+    // directions' commands one for one, so the device->host side is cut into
+    // about the same sizes in the same order as the host->device side (the
+    // first |A window| outputs of a chunk, then the rest): 4 H2D + 4 matched
+    // D2H commands per chunk measured 6.1 ms of copies on C2, 4 + 2 7.0 ms.
+    auto h2d_copy = [&](void* dst, const void* src, size_t bytes) {
+        if (bytes) cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, hs.h2d);
+    };
+    auto d2h_copy = [&](void* dst, const void* src, size_t bytes) {
+        if (bytes) cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, hs.d2h);
+    };
     for (uint64_t c = 0; c < nchunks && rc == COMERGE_OK; ++c) {
         const int sl = int(c % 3);
         unsigned char* base = static_cast<unsigned char*>(buf) + sl * slot_bytes;
-        // slot: [A-pair | B-pair | out-pair], each pair's rows P apart, keys
-        // first unless the host payload array lies below the host key array
-        const size_t P = round256(kb) > round256(vb) ? round256(kb) : round256(vb);
-        auto row = [&](int pair, bool second) { return base + size_t(pair) * 2 * P + (second ? P : 0); };
-        const bool sa = HAS_V && pair_copy::swapped(a, av), sb = HAS_V && pair_copy::swapped(b, bv);
-        const bool so = HAS_V && pair_copy::swapped(out, outv);
-        K* dA = reinterpret_cast<K*>(row(0, sa));
-        uint32_t* dAv = reinterpret_cast<uint32_t*>(row(0, !sa));
-        K* dB = reinterpret_cast<K*>(row(1, sb));
-        uint32_t* dBv = reinterpret_cast<uint32_t*>(row(1, !sb));
-        K* dO = reinterpret_cast<K*>(row(2, so));
-        uint32_t* dOv = reinterpret_cast<uint32_t*>(row(2, !so));
+        K* dA = reinterpret_cast<K*>(base);
+        K* dB = reinterpret_cast<K*>(base + kb);
+        K* dO = reinterpret_cast<K*>(base + 2 * kb);
+        uint32_t* dAv = reinterpret_cast<uint32_t*>(base + 3 * kb);
+        uint32_t* dBv = reinterpret_cast<uint32_t*>(base + 3 * kb + vb);
+        uint32_t* dOv = reinterpret_cast<uint32_t*>(base + 3 * kb + 2 * vb);
         const uint64_t i0 = cuts[c], i1 = cuts[c + 1];
         const uint64_t j0 = js[c], j1 = js[c + 1], k0 = i0 - j0, k1 = i1 - j1;
+        // aligned input windows A[sa, ea) ⊇ A[j0, j1), B[sb, eb) ⊇ B[k0, k1)
+        const uint64_t sa = j0 / G * G, ea = std::min(m, div_up(j1, G) * G);
+        const uint64_t sb = k0 / G * G, eb = std::min(n, div_up(k1, G) * G);
         if (c >= 3) cudaStreamWaitEvent(hs.h2d, hs.out_done[sl], 0);  // slot free again
-        if (HAS_V && sizeof(K) == 4) {  // keys and payloads of a side in one command
-            pair_copy::run(dA, dAv, a + j0, av + j0, (j1 - j0) * 4, cudaMemcpyHostToDevice, hs.h2d);
-            pair_copy::run(dB, dBv, b + k0, bv + k0, (k1 - k0) * 4, cudaMemcpyHostToDevice, hs.h2d);
-        } else {
-            if (j1 > j0) cudaMemcpyAsync(dA, a + j0, (j1 - j0) * sizeof(K), cudaMemcpyHostToDevice, hs.h2d);
-            if (k1 > k0) cudaMemcpyAsync(dB, b + k0, (k1 - k0) * sizeof(K), cudaMemcpyHostToDevice, hs.h2d);
-            if (HAS_V) {
-                if (j1 > j0) cudaMemcpyAsync(dAv, av + j0, (j1 - j0) * 4, cudaMemcpyHostToDevice, hs.h2d);
-                if (k1 > k0) cudaMemcpyAsync(dBv, bv + k0, (k1 - k0) * 4, cudaMemcpyHostToDevice, hs.h2d);
-            }
-        }
+        if (trace) cudaEventRecord(tev[4 * c], hs.h2d);
+        h2d_copy(dA, a + sa, (ea - sa) * sizeof(K));
+        if (HAS_V) h2d_copy(dAv, av + sa, (ea - sa) * 4);
+        h2d_copy(dB, b + sb, (eb - sb) * sizeof(K));
+        if (HAS_V) h2d_copy(dBv, bv + sb, (eb - sb) * 4);
         *h2d += (i1 - i0) * (sizeof(K) + (HAS_V ? 4 : 0));
         cudaEventRecord(hs.in_done[sl], hs.h2d);
+        if (trace) cudaEventRecord(tev[4 * c + 1], hs.h2d);
         cudaStreamWaitEvent(hs.comp, hs.in_done[sl], 0);
         if (first) {
             cudaEventRecord(hs.t0, hs.comp);
             first = false;
         }
-        rc = merge_device<K, HAS_V>(dA, HAS_V ? dAv : nullptr, j1 - j0, dB, HAS_V ? dBv : nullptr,
-                                    k1 - k0, dO, HAS_V ? dOv : nullptr, nullptr, 0, hs.comp);
+        // the chunk is output ranks [(j0-sa)+(k0-sb), +(i1-i0)) of the merge
+        // of A[sa, j1) and B[sb, k1): the leading elements precede every chunk
+        // element in the stable order, so the range is exactly out[i0, i1)
+        const K* pa[1] = {dA};
+        const K* pb[1] = {dB};
+        const uint32_t* pav[1] = {dAv};
+        const uint32_t* pbv[1] = {dBv};
+        const uint64_t la[1] = {j1 - sa}, lb[1] = {k1 - sb};
+        const uint64_t r0 = (j0 - sa) + (k0 - sb);
+        rc = merge_pieces_device<K, HAS_V>(pa, HAS_V ? pav : nullptr, la, 1, pb,
+                                           HAS_V ? pbv : nullptr, lb, 1, r0, r0 + (i1 - i0), dO,
+                                           HAS_V ? dOv : nullptr, nullptr, 0, hs.comp);
         cudaEventRecord(hs.merged[sl], hs.comp);
+        if (trace) cudaEventRecord(tev[4 * c + 2], hs.comp);
         cudaStreamWaitEvent(hs.d2h, hs.merged[sl], 0);
-        if (HAS_V && sizeof(K) == 4) {
-            pair_copy::run(out + i0, outv + i0, dO, dOv, (i1 - i0) * 4, cudaMemcpyDeviceToHost, hs.d2h);
-        } else {
-            cudaMemcpyAsync(out + i0, dO, (i1 - i0) * sizeof(K), cudaMemcpyDeviceToHost, hs.d2h);
-            if (HAS_V) cudaMemcpyAsync(outv + i0, dOv, (i1 - i0) * 4, cudaMemcpyDeviceToHost, hs.d2h);
-        }
+        // out[i0, h) and out[h, i1): h on the G grid near the A window's share
+        const uint64_t h = std::min(i1, i0 + (j1 - j0 + G / 2) / G * G) - i0;
+        d2h_copy(out + i0, dO, h * sizeof(K));
+        if (HAS_V) d2h_copy(outv + i0, dOv, h * 4);
+        d2h_copy(out + i0 + h, dO + h, (i1 - i0 - h) * sizeof(K));
+        if (HAS_V) d2h_copy(outv + i0 + h, dOv + h, (i1 - i0 - h) * 4);
         *d2h += (i1 - i0) * (sizeof(K) + (HAS_V ? 4 : 0));
         cudaEventRecord(hs.out_done[sl], hs.d2h);
+        if (trace) cudaEventRecord(tev[4 * c + 3], hs.d2h);
     }
     cudaEventRecord(hs.t1, hs.comp);
     cudaEventRecord(hs.in_done[0], hs.d2h);  // free the staging after the last copy-out
@@ -774,6 +791,15 @@ int merge_host_pipeline(const K* a, const uint32_t* av, uint64_t m, const K* b,
     e = cudaStreamSynchronize(hs.d2h);
     if (e == cudaSuccess) e = cudaStreamSynchronize(hs.comp);
     if (e != cudaSuccess) return cuda_fail(e, "comerge: host pipeline");
+    if (trace) {
+        for (uint64_t c = 0; c < nchunks; ++c) {
+            float t[4];
+            for (int q = 0; q < 4; ++q) cudaEventElapsedTime(&t[q], tev[0], tev[4 * c + q]);
+            std::fprintf(stderr, "chunk %2llu  h2d %8.1f -> %8.1f  merged %8.1f  d2h done %8.1f us\n",
+                         (unsigned long long)c, 1e3 * t[0], 1e3 * t[1], 1e3 * t[2], 1e3 * t[3]);
+        }
+        for (auto& ev : tev) cudaEventDestroy(ev);
+    }
     if (rc) return rc;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, hs.t0, hs.t1);

@@ -380,6 +380,30 @@ def test_host_buffers_pipelined(cuda, port):
         assert np.array_equal(ok, ek) and np.array_equal(ov, ev)
 
 
+def test_host_pipeline_aligned_windows(cuda, port):
+    """The host pipeline copies 256-byte aligned supersets of each chunk's
+    windows and merges the chunk as an output range: chunk boundaries in the
+    middle of duplicate runs, empty windows, skewed sides, 64-bit keys with
+    payloads, and host arrays that are not 256-byte aligned (offset views)."""
+    rng = np.random.default_rng(2024)
+    cases = [(np.int32, 2_500_003, 1_700_001, 3), (np.int32, 4_000_000, 9, 0),
+             (np.int32, 5, 3_000_000, 1 << 20), (np.uint64, 1_100_000, 1_300_007, 2),
+             (np.uint64, 2_000_000, 2_000_000, 0)]
+    for dt, m, n, alphabet in cases:
+        for shift in (0, 1, 3):
+            a = _draw(rng, dt, m + shift, alphabet)[shift:]
+            b = _draw(rng, dt, n + 1, alphabet)[1:] if shift else _draw(rng, dt, n, alphabet)
+            av, bv = tagged(m, n)
+            ek, ev = port.merge(a, b, av, bv)
+            ok = np.empty(m + n + shift, dt)[shift:]
+            ov = np.empty(m + n + 2, np.uint32)[2:] if shift else np.empty(m + n, np.uint32)
+            P().merge_pairs(a, av, b, bv, ok, ov)
+            assert np.array_equal(ok, ek) and np.array_equal(ov, ev), (dt, m, n, shift)
+            out = np.empty(m + n, dt)
+            P().merge_parallel(a, b, out, 4)
+            assert np.array_equal(out, ek), (dt, m, n, shift)
+
+
 def test_host_pipeline_report_matches_reference_stats(cuda, port):
     """merge_report.corank_iterations of the host pipeline = Algorithm 1's."""
     rng = np.random.default_rng(5)

@@ -6,9 +6,22 @@ import bench
 import paper_1303_4312_b200._native as N
 dev = torch.device("cuda:0")
 inp = bench.make_inputs("C2", device=dev)
-pin = {k: v.cpu().pin_memory() for k, v in inp.items()}
 tot = inp["a"].numel() + inp["b"].numel()
-ok = torch.empty(tot, dtype=torch.int32).pin_memory(); ov = torch.empty(tot, dtype=torch.uint32).pin_memory()
+if os.environ.get("HOSTALLOC"):  # cudaHostAlloc'd host arrays instead of torch's pinned allocator
+    import numpy as np
+    rt = C.CDLL("libcudart.so.12")
+    def halloc(n, dt):
+        p_ = C.c_void_p()
+        assert rt.cudaHostAlloc(C.byref(p_), C.c_size_t(n * 4), 0) == 0
+        arr = np.ctypeslib.as_array(C.cast(p_, C.POINTER(C.c_uint32)), shape=(n,))
+        return torch.from_numpy(arr).view(dt)
+    pin = {}
+    for k, v in inp.items():
+        pin[k] = halloc(v.numel(), v.dtype); pin[k].copy_(v.cpu())
+    ok = halloc(tot, torch.int32); ov = halloc(tot, torch.uint32)
+else:
+    pin = {k: v.cpu().pin_memory() for k, v in inp.items()}
+    ok = torch.empty(tot, dtype=torch.int32).pin_memory(); ov = torch.empty(tot, dtype=torch.uint32).pin_memory()
 p = lambda t: C.c_void_p(t.data_ptr())
 rep = N.MergeReport()
 def call():
