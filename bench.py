@@ -443,9 +443,11 @@ def e2e_measure(cfg, inp, steps, warmup):
     # the e2e result must equal the device-path result
     dev_keys = run_config(cfg, inp)["keys"].cpu()
     assert bool((ok.view(torch.uint8) == dev_keys.view(torch.uint8)).all()), "e2e mismatch"
-    return dict(value=total / statistics.mean(times), unit="elements/s",
+    # median call: one slow call (a PCIe hiccup, seen up to +20%) would move a
+    # mean of a handful of calls by several percent
+    return dict(value=total / statistics.median(times), unit="elements/s", stat=f"median of {steps} calls",
                 h2d_bytes_per_step=int(rep.h2d_bytes), d2h_bytes_per_step=int(rep.d2h_bytes),
-                ms_per_step=1e3 * statistics.mean(times),
+                ms_per_step=1e3 * statistics.median(times),
                 path=f"comerge_merge_parallel{'_pairs' if c['kind'] == 'pairs' else ''}_{suf} "
                      "(host pinned buffers)")
 
@@ -596,7 +598,7 @@ def main():
             torch.cuda.empty_cache()
 
     sorts = None if args.only_headline else sort_extras(device)
-    e2e = None if args.no_e2e or rank != 0 else e2e_measure(cfg, res["inp"], min(args.steps, 5), 1)
+    e2e = None if args.no_e2e or rank != 0 else e2e_measure(cfg, res["inp"], max(5, min(args.steps, 9)), 1)
     cpu = None if args.no_cpu or rank != 0 else cpu_baseline(cfg, res["inp"])
     if rank == 0:
         line = dict(

@@ -39,6 +39,7 @@
 #include "corank.cuh"
 #include "merge_stream.cuh"
 #include "merge_tile.cuh"
+#include "merge_serial.cuh"
 
 namespace comerge_b200 {
 
@@ -105,6 +106,10 @@ struct pipe_layout {
     // segmented batches: the tile's segment-end table (window-relative
     // x1 | y1 << 16 of segments s0 .. s0+SEGCAP-1), written by the producer warp
     static constexpr int SEGCAP = 512;
+    // more segments than this in a tile (average under ~8 VT outputs each, so
+    // many warps hold a thread crossing two segment ends):
+    // consumers use the general per-step segment test instead of the lean loop
+    static constexpr int kLeanSegs = T / (8 * VT);
     static constexpr bool kSeg = SEG == 1 || SEG == 2;  // segmented modes
     static constexpr size_t kStageOffs = kSeg ? size_t(SEGCAP) * 4 : 0;
     static constexpr size_t kStage = kStageKeys + kStageVals + kStageOffs;
@@ -578,7 +583,7 @@ __device__ __forceinline__ void merge_thread_segends(const K* sA, const K* sB, i
         --rem;
         const bool take_b = ib < y1 && (ia >= x1 || kb < ka);
         keys[v] = take_b ? kb : ka;
-        if constexpr (TRACK) src[v] = take_b ? (uint32_t(ib) | 0x80000000u) : uint32_t(ia);
+        if constexpr (TRACK) src[v] = smem_addr(take_b ? sB + ib : sA + ia);
         if (take_b) {
             ++ib;
             kb = kb1;
@@ -1151,37 +1156,48 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         K keys[VT];
         uint32_t src[VT];
         const unsigned long long p0 = args.trace && tid == 0 ? globaltimer_ns() : 0;
+        const K* sA = sk + a_off;
+        const K* sB = sk + b_base + b_off;
         if constexpr (SEGM) {
             const uint64_t k0 = mt[1];
             const uint64_t s_lo = mt[4], s_hi = mt[5];
             if (SEG == 2 && s_lo == s_hi) {  // merge pass, one segment: a plain merge
-                merge_thread<K, VT, HAS_V>(sk + a_off, a_len, sk + b_base + b_off, b_len, diag,
-                                           keys, src);
+                merge_thread_lean<K, VT, HAS_V>(sA, a_len, sB, b_len, diag, keys, src);
             } else if (mt[6]) {  // the producer's segment-end table
                 const uint32_t* se = reinterpret_cast<const uint32_t*>(stage + L::kStageKeys +
                                                                        L::kStageVals);
-                merge_thread_segends<K, VT, HAS_V>(sk + a_off, sk + b_base + b_off, diag, se,
-                                                   int(s_hi - s_lo) + 1, keys, src);
+                const int nse = int(s_hi - s_lo) + 1;
+                // tiles of many short segments (threads cross several segment
+                // ends): the per-step segment test of merge_thread_segends;
+                // otherwise the lean loop (a tile-uniform choice: no divergence)
+                if (nse > L::kLeanSegs)
+                    merge_thread_segends<K, VT, HAS_V>(sA, sB, diag, se, nse, keys, src);
+                else
+                    merge_thread_segends_lean<K, VT, HAS_V>(sA, sB, diag, se, nse, keys, src);
             } else if constexpr (!HAS_V) {
                 const seg_offsets off{args.aoff, args.boff};
-                merge_thread_seg<K, VT>(sk + a_off, a_len, sk + b_base + b_off, b_len, diag, i0,
-                                        i0 - k0, k0, s_lo, s_hi, off, keys);
+                merge_thread_seg<K, VT>(sA, a_len, sB, b_len, diag, i0, i0 - k0, k0, s_lo, s_hi,
+                                        off, keys);
             } else {
                 __trap();  // merge passes have at most a few segments per tile
             }
         } else {
-            merge_thread<K, VT, HAS_V>(sk + a_off, a_len, sk + b_base + b_off, b_len, diag, keys,
-                                       src);
+            merge_thread_lean<K, VT, HAS_V>(sA, a_len, sB, b_len, diag, keys, src);
         }
-        if constexpr (HAS_V) {
+        if constexpr (HAS_V) {  // source element address -> its payload
             const int bv_base = (av_off + a_len + 3) / 4 * 4;
             const int bv_off = int(mt[1] & 3);
             const uint32_t* sav = sv + av_off;
             const uint32_t* sbv = sv + bv_base + bv_off;
+            const uint32_t aA = smem_addr(sA), aB = smem_addr(sB);
+            constexpr int SH = sizeof(K) == 8 ? 3 : 2;
 #pragma unroll
             for (int v = 0; v < VT; ++v)
-                if (diag + v < len)
-                    src[v] = (src[v] & 0x80000000u) ? sbv[src[v] & 0x7fffffffu] : sav[src[v]];
+                if (diag + v < len) {
+                    const bool isb = src[v] >= aB;
+                    const int x = int((src[v] - (isb ? aB : aA)) >> SH);
+                    src[v] = isb ? sbv[x] : sav[x];
+                }
         }
         const unsigned long long p1 = args.trace && tid == 0 ? globaltimer_ns() : 0;
         named_bar_sync(1, NC);  // every thread is done reading the windows

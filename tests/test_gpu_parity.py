@@ -251,6 +251,29 @@ def test_random_segmented(cuda, path, port):
             assert np.array_equal(host(out), port.merge_segmented(a, ao, b, bo)), (nseg, maxlen)
 
 
+def test_segmented_short_segments_inside_long(cuda, path, port):
+    """Tiles of few segments where some threads' outputs still cross one, two
+    or many segment ends (clusters of 0-6 element pairs between long pairs):
+    the consumers' lean loop, its one-switch form and the rolled fallback."""
+    rng = np.random.default_rng(4242)
+    for dt in (np.int32, np.uint32):
+        ma, nb = [], []
+        for _ in range(60):
+            ma.append(int(rng.integers(1000, 9000)))
+            nb.append(int(rng.integers(0, 9000)))
+            for _ in range(int(rng.integers(0, 12))):
+                ma.append(int(rng.integers(0, 4)))
+                nb.append(int(rng.integers(0, 4)))
+        ma, nb = np.array(ma), np.array(nb)
+        a = np.concatenate([_draw(rng, dt, int(x), 50) for x in ma])
+        b = np.concatenate([_draw(rng, dt, int(x), 50) for x in nb])
+        ao = np.concatenate([[0], np.cumsum(ma)]).astype(np.uint64)
+        bo = np.concatenate([[0], np.cumsum(nb)]).astype(np.uint64)
+        out = P().merge_segmented(dev(a, cuda), dev(ao, cuda), dev(b, cuda), dev(bo, cuda))
+        torch.cuda.synchronize()
+        assert np.array_equal(host(out), port.merge_segmented(a, ao, b, bo)), dt
+
+
 def test_co_rank_split_equals_reference_search(cuda, path, port):
     """The partition's one-sided search returns Algorithm 1's split (Lemma 1)."""
     rng = np.random.default_rng(3)

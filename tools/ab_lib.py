@@ -1,0 +1,30 @@
+"""Kernel time per config for the library at COMERGE_LIB_PATH (A/B of build
+variants: run once per variant).   python tools/ab_lib.py NAME C1,C2,... [--steps 20]"""
+import argparse
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("name")
+    ap.add_argument("configs")
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--rounds", type=int, default=2)
+    args = ap.parse_args()
+    import torch
+    import bench
+    bench.CONFIGS.update(bench.EXTRA)
+    dev = torch.device("cuda:0")
+    for cfg in args.configs.split(","):
+        r = [statistics.mean(bench.time_config(cfg, args.steps, 3, dev)["kern_ms"]) * 1e3
+             for _ in range(args.rounds)]
+        print(f"{args.name:8s} {cfg:4s} kernel us {min(r):8.1f}  (rounds {[round(x, 1) for x in r]})",
+              flush=True)
+
+
+if __name__ == "__main__":
+    main()
