@@ -670,20 +670,28 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             e ^= tail_hash(lc, 0x5eedull, 0, 0);
         }
         scratch[38] = e;
+        // pull this CTA's share of an array into L2 (cp.async.bulk.prefetch)
+        auto pull = [&](const void* base, uint64_t len, uint32_t esz) {
+            const uint64_t x0 = len * c / G, x1 = len * (c + 1) / G;
+            uint64_t b0 = (x0 * esz) & ~uint64_t(15), b1 = (x1 * esz) & ~uint64_t(15);
+            const unsigned char* p = static_cast<const unsigned char*>(base);
+            while (b1 > b0) {
+                const uint64_t chunk = b1 - b0 < (uint64_t(1) << 20) ? b1 - b0 : (uint64_t(1) << 20);
+                prefetch_l2(p + b0, uint32_t(chunk));
+                b0 += chunk;
+            }
+        };
+        if (SEG == 1 && !(args.flags & 8192u)) {
+            // segmented batches: the segment offsets (16 B per pair, a few
+            // hundred bytes per CTA) go to L2 at once; every start-up boundary
+            // search probes them first, so its later segment rounds hit L2
+            pull(args.aoff, args.nseg + 1, 8);
+            pull(args.boff, args.nseg + 1, 8);
+        }
         if (SEG == 0 && args.eager_start && !(args.flags & 4096u)) {
             // small inputs: pull this CTA's share of A and B (and payloads) into
             // L2 at once, so the start-up co-rank rounds and the first window
             // loads run at L2 instead of HBM latency
-            auto pull = [&](const void* base, uint64_t len, uint32_t esz) {
-                const uint64_t x0 = len * c / G, x1 = len * (c + 1) / G;
-                uint64_t b0 = (x0 * esz) & ~uint64_t(15), b1 = (x1 * esz) & ~uint64_t(15);
-                const unsigned char* p = static_cast<const unsigned char*>(base);
-                while (b1 > b0) {
-                    const uint64_t chunk = b1 - b0 < (uint64_t(1) << 20) ? b1 - b0 : (uint64_t(1) << 20);
-                    prefetch_l2(p + b0, uint32_t(chunk));
-                    b0 += chunk;
-                }
-            };
             if (m) pull(args.a, m, sizeof(K));
             if (n) pull(args.b, n, sizeof(K));
             if (HAS_V && m) pull(args.av, m, 4);
