@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--static-pct", type=int, default=0)
+    ap.add_argument("--lookahead", default="0", help="comma list: A/B the tail look-ahead instead of flags")
     args = ap.parse_args()
     import torch
     import bench
@@ -24,15 +25,21 @@ def main():
     bench.CONFIGS.update(bench.EXTRA)
     dev = torch.device("cuda:0")
     flags = [int(x) for x in args.flags.split(",")]
+    las = [int(x) for x in args.lookahead.split(",")]
+    if len(las) > 1:  # A/B the look-ahead at flags[0]
+        flags = las
     res = {f: [] for f in flags}
     for r in range(args.rounds):
         for f in flags:
-            N.lib.comerge_cuda_set_tuning(args.static_pct, f, 0)
+            if len(las) > 1:
+                N.lib.comerge_cuda_set_tuning(args.static_pct, int(args.flags.split(",")[0]), f)
+            else:
+                N.lib.comerge_cuda_set_tuning(args.static_pct, f, las[0])
             t = bench.time_config(args.config, args.steps, 3, dev)
             res[f].append(statistics.mean(t["kern_ms"]) * 1e3)
     N.lib.comerge_cuda_set_tuning(0, 0, 0)
     for f in flags:
-        print(f"{args.config} flags={f}: kernel us per round {[round(x, 1) for x in res[f]]} "
+        print(f"{args.config} {'lookahead' if len(las) > 1 else 'flags'}={f}: kernel us per round {[round(x, 1) for x in res[f]]} "
               f"mean {statistics.mean(res[f]):.1f}")
 
 
