@@ -80,9 +80,11 @@ int comerge_cuda_last_path(void);
  * host memory over PCIe), 2 = plain staging (copy in, merge, copy out). */
 void comerge_cuda_set_host_mode(int mode);
 /* Debug tracing of the persistent kernels: when non-NULL (at least
- * 12*4096 uint64), CTA c writes %globaltimer stamps and counters to
- * device_buffer[8c .. 8c+7] and consumer phase sums to
- * device_buffer[8*4096 + 4c ..].  NULL disables. */
+ * 20*4096 uint64), CTA c writes %globaltimer stamps and counters to
+ * device_buffer[8c .. 8c+7], consumer phase sums to
+ * device_buffer[8*4096 + 4c ..], producer starvation (static range / tail)
+ * to device_buffer[12*4096 + 4c ..] and scheduler tail counters to
+ * device_buffer[16*4096 + 4c ..].  NULL disables. */
 void comerge_cuda_set_trace(unsigned long long* device_buffer);
 /* Tuning knobs of the tile pipeline (benchmarking only; 0 = default): the
  * statically assigned share of tiles in percent (default 70; the rest is the

@@ -429,13 +429,19 @@ __device__ __forceinline__ void ld_pair(const uint64_t* p, uint64_t& x, uint64_t
                  : "memory");
 }
 
-// Claim the next tail tile index (0-based) of this launch.
-__device__ __forceinline__ uint64_t tail_claim(uint64_t* tail, uint64_t epoch) {
-    uint64_t tag, cnt;
-    ld_pair(tail, tag, cnt);
-    if (tag != epoch) {
-        uint64_t dt, dc;
-        cas128(tail, tag, cnt, epoch, 0, dt, dc);  // first claimer of this launch resets
+// Claim the next tail tile index (0-based) of this launch.  `checked`: this
+// caller has already seen the counter carry this launch's tag (it cannot
+// change again within the launch), so the claim is one atomic round trip
+// instead of a tag read followed by the atomic.
+__device__ __forceinline__ uint64_t tail_claim(uint64_t* tail, uint64_t epoch, bool& checked) {
+    if (!checked) {
+        uint64_t tag, cnt;
+        ld_pair(tail, tag, cnt);
+        if (tag != epoch) {
+            uint64_t dt, dc;
+            cas128(tail, tag, cnt, epoch, 0, dt, dc);  // first claimer of this launch resets
+        }
+        checked = true;
     }
     return atomicAdd(reinterpret_cast<unsigned long long*>(tail + 1), 1ull);
 }
@@ -698,6 +704,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             if (HAS_V && n) pull(args.bv, n, 4);
         }
         mbar_fence_init();
+        __threadfence_block();
     }
     // ---- start-up: this worker's static range [ts0, te0), an equal share of
     // the first NS tiles, then co-rank its start with one warp (33-ary; few
@@ -717,6 +724,42 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
     // searches concurrently (boundary w is in [lo, hi + (i_w - i_0)])
     const bool split_start = SEG == 0 && !args.eager_start && known > 0 && !(args.flags & 1u);
     constexpr int kSplitBar = 32 * (L::kCW + 1);
+    if (warp == 0) {  // thread 0's initialisation (the tail epoch) is done
+        __syncwarp();
+        named_bar_arrive(5, 64);
+    }
+    if (warp == W_TAIL) {
+        // ------------------------------------------------------ tail warp
+        // (takes no part in the start-up: it starts at once, with the epoch
+        // handed over by warp 0 on named barrier 5, so its full-diagonal
+        // searches finish ~the start-up's length earlier -- on C2 the first
+        // tail claims otherwise found their slots unpublished)
+        named_bar_sync(5, 64);
+        const uint64_t epoch = scratch[38];
+        // co-rank the tail boundaries q = c, c+G, ... (in passes of up to 32,
+        // lane groups, full-diagonal brackets) and publish them
+        // slots 0 .. nq-1; boundary NT is trivial for a whole merge, else co-ranked too
+        const uint64_t nq = NT > NS ? NT - NS + (out_end < total ? 1 : 0) : 0;
+        for (uint64_t q0 = c; q0 < nq; q0 += 32 * uint64_t(G)) {
+            uint64_t left = (nq - q0 + G - 1) / G;
+            const int k = int(left < 32 ? left : 32);
+            const int P = pow2_group(k);
+            const int g = lane / P;
+            const uint64_t q = q0 + uint64_t(g < k ? g : k - 1) * G;
+            const uint64_t i = diag_of(NS + q);
+            uint64_t lo, hi;
+            full_bracket(i, lo, hi);
+            const boundary bd = find_boundary<K, SEG>(args, i, lo, hi, 0, P, nullptr);
+            if (lane % P == 0 && g < k) {
+                uint64_t* slot = args.tail + kTailSlots + 4 * q;
+                st_pair(slot, bd.j, bd.s);
+                st_pair(slot + 2, tail_hash(epoch, q, bd.j, bd.s), 0);
+            }
+        }
+        if (args.trace && lane == 0) args.trace[16 * 4096 + 4 * c + 1] = globaltimer_ns();
+        return;
+    }
+
     if (warp == W_SCHED) {
         if (te0 > ts0) {
             const uint64_t i = diag_of(ts0);
@@ -763,7 +806,8 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             }
         }
     }
-    __syncthreads();
+    constexpr int kStartBar = L::kThreads - 32;  // every warp but the tail warp
+    named_bar_sync(4, kStartBar);
     if (!split_start && !args.eager_start && known > 0) {
         // segmented batches: boundaries ts0+1 .. ts0+known bracketed by the start
         if (warp < known) {
@@ -777,38 +821,13 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
                 scratch[11 + warp] = bd.s;
             }
         }
-        __syncthreads();
+        named_bar_sync(4, kStartBar);
     }
     if (args.trace && tid == 0) args.trace[8 * c + 5] = globaltimer_ns();
     const uint64_t epoch = scratch[38];  // written by thread 0 before the start-up barriers
-    if (warp == W_TAIL) {
-        // ------------------------------------------------------ tail warp
-        // co-rank the tail boundaries q = c, c+G, ... (in passes of up to 32,
-        // lane groups, full-diagonal brackets) and publish them
-        // slots 0 .. nq-1; boundary NT is trivial for a whole merge, else co-ranked too
-        const uint64_t nq = NT > NS ? NT - NS + (out_end < total ? 1 : 0) : 0;
-        for (uint64_t q0 = c; q0 < nq; q0 += 32 * uint64_t(G)) {
-            uint64_t left = (nq - q0 + G - 1) / G;
-            const int k = int(left < 32 ? left : 32);
-            const int P = pow2_group(k);
-            const int g = lane / P;
-            const uint64_t q = q0 + uint64_t(g < k ? g : k - 1) * G;
-            const uint64_t i = diag_of(NS + q);
-            uint64_t lo, hi;
-            full_bracket(i, lo, hi);
-            const boundary bd = find_boundary<K, SEG>(args, i, lo, hi, 0, P, nullptr);
-            if (lane % P == 0 && g < k) {
-                uint64_t* slot = args.tail + kTailSlots + 4 * q;
-                st_pair(slot, bd.j, bd.s);
-                st_pair(slot + 2, tail_hash(epoch, q, bd.j, bd.s), 0);
-            }
-        }
-        return;
-    }
-
     if (warp == W_SCHED) {
         // ------------------------------------------------------ scheduler
-        uint32_t n_rounds = 0, n_claims = 0;
+        uint32_t n_rounds = 0, n_claims = 0, n_fallback = 0;
         unsigned long long t_search = 0;
         // at most `ahead` tiles co-ranked beyond the producer, in passes of at
         // most 8: the probes' sectors are then still in L2 when the tile's
@@ -887,37 +906,46 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         // co-ranked in the background by the tail warps (slot q = boundary
         // NS + q), a slot not yet valid is co-ranked here instead.
         if (NS < NT) {
+            bool tag_seen = false;  // lane 0: the tail counter carries this launch's tag
             for (;;) {
                 while (*pushed - *issued >= args.lookahead) __nanosleep(500);
                 uint64_t q = 0;
                 if (lane == 0) {
-                    q = tail_claim(args.tail, epoch);
+                    q = tail_claim(args.tail, epoch, tag_seen);
                     if (q == NT - NS + G - 1)  // the launch's last claim: next launch, new epoch
                         atomicAdd(reinterpret_cast<unsigned long long*>(args.tail + 4), 1ull);
                 }
                 q = __shfl_sync(0xffffffffu, q, 0);
                 if (NS + q >= NT) break;
+                if (args.trace && lane == 0 && n_claims == 0)
+                    args.trace[16 * 4096 + 4 * c + 2] = globaltimer_ns();  // first tail claim
                 ++n_claims;
+                // both boundaries' slots in one round trip: lane e (< 2) loads
+                // slot q + e (the tile's start and end), the warp validates
+                const uint64_t qq = q + uint64_t(lane & 1);
+                boundary bd{m, SEGM ? args.nseg - 1 : 0};  // the last boundary is (m, n)
+                bool ok = NS + qq == NT && out_end == total;
+                if (!ok && lane < 2) {
+                    const uint64_t* slot = args.tail + kTailSlots + 4 * qq;
+                    uint64_t tag, pad;
+                    ld_pair(slot, bd.j, bd.s);
+                    ld_pair(slot + 2, tag, pad);
+                    ok = tag == tail_hash(epoch, qq, bd.j, bd.s);
+                }
                 boundary bb[2];
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
-                    const uint64_t qq = q + e;
-                    const uint64_t i = diag_of(NS + qq);
-                    boundary bd{m, SEGM ? args.nseg - 1 : 0};  // the last boundary is (m, n)
-                    bool ok = NS + qq == NT && out_end == total;
-                    if (!ok) {
-                        const uint64_t* slot = args.tail + kTailSlots + 4 * qq;
-                        uint64_t tag, pad;
-                        ld_pair(slot, bd.j, bd.s);
-                        ld_pair(slot + 2, tag, pad);
-                        ok = tag == tail_hash(epoch, qq, bd.j, bd.s);
-                    }
-                    if (!__shfl_sync(0xffffffffu, ok, 0)) {
+                    bb[e] = shfl_b(bd, e);
+                    if (!__shfl_sync(0xffffffffu, ok, e)) {  // not published yet: co-rank here
+                        if (args.trace && lane == 0) {
+                            ++n_fallback;
+                            args.trace[16 * 4096 + 4 * c + 3] = NS + q + e;  // the last one
+                        }
+                        const uint64_t i = diag_of(NS + q + e);
                         uint64_t lo, hi;
                         full_bracket(i, lo, hi);
-                        bd = find_boundary<K, SEG>(args, i, lo, hi, 0, 32, &n_rounds);
+                        bb[e] = shfl_b(find_boundary<K, SEG>(args, i, lo, hi, 0, 32, &n_rounds), 0);
                     }
-                    bb[e] = shfl_b(bd, 0);
                 }
                 push(NS + q, 1, bb[0], bb[1]);
             }
@@ -925,6 +953,7 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         if (args.trace && lane == 0) {
             args.trace[8 * c + 1] = (uint64_t(n_claims) << 48) | (uint64_t(n_rounds) << 32) |
                                     (t_search / 1000);  // claims | rounds | search us
+            args.trace[16 * 4096 + 4 * c] = n_fallback;  // tail slots co-ranked here
         }
         // end marker
         {
@@ -996,7 +1025,16 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             if (*pushed <= s) {
                 const unsigned long long w0 = args.trace ? globaltimer_ns() : 0;
                 while (*pushed <= s) __nanosleep(200);
-                if (args.trace) starve += globaltimer_ns() - w0;
+                if (args.trace) {
+                    const unsigned long long w = globaltimer_ns() - w0;
+                    starve += w;
+                    // trace region 3 (4 u64 per CTA): starved ns in the static
+                    // range, in the dynamic tail, and the count of waits of each
+                    unsigned long long* r3 = args.trace + 12 * 4096 + 4 * c;
+                    const bool in_tail = uint64_t(s) >= te0 - ts0;
+                    r3[in_tail ? 1 : 0] += w;
+                    r3[in_tail ? 3 : 2] += 1;
+                }
             }
             __threadfence_block();
             const uint64_t* d = desc + 8 * (s % NB);

@@ -21,10 +21,10 @@ int main(int argc, char** argv) {
     comerge_testkit_generate_sorted(COMERGE_KEY_I32, 1, 1, n, 16, b, 0);
     size_t wsb = comerge_cuda_merge_workspace_bytes(m, n, COMERGE_KEY_I32, 1);
     void* ws; cudaMalloc(&ws, wsb);
-    unsigned long long *tr, *mk; cudaMalloc(&tr, 16 * 4096 * 8); cudaMalloc(&mk, 64);
+    unsigned long long *tr, *mk; cudaMalloc(&tr, 20 * 4096 * 8); cudaMalloc(&mk, 64);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     for (int r = 0; r < 6; ++r) {
-        cudaMemset(tr, 0, 16 * 4096 * 8);
+        cudaMemset(tr, 0, 20 * 4096 * 8);
         comerge_cuda_set_trace(tr);
         cudaEventRecord(e0);
         marker<<<1, 1>>>(mk);

@@ -34,7 +34,7 @@ def main():
     P.set_kernel_path(args.path)
     N.lib.comerge_cuda_set_tuning(args.static_pct, args.flags, args.lookahead)
     flush = torch.empty(512 * 2**20 // 4, dtype=torch.int32, device=dev)
-    trace = torch.zeros(16 * 4096, dtype=torch.int64, device=dev) if args.trace else None
+    trace = torch.zeros(20 * 4096, dtype=torch.int64, device=dev) if args.trace else None
     for r in range(args.reps):
         flush.fill_(r)
         if trace is not None and r == args.reps - 1:
@@ -73,6 +73,16 @@ def main():
         print("  consumer us: merge", q(ext[:, 0]), "bar1", q(ext[:, 1]), "stage+bar2", q(ext[:, 2]))
         print("  stores drained after consumer end us", q((ext_raw[:, 3] - full[:, 3]).double() / 1e3))
         print("  producer starved us", q(full[:, 6].double() / 1e3))
+        r3 = trace[12 * 4096: 12 * 4096 + 4 * 4096].view(-1, 4).cpu()[live]
+        print("    static range us", q(r3[:, 0].double() / 1e3), "waits", q(r3[:, 2].double()),
+              "| tail us", q(r3[:, 1].double() / 1e3), "waits", q(r3[:, 3].double()))
+        r4 = trace[16 * 4096: 16 * 4096 + 4 * 4096].view(-1, 4).cpu()[live]
+        print("  tail slots co-ranked by the scheduler (not yet published)", q(r4[:, 0].double()),
+              "tail warp done us", q((r4[:, 1] - t0).double() / 1e3),
+              "first tail claim us", q((r4[:, 2] - t0).double() / 1e3))
+        fb = r4[:, 0] > 0
+        if fb.any():
+            print("  last fallback tile index (of NT)", q(r4[fb, 3].double()))
         print("  consumer data-wait us", q(full[:, 7].double() / 1e3))
         print("  slowest 12 (cta, smid, us):",
               [(int(i), int(sm[i]), round(float(dur[i]), 1)) for i in order[-12:]])
