@@ -698,10 +698,15 @@ int merge_host_pipeline(const K* a, const uint32_t* av, uint64_t m, const K* b,
     const uint64_t nchunks = cuts.size() - 1;
     uint64_t chunk = 0;
     for (uint64_t c = 0; c < nchunks; ++c) chunk = std::max(chunk, cuts[c + 1] - cuts[c]);
-    // chunk boundaries: the Lemma-1 split of every chunk start, on host data
+    // chunk boundaries: the Lemma-1 split of every chunk start, on host data,
+    // each computed just before its chunk is enqueued (the host's cache-missing
+    // probes then overlap the copies already running)
     std::vector<uint64_t> js(nchunks + 1);
-    for (uint64_t c = 0; c <= nchunks; ++c)
-        js[c] = co_rank_split<K, uint64_t>(cuts[c], a, m, b, n, [](const K* p) { return *p; });
+    auto split = [&](uint64_t i) {
+        return co_rank_split<K, uint64_t>(i, a, m, b, n, [](const K* p) { return *p; });
+    };
+    js[0] = 0;
+    js[nchunks] = m;
     // three slots of device windows (A, B, out [+ payloads]) from the pool;
     // an input window is copied from its G-aligned start, so it holds up to
     // G - 1 leading elements of the previous chunk (+ G of end round-up)
@@ -741,6 +746,7 @@ int merge_host_pipeline(const K* a, const uint32_t* av, uint64_t m, const K* b,
         uint32_t* dBv = reinterpret_cast<uint32_t*>(base + 3 * kb + vb);
         uint32_t* dOv = reinterpret_cast<uint32_t*>(base + 3 * kb + 2 * vb);
         const uint64_t i0 = cuts[c], i1 = cuts[c + 1];
+        if (c + 1 < nchunks) js[c + 1] = split(i1);
         const uint64_t j0 = js[c], j1 = js[c + 1], k0 = i0 - j0, k1 = i1 - j1;
         // aligned input windows A[sa, ea) ⊇ A[j0, j1), B[sb, eb) ⊇ B[k0, k1)
         const uint64_t sa = j0 / G * G, ea = std::min(m, div_up(j1, G) * G);
