@@ -920,3 +920,56 @@ def test_merge_pieces_large_range_with_dynamic_tail(cuda, port, dt):
         out = P().merge_pieces(pa, pb, lo, hi)
         torch.cuda.synchronize()
         assert np.array_equal(host(out), expect[lo:hi]), (lo, hi)
+
+
+def test_concurrent_streams_and_host_threads(cuda, port):
+    """Reentrancy (async on the caller's stream, reentrant across
+    streams, no global mutable state): 4 host threads, each on its own CUDA
+    stream, interleave device key-value merges (tile pipeline with dynamic
+    tails running concurrently, scratch from the private pool), segmented
+    batches and host-buffer merges (the chunked H2D/merge/D2H pipeline);
+    every result bit-exact against the oracle."""
+    import threading
+    rng = np.random.default_rng(777)
+    cases = []
+    for t in range(4):
+        m, n = int(rng.integers(300_000, 2_500_000)), int(rng.integers(300_000, 2_500_000))
+        a = _draw(rng, np.int32, m, 1000 if t % 2 else 0)
+        b = _draw(rng, np.int32, n, 1000 if t % 2 else 0)
+        av, bv = tagged(m, n)
+        la, lb = rng.integers(0, 3000, 200), rng.integers(0, 3000, 200)
+        sa = np.concatenate([_draw(rng, np.int32, int(x), 1 << 20) for x in la])
+        sb = np.concatenate([_draw(rng, np.int32, int(x), 1 << 20) for x in lb])
+        ao = np.concatenate([[0], np.cumsum(la)]).astype(np.uint64)
+        bo = np.concatenate([[0], np.cumsum(lb)]).astype(np.uint64)
+        cases.append(dict(a=a, b=b, av=av, bv=bv, sa=sa, sb=sb, ao=ao, bo=bo,
+                          ek=port.merge(a, b, av, bv), es=port.merge_segmented(sa, ao, sb, bo)))
+    errors = []
+
+    def worker(t):
+        try:
+            c = cases[t]
+            s = torch.cuda.Stream(device=cuda)
+            with torch.cuda.stream(s):
+                ta, tb = dev(c["a"], cuda), dev(c["b"], cuda)
+                tav, tbv = dev(c["av"], cuda), dev(c["bv"], cuda)
+                ts = [dev(c[k], cuda) for k in ("sa", "ao", "sb", "bo")]
+                for _ in range(5):
+                    ok, ov = P().merge_pairs(ta, tav, tb, tbv)
+                    so = P().merge_segmented(*ts)
+                    hk = np.empty(len(c["a"]) + len(c["b"]), np.int32)
+                    P().merge_parallel(c["a"], c["b"], hk, 3)  # host buffers
+                    s.synchronize()
+                    assert np.array_equal(host(ok), c["ek"][0]), t
+                    assert np.array_equal(host(ov), c["ek"][1]), t
+                    assert np.array_equal(host(so), c["es"]), t
+                    assert np.array_equal(hk, c["ek"][0]), t
+        except Exception as e:  # noqa: BLE001 -- reported below
+            errors.append((t, repr(e)))
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
