@@ -263,6 +263,8 @@ int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const ui
     const uint64_t out_end = pieces ? pieces->out_end : total;
     const uint64_t ptiles = div_up(out_end - out_base, PL::T);
     if (ptiles == 0) return COMERGE_OK;
+    if (SEG == 2 && (run_len == 0 || (run_len & (run_len - 1))))
+        return fail(COMERGE_E_INVALID, "comerge: merge-pass run length must be a power of two");
     int limit = pipe_grid_limit<K, HAS_V, SEG>();
     if (limit > kMaxPipeGrid) limit = kMaxPipeGrid;
     const uint32_t grid = uint32_t(ptiles < uint64_t(limit) ? ptiles : uint64_t(limit));

@@ -240,6 +240,11 @@ __device__ __forceinline__ uint32_t stage_copy_plan(const E* __restrict__ src, u
     return uint32_t((hi_al - lo_al) * sizeof(E));
 }
 
+// merge-pass runs: L is a power of two (sort.cuh's base runs, doubled every
+// pass; checked at launch), so run arithmetic is shifts, not 64-bit divisions
+// (the producer lane stages every window through stage_runs)
+__device__ __forceinline__ int run_lg(uint64_t L) { return __ffsll((long long)L) - 1; }
+
 // Merge pass: stage the window [x0, x1) of one side's index space, element x
 // at src[x + (x/L + shift) * L] (shift 0 for A, 1 for B), as one TMA copy per
 // run it touches (runs are physically contiguous; L is a multiple of vece, so
@@ -253,10 +258,11 @@ __device__ __forceinline__ uint32_t stage_runs(const E* __restrict__ src, uint64
                                                uint64_t* bar, uint64_t policy) {
     uint32_t total = 0;
     const uint64_t base = x0 - x0 % vece;
+    const int lg = run_lg(L);
     for (uint64_t x = x0; x < x1;) {
-        const uint64_t run = x / L;
-        const uint64_t y = x1 < (run + 1) * L ? x1 : (run + 1) * L;
-        const uint64_t sh = (run + shift) * L;  // physical = index + sh
+        const uint64_t run = x >> lg;
+        const uint64_t y = x1 < ((run + 1) << lg) ? x1 : ((run + 1) << lg);
+        const uint64_t sh = (run + shift) << lg;  // physical = index + sh
         E* d = dst + ((x - x % vece) - base);
         if (!issue) {
             total += stage_copy_plan(src, phys_len, x + sh, y + sh, d, vece);
@@ -283,8 +289,10 @@ __device__ __forceinline__ uint64_t run_off(uint64_t s, uint64_t L, uint64_t len
     const uint64_t o = s * L;
     return o < len ? o : len;
 }
-__device__ __forceinline__ uint64_t run_pos_a(uint64_t x, uint64_t L) { return x + (x / L) * L; }
-__device__ __forceinline__ uint64_t run_pos_b(uint64_t y, uint64_t L) { return y + (y / L + 1) * L; }
+__device__ __forceinline__ uint64_t run_pos_a(uint64_t x, uint64_t L) { return x + (x & ~(L - 1)); }
+__device__ __forceinline__ uint64_t run_pos_b(uint64_t y, uint64_t L) {
+    return y + (y & ~(L - 1)) + L;
+}
 
 // SEG == 3: element x of a pieced input (linear scan: at most kMaxPieces)
 template <typename K>
@@ -360,7 +368,7 @@ __device__ __forceinline__ boundary find_boundary(const pipe_args& args, uint64_
     } else {
         if constexpr (SEG == 2) {  // merge pass: pair s holds output ranks [2sL, 2sL + 2L)
             const uint64_t L = args.run_len;
-            uint64_t s = i / (2 * L);
+            uint64_t s = i >> (run_lg(L) + 1);
             if (s > args.nseg - 1) s = args.nseg - 1;
             const uint64_t as = run_off(s, L, args.m), bs = run_off(s, L, args.n);
             const uint64_t ma = run_off(s + 1, L, args.m) - as, nb = run_off(s + 1, L, args.n) - bs;
