@@ -273,8 +273,15 @@ def time_config(cfg, steps, warmup, device, seed=SEED, dist_ctx=None, clocks=Fal
     total = inp["a"].numel() + inp["b"].numel()
     flush = torch.empty(512 * 2**20 // 4, dtype=torch.int32, device=device)
     stream = torch.cuda.current_stream(device)
-    for _ in range(max(warmup, 0)):
+    # warm-up steps are the timed step exactly (flush, events, merge), untimed:
+    # the first flush launch of a process otherwise lands in timed step 0
+    # (seen: +113 us on the first step of a fresh process, lazy module load)
+    wev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    for k in range(max(warmup, 0)):
+        flush.fill_(k)
+        wev[0].record(stream)
         run_config(cfg, inp, out)
+        wev[1].record(stream)
     torch.cuda.synchronize(device)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] + list(raw_events(2))
           for _ in range(steps)]

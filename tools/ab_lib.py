@@ -20,10 +20,13 @@ def main():
     bench.CONFIGS.update(bench.EXTRA)
     dev = torch.device("cuda:0")
     for cfg in args.configs.split(","):
-        r = [statistics.mean(bench.time_config(cfg, args.steps, 3, dev)["kern_ms"]) * 1e3
-             for _ in range(args.rounds)]
-        print(f"{args.name:8s} {cfg:4s} kernel us {min(r):8.1f}  (rounds {[round(x, 1) for x in r]})",
-              flush=True)
+        r, st = [], []
+        for _ in range(args.rounds):
+            t = bench.time_config(cfg, args.steps, 3, dev)
+            r.append(statistics.mean(t["kern_ms"]) * 1e3)
+            st.append(statistics.mean(t["step_ms"]) * 1e3)
+        print(f"{args.name:8s} {cfg:4s} kernel us {min(r):8.1f}  step us {min(st):8.1f}  "
+              f"(rounds {[round(x, 1) for x in r]})", flush=True)
 
 
 if __name__ == "__main__":
