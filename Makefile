@@ -40,8 +40,20 @@ $(LIB): $(OBJS)
 oracle:
 	$(MAKE) -C oracle
 
+# the library with device invariant checks (tile descriptors, segmented
+# splits; a violation traps): COMERGE_LIB_PATH=lib_var/dbg/libcomerge_cuda.so
+# runs any test or tool against it (compute-sanitizer is unavailable on the
+# GPU pool)
+DBG := lib_var/dbg/libcomerge_cuda.so
+debug-lib: $(DBG)
+$(DBG): $(SRCS) $(HDRS)
+	@mkdir -p lib_var/dbg
+	$(NVCC) $(NVFLAGS) -DCOMERGE_DEBUG_CHECKS=1 -c $(PKG)/csrc/comerge_cuda.cu -o lib_var/dbg/comerge_cuda.o
+	$(NVCC) $(NVFLAGS) -DCOMERGE_DEBUG_CHECKS=1 -c $(PKG)/csrc/testkit.cu -o lib_var/dbg/testkit.o
+	$(NVCC) $(ARCH) -shared -o $@ lib_var/dbg/comerge_cuda.o lib_var/dbg/testkit.o -lcudart
+
 clean:
 	rm -f $(PKG)/lib/*.o $(PKG)/lib/*.so $(PKG)/lib/*.ptxas.txt $(SHIM_TEST) $(CLI)
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle clean
+.PHONY: all oracle clean debug-lib

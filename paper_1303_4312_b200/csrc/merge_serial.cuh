@@ -24,6 +24,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 
 namespace comerge_b200 {
 
@@ -161,6 +162,16 @@ __device__ __forceinline__ void merge_thread_segends_lean(const K* sA, const K* 
     const int ia = x0 + smem_split<K>(sA + x0, x1 - x0, sB + y0, y1 - y0, dl);
     const int ib = y0 + (dl - (ia - x0));
     const int rem = (x1 - ia) + (y1 - ib);  // outputs left in segment k
+#ifdef COMERGE_DEBUG_CHECKS
+    // the segment-end table is monotone and the split lies inside segment k
+    if (!(x0 <= ia && ia <= x1 && y0 <= ib && ib <= y1 && x0 <= x1 && y0 <= y1 &&
+          (k + 1 >= nse || (int(se[k + 1] & 0xffffu) >= x1 && int(se[k + 1] >> 16) >= y1)) &&
+          (diag >= int(se[nse - 1] & 0xffffu) + int(se[nse - 1] >> 16) || rem > 0))) {
+        printf("comerge: bad segmented split diag %d k %d/%d x %d..%d..%d y %d..%d..%d\n", diag,
+               k, nse, x0, ia, x1, y0, ib, y1);
+        __trap();
+    }
+#endif
     const uint32_t a0 = smem_addr(sA), b0 = smem_addr(sB);
     constexpr uint32_t S = sizeof(K);
     if (rem >= VT || k == nse - 1) {  // no segment end inside (the common case)
