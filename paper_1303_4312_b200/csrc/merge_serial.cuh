@@ -18,7 +18,8 @@
 //
 // Segmented tiles: inside a segment it is the same loop with the segment's
 // window limits; a thread whose VT outputs cross one segment end switches the
-// limits at a fixed step (one compare and two predicated moves per step);
+// limits at a fixed step (one compare and two predicated moves per step; the
+// whole warp runs that loop when any of its lanes needs it);
 // threads crossing two or more segment ends (segments shorter than VT) run a
 // compact rolled loop through local memory.
 #pragma once
