@@ -1064,7 +1064,100 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
                 __threadfence_block();
                 *issued = s + 1;
             }
-            if constexpr (SEGM) {  // segment-end table (merge_thread_segends)
+            if (lane == 0) {
+#ifdef COMERGE_DEBUG_CHECKS
+                if (!(j0 <= j1 && i0 <= i1 && i1 - i0 <= uint64_t(T) && i0 >= j0 && i1 >= j1 &&
+                      i1 - j1 >= i0 - j0 && j1 <= m && i1 - j1 <= n && seg0 <= seg1 &&
+                      (!SEGM || seg1 < args.nseg))) {
+                    printf("comerge: bad tile descriptor cta %u s %u: i0 %llu i1 %llu j0 %llu j1 %llu "
+                           "s0 %llu s1 %llu\n", c, s, (unsigned long long)i0, (unsigned long long)i1,
+                           (unsigned long long)j0, (unsigned long long)j1,
+                           (unsigned long long)seg0, (unsigned long long)seg1);
+                    __trap();
+                }
+#endif
+                mt[4] = seg0;
+                mt[5] = seg1;
+                const uint64_t k0 = i0 - j0, k1 = i1 - j1;
+                const uint32_t a_len = uint32_t(j1 - j0), b_len = uint32_t(k1 - k0);
+                unsigned char* stage = smem + L::oStages + size_t(st) * L::kStage;
+                K* sk = reinterpret_cast<K*>(stage);
+                uint32_t* sv = reinterpret_cast<uint32_t*>(stage + L::kStageKeys);
+                const uint32_t a_off = uint32_t(j0 % VECE);
+                const uint32_t b_base = (a_off + a_len + VECE - 1) / VECE * VECE;
+                const uint32_t b_off = uint32_t(k0 % VECE);
+                const uint64_t RL = SEG == 2 ? args.run_len : 0;  // merge pass (see pipe_args)
+                uint32_t ab, bb;
+                if constexpr (SEG == 3) {
+                    ab = stage_pieces(args.pa, args.pa_start, args.npa, j0, j1, sk, VECE, false,
+                                      nullptr, 0);
+                    bb = stage_pieces(args.pb, args.pb_start, args.npb, k0, k1, sk + b_base, VECE,
+                                      false, nullptr, 0);
+                } else {
+                    ab = RL ? stage_runs(a, m + n, j0, j1, RL, 0, sk, VECE, false, nullptr, 0)
+                            : stage_copy_plan(a, m, j0, j1, sk, VECE);
+                    bb = RL ? stage_runs(b, m + n, k0, k1, RL, 1, sk + b_base, VECE, false, nullptr, 0)
+                            : stage_copy_plan(b, n, k0, k1, sk + b_base, VECE);
+                }
+                uint32_t avb = 0, bvb = 0, av_off = 0, bv_base = 0;
+                if constexpr (HAS_V) {
+                    av_off = uint32_t(j0 % 4);
+                    bv_base = (av_off + a_len + 3) / 4 * 4;
+                    if constexpr (SEG == 3) {
+                        avb = stage_pieces(reinterpret_cast<const void* const*>(args.pav),
+                                           args.pa_start, args.npa, j0, j1, sv, 4, false, nullptr, 0);
+                        bvb = stage_pieces(reinterpret_cast<const void* const*>(args.pbv),
+                                           args.pb_start, args.npb, k0, k1, sv + bv_base, 4, false,
+                                           nullptr, 0);
+                    } else {
+                        avb = RL ? stage_runs(args.av, m + n, j0, j1, RL, 0, sv, 4, false, nullptr, 0)
+                                 : stage_copy_plan(args.av, m, j0, j1, sv, 4);
+                        bvb = RL ? stage_runs(args.bv, m + n, k0, k1, RL, 1, sv + bv_base, 4, false,
+                                              nullptr, 0)
+                                 : stage_copy_plan(args.bv, n, k0, k1, sv + bv_base, 4);
+                    }
+                }
+                mt[0] = i0;
+                mt[1] = k0;
+                mt[2] = (uint64_t(a_len) << 32) | b_len;
+                mt[3] = (uint64_t(a_off) << 48) | (uint64_t(b_base) << 24) | (uint64_t(b_off) << 8) |
+                        uint64_t(av_off);
+                if constexpr (SEGM) mt[6] = seg1 - seg0 + 1 <= uint64_t(L::SEGCAP) ? 1 : 0;  // table?
+                mbar_arrive_expect_tx(&full[st], ab + bb + avb + bvb);
+                if constexpr (SEG == 3) {
+                    stage_pieces(args.pa, args.pa_start, args.npa, j0, j1, sk, VECE, true, &full[st],
+                                 policy);
+                    stage_pieces(args.pb, args.pb_start, args.npb, k0, k1, sk + b_base, VECE, true,
+                                 &full[st], policy);
+                } else if (RL) {
+                    stage_runs(a, m + n, j0, j1, RL, 0, sk, VECE, true, &full[st], policy);
+                    stage_runs(b, m + n, k0, k1, RL, 1, sk + b_base, VECE, true, &full[st], policy);
+                } else {
+                    if (ab) tma_load_1d(sk, a + (j0 - j0 % VECE), ab, &full[st], policy);
+                    if (bb) tma_load_1d(sk + b_base, b + (k0 - k0 % VECE), bb, &full[st], policy);
+                }
+                if constexpr (HAS_V && SEG == 3) {
+                    stage_pieces(reinterpret_cast<const void* const*>(args.pav), args.pa_start,
+                                 args.npa, j0, j1, sv, 4, true, &full[st], policy);
+                    stage_pieces(reinterpret_cast<const void* const*>(args.pbv), args.pb_start,
+                                 args.npb, k0, k1, sv + bv_base, 4, true, &full[st], policy);
+                } else if constexpr (HAS_V) {
+                    if (RL) {
+                        stage_runs(args.av, m + n, j0, j1, RL, 0, sv, 4, true, &full[st], policy);
+                        stage_runs(args.bv, m + n, k0, k1, RL, 1, sv + bv_base, 4, true, &full[st],
+                                   policy);
+                    } else {
+                        if (avb) tma_load_1d(sv, args.av + (j0 - j0 % 4), avb, &full[st], policy);
+                        if (bvb)
+                            tma_load_1d(sv + bv_base, args.bv + (k0 - k0 % 4), bvb, &full[st], policy);
+                    }
+                }
+            }
+            // segmented: the segment-end table (merge_thread_segends), written by
+            // the whole warp after lane 0 has issued the window loads (its
+            // offset reads then overlap the loads; the stage's full barrier
+            // waits for both)
+            if constexpr (SEGM) {
                 const uint64_t nse = seg1 - seg0 + 1;
                 uint32_t* se = reinterpret_cast<uint32_t*>(smem + L::oStages + size_t(st) * L::kStage +
                                                            L::kStageKeys + L::kStageVals);
@@ -1086,94 +1179,6 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&full[st]);  // table written (release)
-                if (lane != 0) continue;
-            }
-#ifdef COMERGE_DEBUG_CHECKS
-            if (!(j0 <= j1 && i0 <= i1 && i1 - i0 <= uint64_t(T) && i0 >= j0 && i1 >= j1 &&
-                  i1 - j1 >= i0 - j0 && j1 <= m && i1 - j1 <= n && seg0 <= seg1 &&
-                  (!SEGM || seg1 < args.nseg))) {
-                printf("comerge: bad tile descriptor cta %u s %u: i0 %llu i1 %llu j0 %llu j1 %llu "
-                       "s0 %llu s1 %llu\n", c, s, (unsigned long long)i0, (unsigned long long)i1,
-                       (unsigned long long)j0, (unsigned long long)j1,
-                       (unsigned long long)seg0, (unsigned long long)seg1);
-                __trap();
-            }
-#endif
-            mt[4] = seg0;
-            mt[5] = seg1;
-            const uint64_t k0 = i0 - j0, k1 = i1 - j1;
-            const uint32_t a_len = uint32_t(j1 - j0), b_len = uint32_t(k1 - k0);
-            unsigned char* stage = smem + L::oStages + size_t(st) * L::kStage;
-            K* sk = reinterpret_cast<K*>(stage);
-            uint32_t* sv = reinterpret_cast<uint32_t*>(stage + L::kStageKeys);
-            const uint32_t a_off = uint32_t(j0 % VECE);
-            const uint32_t b_base = (a_off + a_len + VECE - 1) / VECE * VECE;
-            const uint32_t b_off = uint32_t(k0 % VECE);
-            const uint64_t RL = SEG == 2 ? args.run_len : 0;  // merge pass (see pipe_args)
-            uint32_t ab, bb;
-            if constexpr (SEG == 3) {
-                ab = stage_pieces(args.pa, args.pa_start, args.npa, j0, j1, sk, VECE, false,
-                                  nullptr, 0);
-                bb = stage_pieces(args.pb, args.pb_start, args.npb, k0, k1, sk + b_base, VECE,
-                                  false, nullptr, 0);
-            } else {
-                ab = RL ? stage_runs(a, m + n, j0, j1, RL, 0, sk, VECE, false, nullptr, 0)
-                        : stage_copy_plan(a, m, j0, j1, sk, VECE);
-                bb = RL ? stage_runs(b, m + n, k0, k1, RL, 1, sk + b_base, VECE, false, nullptr, 0)
-                        : stage_copy_plan(b, n, k0, k1, sk + b_base, VECE);
-            }
-            uint32_t avb = 0, bvb = 0, av_off = 0, bv_base = 0;
-            if constexpr (HAS_V) {
-                av_off = uint32_t(j0 % 4);
-                bv_base = (av_off + a_len + 3) / 4 * 4;
-                if constexpr (SEG == 3) {
-                    avb = stage_pieces(reinterpret_cast<const void* const*>(args.pav),
-                                       args.pa_start, args.npa, j0, j1, sv, 4, false, nullptr, 0);
-                    bvb = stage_pieces(reinterpret_cast<const void* const*>(args.pbv),
-                                       args.pb_start, args.npb, k0, k1, sv + bv_base, 4, false,
-                                       nullptr, 0);
-                } else {
-                    avb = RL ? stage_runs(args.av, m + n, j0, j1, RL, 0, sv, 4, false, nullptr, 0)
-                             : stage_copy_plan(args.av, m, j0, j1, sv, 4);
-                    bvb = RL ? stage_runs(args.bv, m + n, k0, k1, RL, 1, sv + bv_base, 4, false,
-                                          nullptr, 0)
-                             : stage_copy_plan(args.bv, n, k0, k1, sv + bv_base, 4);
-                }
-            }
-            mt[0] = i0;
-            mt[1] = k0;
-            mt[2] = (uint64_t(a_len) << 32) | b_len;
-            mt[3] = (uint64_t(a_off) << 48) | (uint64_t(b_base) << 24) | (uint64_t(b_off) << 8) |
-                    uint64_t(av_off);
-            if constexpr (SEGM) mt[6] = seg1 - seg0 + 1 <= uint64_t(L::SEGCAP) ? 1 : 0;  // table?
-            mbar_arrive_expect_tx(&full[st], ab + bb + avb + bvb);
-            if constexpr (SEG == 3) {
-                stage_pieces(args.pa, args.pa_start, args.npa, j0, j1, sk, VECE, true, &full[st],
-                             policy);
-                stage_pieces(args.pb, args.pb_start, args.npb, k0, k1, sk + b_base, VECE, true,
-                             &full[st], policy);
-            } else if (RL) {
-                stage_runs(a, m + n, j0, j1, RL, 0, sk, VECE, true, &full[st], policy);
-                stage_runs(b, m + n, k0, k1, RL, 1, sk + b_base, VECE, true, &full[st], policy);
-            } else {
-                if (ab) tma_load_1d(sk, a + (j0 - j0 % VECE), ab, &full[st], policy);
-                if (bb) tma_load_1d(sk + b_base, b + (k0 - k0 % VECE), bb, &full[st], policy);
-            }
-            if constexpr (HAS_V && SEG == 3) {
-                stage_pieces(reinterpret_cast<const void* const*>(args.pav), args.pa_start,
-                             args.npa, j0, j1, sv, 4, true, &full[st], policy);
-                stage_pieces(reinterpret_cast<const void* const*>(args.pbv), args.pb_start,
-                             args.npb, k0, k1, sv + bv_base, 4, true, &full[st], policy);
-            } else if constexpr (HAS_V) {
-                if (RL) {
-                    stage_runs(args.av, m + n, j0, j1, RL, 0, sv, 4, true, &full[st], policy);
-                    stage_runs(args.bv, m + n, k0, k1, RL, 1, sv + bv_base, 4, true, &full[st],
-                               policy);
-                } else {
-                    if (avb) tma_load_1d(sv, args.av + (j0 - j0 % 4), avb, &full[st], policy);
-                    if (bvb)
-                        tma_load_1d(sv + bv_base, args.bv + (k0 - k0 % 4), bvb, &full[st], policy);
-                }
             }
         }
         return;
