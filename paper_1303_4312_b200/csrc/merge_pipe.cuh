@@ -109,7 +109,10 @@ struct pipe_layout {
     // more segments than this in a tile (average under ~8 VT outputs each, so
     // many warps hold a thread crossing two segment ends):
     // consumers use the general per-step segment test instead of the lean loop
-    static constexpr int kLeanSegs = T / (8 * VT);
+#ifndef PIPE_LEAN_SEGS_DIV
+#define PIPE_LEAN_SEGS_DIV 8
+#endif
+    static constexpr int kLeanSegs = PIPE_LEAN_SEGS_DIV ? T / (PIPE_LEAN_SEGS_DIV * VT) : SEGCAP;
     static constexpr bool kSeg = SEG == 1 || SEG == 2;  // segmented modes
     static constexpr size_t kStageOffs = kSeg ? size_t(SEGCAP) * 4 : 0;
     static constexpr size_t kStage = kStageKeys + kStageVals + kStageOffs;

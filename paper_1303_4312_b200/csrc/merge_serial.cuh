@@ -190,6 +190,8 @@ __device__ __forceinline__ void merge_thread_segends_lean(const K* sA, const K* 
     // barrier; now the whole warp switches (lanes without a segment end never
     // reach step VT), 15 instead of 12 instructions per step for that warp.
     const bool warp_switch = __any_sync(0xffffffffu, path == 1);
+    // likewise the rolled loop (it handles every case): all lanes or none
+    if (__any_sync(0xffffffffu, path == 2)) path = 2;
     if (path != 2) {
         if (warp_switch)
             serial_merge<K, VT, TRACK, true>(a0 + ia * S, a0 + x1 * S, b0 + ib * S, b0 + y1 * S,
