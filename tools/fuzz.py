@@ -2,7 +2,7 @@
 oracle, for a fixed wall-clock budget:  python tools/fuzz.py [seconds] [seed]
 
 Each round draws an entry point (keys / key-value merge, segmented batch,
-sort, sort of pairs, pieced range merge, host-buffer merge), a key type, a
+sort, sort of pairs, pieced range merge, host-buffer merges), a key type, a
 size (empty, tiny, around tile multiples, up to a few million), a distribution
 (all equal, few distinct, uniform, disjoint ranges, one side tiny) and a
 misalignment of the views, runs it on cuda:0 and compares bit-exactly."""
@@ -62,7 +62,8 @@ P_T = {np.dtype(np.int32): torch.int32, np.dtype(np.uint32): torch.uint32,
 
 
 def one(rng):
-    kind = ["keys", "pairs", "seg", "sort", "sortp", "pieces", "host"][int(rng.integers(0, 7))]
+    kinds = ["keys", "pairs", "seg", "sort", "sortp", "pieces", "host", "hostp"]
+    kind = kinds[int(rng.integers(0, len(kinds)))]
     dt = [np.int32, np.uint32, np.uint64][int(rng.integers(0, 3))]
     if kind == "seg" and dt == np.uint64:
         dt = np.int32
@@ -117,10 +118,19 @@ def one(rng):
         hi = int(rng.integers(lo, total + 1))
         out = P.merge_pieces(cut(a), cut(b), lo, hi)
         assert np.array_equal(out.cpu().numpy(), port.merge(a, b)[lo:hi]), tag + f" [{lo},{hi})"
-    else:  # host buffers
+    elif kind == "host":  # host buffers: keys
         out = np.empty(m + n, dt)
         P.merge_parallel(a, b, out, int(rng.integers(1, 40)))
         assert np.array_equal(out, port.merge(a, b)), tag
+    else:  # host buffers: key-value (misaligned host views sometimes)
+        sh = int(rng.integers(0, 3))
+        av = np.arange(m, dtype=np.uint32)
+        bv = np.arange(n, dtype=np.uint32) | np.uint32(1 << 31)
+        ok = np.empty(m + n + sh, dt)[sh:]
+        ov = np.empty(m + n + sh, np.uint32)[sh:]
+        P.merge_pairs(a, av, b, bv, ok, ov)
+        ek, ev = port.merge(a, b, av, bv)
+        assert np.array_equal(ok, ek) and np.array_equal(ov, ev), tag + f" shift={sh}"
     torch.cuda.synchronize()
     return kind
 
