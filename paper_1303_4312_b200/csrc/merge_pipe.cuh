@@ -9,7 +9,8 @@
 //     worker's block, parallel.hpp:201-207: co-rank its start, then every
 //     later boundary); the remaining 30% form a dynamic tail claimed one tile
 //     at a time from a global counter, their co-ranks computed in the
-//     background by a tail warp in every CTA.  The tail absorbs the start-up
+//     background by a tail warp in every CTA (from kernel start: it takes no
+//     part in the start-up barriers).  The tail absorbs the start-up
 //     skew between CTAs and the ~25% spread of per-SM streaming rates
 //     (B200 GPCs differ).
 //   * Scheduler warp: co-ranks its range start (33-ary warp search over the
@@ -21,10 +22,11 @@
 //   * Producer warp: per descriptor, waits for a free stage and TMA-loads
 //     exactly the tile's A window [j0, j1) and B window [i0-j0, i1-j1) (16-byte
 //     aligned supersets, payloads too): every input byte crosses HBM once.
-//     Segmented batches: the whole warp also writes the tile's segment-end
-//     table into the stage.
+//     Segmented batches: after the loads are issued, the whole warp writes
+//     the tile's segment-end table into the stage.
 //   * Consumers (8 warps): tile-local co-rank per VT-slot diagonal and the
-//     branch-free serial merge (merge.hpp:22-31, ties to A) of merge_tile.cuh;
+//     branch-free serial merge (merge.hpp:22-31, ties to A) of
+//     merge_serial.cuh (12 instructions per output step);
 //     the merged tile is written back into the stage and handed to the store
 //     warp, which stores it with one TMA bulk store and releases the stage
 //     once the store has read it (consumers never wait on a store).
