@@ -7,21 +7,24 @@ NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -Wall \
            --expt-relaxed-constexpr -Iinclude
 PKG := paper_1303_4312_b200
 LIB := $(PKG)/lib/libcomerge_cuda.so
-SRCS := $(PKG)/csrc/comerge_cuda.cu $(PKG)/csrc/testkit.cu
+# test / bench infrastructure (seeded generators, full-size checkers): its own
+# library, never linked into the product
+TKLIB := $(PKG)/lib/libcomerge_cuda_testkit.so
+SRCS := $(PKG)/csrc/comerge_cuda.cu
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/comerge_cuda.h include/comerge_cuda_testkit.h
 OBJS := $(patsubst $(PKG)/csrc/%.cu,$(PKG)/lib/%.o,$(SRCS))
 
 SHIM_TEST := tests/cpp/shim_test
 CLI := bin/comerge_cuda
 
-all: $(LIB) oracle $(SHIM_TEST) $(CLI)
+all: $(LIB) $(TKLIB) oracle $(SHIM_TEST) $(CLI)
 
 # the reference's command line tool with device merges (cli/)
 $(CLI): cli/comerge_cuda.cpp cli/keyfile.hpp include/comerge/cuda.hpp include/comerge_cuda.h \
-        include/comerge_cuda_testkit.h $(LIB)
+        include/comerge_cuda_testkit.h $(LIB) $(TKLIB)
 	@mkdir -p bin
 	g++ -std=c++20 -O2 -Wall -Wextra -Iinclude -Icli -I/usr/local/cuda/include -o $@ $< \
-	    -L$(PKG)/lib -lcomerge_cuda -L/usr/local/cuda/lib64 -lcudart \
+	    -L$(PKG)/lib -lcomerge_cuda -lcomerge_cuda_testkit -L/usr/local/cuda/lib64 -lcudart \
 	    -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib' -Wl,-rpath,/usr/local/cuda/lib64
 
 # C++ drop-in shim test (include/comerge/cuda.hpp over the C ABI)
@@ -37,6 +40,9 @@ $(PKG)/lib/%.o: $(PKG)/csrc/%.cu $(HDRS)
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
 
+$(TKLIB): $(PKG)/lib/testkit.o
+	$(NVCC) $(ARCH) -shared -o $@ $< -lcudart
+
 oracle:
 	$(MAKE) -C oracle
 
@@ -49,8 +55,7 @@ debug-lib: $(DBG)
 $(DBG): $(SRCS) $(HDRS)
 	@mkdir -p lib_var/dbg
 	$(NVCC) $(NVFLAGS) -DCOMERGE_DEBUG_CHECKS=1 -c $(PKG)/csrc/comerge_cuda.cu -o lib_var/dbg/comerge_cuda.o
-	$(NVCC) $(NVFLAGS) -DCOMERGE_DEBUG_CHECKS=1 -c $(PKG)/csrc/testkit.cu -o lib_var/dbg/testkit.o
-	$(NVCC) $(ARCH) -shared -o $@ lib_var/dbg/comerge_cuda.o lib_var/dbg/testkit.o -lcudart
+	$(NVCC) $(ARCH) -shared -o $@ lib_var/dbg/comerge_cuda.o -lcudart
 
 clean:
 	rm -f $(PKG)/lib/*.o $(PKG)/lib/*.so $(PKG)/lib/*.ptxas.txt $(SHIM_TEST) $(CLI)

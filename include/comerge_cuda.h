@@ -96,8 +96,11 @@ void comerge_cuda_set_tuning(int static_pct, int flags, int lookahead);
 /* ------------------------------------------------------------ workspace */
 
 /* Bytes of scratch the merge entry points need for (m, n): the tile
- * boundary co-ranks.  Replaces nothing in the reference (which allocates
- * per-worker slots itself, parallel.hpp:189); CUB-style query. */
+ * boundary co-ranks / the pipeline's dynamic-tail state.  Replaces nothing in
+ * the reference (which allocates per-worker slots itself, parallel.hpp:189);
+ * CUB-style query.  A workspace may have any alignment: the library uses it
+ * from its first 256-byte boundary, and every *_workspace_bytes figure
+ * includes those 256 bytes of slack (also for the sort queries below). */
 size_t comerge_cuda_merge_workspace_bytes(size_t m, size_t n, int key_kind, int has_payload);
 size_t comerge_cuda_segmented_workspace_bytes(size_t total, size_t nseg, int key_kind);
 

@@ -13,8 +13,10 @@ import re
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 REPO_DIR = os.path.dirname(PKG_DIR)
 LIB_PATH = os.environ.get("COMERGE_LIB_PATH") or os.path.join(PKG_DIR, "lib", "libcomerge_cuda.so")
-HEADERS = [os.path.join(REPO_DIR, "include", "comerge_cuda.h"),
-           os.path.join(REPO_DIR, "include", "comerge_cuda_testkit.h")]
+# test / bench infrastructure (seeded generators, checkers): a separate library
+TESTKIT_PATH = os.path.join(PKG_DIR, "lib", "libcomerge_cuda_testkit.so")
+HEADERS = [os.path.join(REPO_DIR, "include", "comerge_cuda.h")]
+TESTKIT_HEADERS = [os.path.join(REPO_DIR, "include", "comerge_cuda_testkit.h")]
 
 OK, E_INVALID, E_RANGE, E_LENGTH, E_CUDA = 0, 1, 2, 3, 4
 KEY_I32, KEY_U32, KEY_U64 = 0, 1, 2
@@ -43,7 +45,6 @@ def _load():
             "(there is no CPU fallback)")
     lib = C.CDLL(LIB_PATH)
     lib.comerge_cuda_last_error.restype = C.c_char_p
-    lib.comerge_testkit_last_error.restype = C.c_char_p
     lib.comerge_cuda_abi_version.restype = _i
     lib.comerge_cuda_merge_workspace_bytes.argtypes = [_sz, _sz, _i, _i]
     lib.comerge_cuda_merge_workspace_bytes.restype = _sz
@@ -92,25 +93,40 @@ def _load():
     lib.comerge_cuda_set_trace.restype = None
     lib.comerge_cuda_set_tuning.argtypes = [_i, _i, _i]
     lib.comerge_cuda_set_tuning.restype = None
-    lib.comerge_testkit_generate_raw.argtypes = [_u64, _u64, _sz, _u64, _p, _p]
-    lib.comerge_testkit_generate_runs.argtypes = [_i, _u64, _u64, _p, _sz, _sz, _u64, _p, _p]
     lib.comerge_partition_output.argtypes = [_u64, _u64, _u64, C.POINTER(_u64)]
-    lib.comerge_testkit_generate_sorted.argtypes = [_i, _u64, _u64, _sz, _u64, _p, _p]
-    lib.comerge_testkit_iota.argtypes = [_p, _sz, C.c_uint32, _p]
-    lib.comerge_testkit_fill_runs.argtypes = [_i, _sz, _u64, _u64, _p, _p]
-    lib.comerge_testkit_verify_pairs.argtypes = [_i, _p, _sz, _p, _sz, _p, _p, _p, _p]
-    lib.comerge_testkit_checksum.argtypes = [_i, _p, _sz, _p, _p]
-    lib.comerge_testkit_count_unsorted.argtypes = [_i, _p, _sz, _p, _p]
     return lib
 
 
 lib = _load()
+_tk = None
 
 
-def declared_symbols():
-    """Every function name declared in include/*.h (for the export test)."""
+def tk():
+    """The testkit library (libcomerge_cuda_testkit.so: seeded device
+    generators and full-size checkers for tests and the bench), loaded on first
+    use.  Not part of the merge path."""
+    global _tk
+    if _tk is None:
+        if not os.path.exists(TESTKIT_PATH):
+            raise ImportError(f"libcomerge_cuda_testkit.so not built at {TESTKIT_PATH}; run `make`")
+        t = C.CDLL(TESTKIT_PATH)
+        t.comerge_testkit_last_error.restype = C.c_char_p
+        t.comerge_testkit_generate_raw.argtypes = [_u64, _u64, _sz, _u64, _p, _p]
+        t.comerge_testkit_generate_runs.argtypes = [_i, _u64, _u64, _p, _sz, _sz, _u64, _p, _p]
+        t.comerge_testkit_generate_sorted.argtypes = [_i, _u64, _u64, _sz, _u64, _p, _p]
+        t.comerge_testkit_iota.argtypes = [_p, _sz, C.c_uint32, _p]
+        t.comerge_testkit_fill_runs.argtypes = [_i, _sz, _u64, _u64, _p, _p]
+        t.comerge_testkit_verify_pairs.argtypes = [_i, _p, _sz, _p, _sz, _p, _p, _p, _p]
+        t.comerge_testkit_checksum.argtypes = [_i, _p, _sz, _p, _p]
+        t.comerge_testkit_count_unsorted.argtypes = [_i, _p, _sz, _p, _p]
+        _tk = t
+    return _tk
+
+
+def declared_symbols(headers=None):
+    """Every function name declared in the product header (or `headers`)."""
     names = []
-    for h in HEADERS:
+    for h in headers or HEADERS:
         text = open(h).read()
         text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
         names += re.findall(r"\b(comerge_\w+)\s*\(", text)
@@ -125,7 +141,7 @@ def check(rc: int, testkit: bool = False):
     """Map a status code onto the reference's exception types."""
     if rc == OK:
         return
-    msg = (lib.comerge_testkit_last_error() if testkit else lib.comerge_cuda_last_error()).decode()
+    msg = (tk().comerge_testkit_last_error() if testkit else lib.comerge_cuda_last_error()).decode()
     if rc == E_INVALID:
         raise ValueError(msg)        # std::invalid_argument
     if rc == E_RANGE:

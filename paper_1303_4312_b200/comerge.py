@@ -28,6 +28,7 @@ independent pairs) and ``co_rank_batch``.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 from dataclasses import dataclass, field
 from typing import List, Optional
@@ -84,6 +85,14 @@ def _stream(x=None):
     return None
 
 
+def _on(x):
+    """Run a call with x's device current (kernels launch on the current
+    device; the library caches its per-device state by it)."""
+    if _is_torch(x) and x.is_cuda:
+        return torch.cuda.device(x.device)
+    return contextlib.nullcontext()
+
+
 def _empty_like_merge(a, total):
     if _is_torch(a):
         return torch.empty(total, dtype=a.dtype, device=a.device)
@@ -117,9 +126,10 @@ def co_rank(target: int, a, b, stats: Optional[CoRankStats] = None):
     if target < 0:
         raise IndexError("co_rank: rank out of range (exceeds m+n)")
     j, k, it, cmp = C.c_uint64(), C.c_uint64(), C.c_uint32(), C.c_uint32()
-    N.check(getattr(N.lib, f"comerge_co_rank_{suf}")(
-        int(target), _ptr(a), _len(a), _ptr(b), _len(b), C.byref(j), C.byref(k), C.byref(it),
-        C.byref(cmp)))
+    with _on(a):
+        N.check(getattr(N.lib, f"comerge_co_rank_{suf}")(
+            int(target), _ptr(a), _len(a), _ptr(b), _len(b), C.byref(j), C.byref(k), C.byref(it),
+            C.byref(cmp)))
     if stats is not None:
         stats.iterations, stats.comparisons = it.value, cmp.value
     return (j.value, k.value)
@@ -140,23 +150,22 @@ def co_rank_batch(ranks, a, b, with_stats: bool = False):
     j = torch.empty(q, dtype=torch.uint64, device=dev)
     it = torch.empty(q, dtype=torch.uint32, device=dev) if with_stats else None
     cmp = torch.empty(q, dtype=torch.uint32, device=dev) if with_stats else None
-    N.check(getattr(N.lib, f"comerge_cuda_co_rank_batch_{suf}")(
-        _ptr(ranks), q, _ptr(a), _len(a), _ptr(b), _len(b), _ptr(j), _ptr(it), _ptr(cmp),
-        _stream(a)))
+    with _on(a):
+        N.check(getattr(N.lib, f"comerge_cuda_co_rank_batch_{suf}")(
+            _ptr(ranks), q, _ptr(a), _len(a), _ptr(b), _len(b), _ptr(j), _ptr(it), _ptr(cmp),
+            _stream(a)))
     return (j, it, cmp) if with_stats else j
 
 
 # ------------------------------------------------------------------- merges
 
-KERNEL_PATHS = {"auto": 0, "tile": 1, "stream": 2, "pipe": 3}
+KERNEL_PATHS = {"auto": 0, "tile": 1, "pipe": 3}
 
 
 def set_kernel_path(path: str = "auto") -> None:
     """Select the device kernel for merges issued from this thread: "auto",
-    "tile" (partition + one CTA per tile; any alignment), "stream" (ring
-    streaming kernel) or "pipe" (persistent tile pipeline; the default for
-    aligned buffers, segmented batches included).  "stream" / "pipe" need
-    16-byte aligned buffers."""
+    "tile" (partition + one CTA per tile; any alignment) or "pipe" (persistent
+    tile pipeline; the default, segmented batches included)."""
     N.lib.comerge_cuda_set_path(KERNEL_PATHS[path])
 
 
@@ -200,8 +209,9 @@ def stable_merge(a, b, out=None, workspace=None):
     _check_out("stable_merge", a, b, out)
     if _is_torch(a) and a.is_cuda:
         wsp, wsb = _ws(workspace)
-        N.check(getattr(N.lib, f"comerge_cuda_merge_keys_{suf}")(
-            _ptr(a), _len(a), _ptr(b), _len(b), _ptr(out), wsp, wsb, _stream(a)))
+        with _on(a):
+            N.check(getattr(N.lib, f"comerge_cuda_merge_keys_{suf}")(
+                _ptr(a), _len(a), _ptr(b), _len(b), _ptr(out), wsp, wsb, _stream(a)))
     else:
         rep = N.MergeReport()
         rc = getattr(N.lib, f"comerge_merge_parallel_{suf}")(
@@ -258,10 +268,11 @@ def _merge_parallel(who, a, b, out, workers, opts, synced):
     mo = N.MergeOptions(int(synced), int(count))
     if _is_torch(out) and out.is_cuda:
         torch.cuda.current_stream(out.device).synchronize()
-    N.check(getattr(N.lib, f"comerge_merge_parallel_ex_{suf}")(
-        _ptr(a), None, _len(a), _ptr(b), None, _len(b), _ptr(out), None, _len(out), workers,
-        C.byref(mo), C.byref(rep), C.c_void_p(bs.ctypes.data), C.c_void_p(its.ctypes.data),
-        C.byref(cmp)))
+    with _on(out if _is_torch(out) and out.is_cuda else a):
+        N.check(getattr(N.lib, f"comerge_merge_parallel_ex_{suf}")(
+            _ptr(a), None, _len(a), _ptr(b), None, _len(b), _ptr(out), None, _len(out), workers,
+            C.byref(mo), C.byref(rep), C.c_void_p(bs.ctypes.data), C.c_void_p(its.ctypes.data),
+            C.byref(cmp)))
     return MergeReport(
         m=rep.m, n=rep.n, workers=rep.workers, wall_ns=rep.wall_ns,
         block_sizes=[int(x) for x in bs[:workers]],
@@ -315,8 +326,9 @@ def plan(a, b, workers: int):
     raw = np.zeros(7 * workers, np.uint64)
     if _is_torch(a) and a.is_cuda:
         torch.cuda.current_stream(a.device).synchronize()
-    N.check(getattr(N.lib, f"comerge_plan_{suf}")(_ptr(a), _len(a), _ptr(b), _len(b), workers,
-                                                   C.c_void_p(raw.ctypes.data)))
+    with _on(a):
+        N.check(getattr(N.lib, f"comerge_plan_{suf}")(_ptr(a), _len(a), _ptr(b), _len(b), workers,
+                                                       C.c_void_p(raw.ctypes.data)))
     return [BlockAssignment(*(int(x) for x in raw[7 * r:7 * r + 7])) for r in range(workers)]
 
 
@@ -334,9 +346,10 @@ def merge_pairs(a_keys, a_vals, b_keys, b_vals, out_keys=None, out_vals=None, wo
     _check_out("merge_pairs", a_vals, b_vals, out_vals)
     if _is_torch(a_keys) and a_keys.is_cuda:
         wsp, wsb = _ws(workspace)
-        N.check(getattr(N.lib, f"comerge_cuda_merge_pairs_{suf}")(
-            _ptr(a_keys), _ptr(a_vals), _len(a_keys), _ptr(b_keys), _ptr(b_vals), _len(b_keys),
-            _ptr(out_keys), _ptr(out_vals), wsp, wsb, _stream(a_keys)))
+        with _on(a_keys):
+            N.check(getattr(N.lib, f"comerge_cuda_merge_pairs_{suf}")(
+                _ptr(a_keys), _ptr(a_vals), _len(a_keys), _ptr(b_keys), _ptr(b_vals),
+                _len(b_keys), _ptr(out_keys), _ptr(out_vals), wsp, wsb, _stream(a_keys)))
     else:
         rep = N.MergeReport()
         N.check(getattr(N.lib, f"comerge_merge_parallel_pairs_{suf}")(
@@ -356,9 +369,10 @@ def merge_segmented(a, a_off, b, b_off, out=None, workspace=None):
         out = _empty_like_merge(a, _len(a) + _len(b))
     _check_out("merge_segmented", a, b, out)
     wsp, wsb = _ws(workspace)
-    N.check(getattr(N.lib, f"comerge_cuda_merge_segmented_{suf}")(
-        _ptr(a), _ptr(a_off), _len(a), _ptr(b), _ptr(b_off), _len(b), max(nseg, 0), _ptr(out),
-        wsp, wsb, _stream(a)))
+    with _on(a):
+        N.check(getattr(N.lib, f"comerge_cuda_merge_segmented_{suf}")(
+            _ptr(a), _ptr(a_off), _len(a), _ptr(b), _ptr(b_off), _len(b), max(nseg, 0),
+            _ptr(out), wsp, wsb, _stream(a)))
     return out
 
 
@@ -381,8 +395,9 @@ def sort(keys, out=None, workspace=None):
     if _len(out) != _len(keys):
         raise ValueError("sort: output length must equal the input length")
     wsp, wsb = _ws(workspace)
-    N.check(getattr(N.lib, f"comerge_cuda_sort_keys_{suf}")(
-        _ptr(keys), _len(keys), _ptr(out), wsp, wsb, _stream(keys)))
+    with _on(keys):
+        N.check(getattr(N.lib, f"comerge_cuda_sort_keys_{suf}")(
+            _ptr(keys), _len(keys), _ptr(out), wsp, wsb, _stream(keys)))
     return out
 
 
@@ -404,9 +419,10 @@ def sort_pairs(keys, vals, out_keys=None, out_vals=None, workspace=None):
         wsp, wsb = None, 0
     else:
         wsp, wsb = _ws(workspace)
-    N.check(getattr(N.lib, f"comerge_cuda_sort_pairs_{suf}")(
-        _ptr(keys), _ptr(vals), _len(keys), _ptr(out_keys), _ptr(out_vals), wsp, wsb,
-        _stream(keys)))
+    with _on(keys):
+        N.check(getattr(N.lib, f"comerge_cuda_sort_pairs_{suf}")(
+            _ptr(keys), _ptr(vals), _len(keys), _ptr(out_keys), _ptr(out_vals), wsp, wsb,
+            _stream(keys)))
     return out_keys, out_vals
 
 
@@ -447,17 +463,19 @@ def merge_pieces(a_pieces, b_pieces, out_begin: int, out_end: int, out=None, wor
     bl = (C.c_uint64 * len(b_pieces))(*[t.numel() for t in b_pieces])
     wsp, wsb = _ws(workspace)
     if not pairs:
-        N.check(getattr(N.lib, f"comerge_cuda_merge_keys_pieces_{suf}")(
-            ptrs(a_pieces), al, len(a_pieces), ptrs(b_pieces), bl, len(b_pieces), out_begin,
-            out_end, _ptr(out), wsp, wsb, _stream(out)))
+        with _on(out):
+            N.check(getattr(N.lib, f"comerge_cuda_merge_keys_pieces_{suf}")(
+                ptrs(a_pieces), al, len(a_pieces), ptrs(b_pieces), bl, len(b_pieces), out_begin,
+                out_end, _ptr(out), wsp, wsb, _stream(out)))
         return out
     for v, k in zip(list(a_val_pieces) + list(b_val_pieces), list(a_pieces) + list(b_pieces)):
         if _len(v) != _len(k):
             raise ValueError("merge_pieces: payload length must equal key length")
     if out_vals is None:
         out_vals = torch.empty(out_end - out_begin, dtype=torch.uint32, device=dev_)
-    N.check(getattr(N.lib, f"comerge_cuda_merge_pairs_pieces_{suf}")(
-        ptrs(a_pieces), ptrs(a_val_pieces), al, len(a_pieces), ptrs(b_pieces),
-        ptrs(b_val_pieces), bl, len(b_pieces), out_begin, out_end, _ptr(out), _ptr(out_vals),
-        wsp, wsb, _stream(out)))
+    with _on(out):
+        N.check(getattr(N.lib, f"comerge_cuda_merge_pairs_pieces_{suf}")(
+            ptrs(a_pieces), ptrs(a_val_pieces), al, len(a_pieces), ptrs(b_pieces),
+            ptrs(b_val_pieces), bl, len(b_pieces), out_begin, out_end, _ptr(out), _ptr(out_vals),
+            wsp, wsb, _stream(out)))
     return out, out_vals

@@ -11,13 +11,13 @@
 #include <cstring>
 #include <atomic>
 #include <chrono>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
 
 #include "../../include/comerge_cuda.h"
 #include "merge_pipe.cuh"
-#include "merge_stream.cuh"
 #include "merge_tile.cuh"
 #include "sort.cuh"
 
@@ -27,27 +27,44 @@ namespace {
 
 thread_local std::string g_error;
 thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;
-thread_local int g_path = 0;  // 0 auto, 1 tile (v1), 2 ring streaming (v2), 3 tile pipeline (v3)
-thread_local int g_last_path = 0;  // kernel of the last merge: 1 tile, 2 ring, 3 pipe, 4 segmented
+thread_local int g_path = 0;  // 0 auto, 1 tile (v1), 3 tile pipeline
+thread_local int g_last_path = 0;  // kernel of the last merge: 1 tile, 3 pipe, 4 segmented tile, 5-7 pipe modes
 thread_local unsigned long long* g_trace = nullptr;  // debug: per-CTA timestamps
 // tuning knobs of the tile pipeline (0 = default)
 thread_local int g_tune_lookahead = 0, g_tune_static_pct = 0, g_tune_flags = 0;
 thread_local int g_host_mode = 0;  // host buffers: 0 chunked pipeline, 1 zero-copy, 2 plain staging
 
-int sm_count() {
-    static const int n = [] {
-        int dev = 0, v = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        return v > 0 ? v : 148;
-    }();
-    return n;
+// Per-device state: kernel attributes (the dynamic shared-memory opt-in is
+// per device context), grid limits and the library's streams are cached per
+// device, indexed by the caller's current device.
+constexpr int kMaxDevices = 64;
+
+int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev >= 0 && dev < kMaxDevices ? dev : 0;
 }
 
-// Persistent grid size for the tile-pipeline kernel (resident CTAs, cached).
+int sm_count() {
+    static std::once_flag once[kMaxDevices];
+    static int n[kMaxDevices];
+    const int dev = current_device();
+    std::call_once(once[dev], [dev] {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        n[dev] = v > 0 ? v : 148;
+    });
+    return n[dev];
+}
+
+// Persistent grid size for the tile-pipeline kernel (resident CTAs), with the
+// kernel's shared-memory opt-in set once per device.
 template <typename K, bool HAS_V, int SEG>
 int pipe_grid_limit() {
-    static const int limit = [] {
+    static std::once_flag once[kMaxDevices];
+    static int limit[kMaxDevices];
+    const int dev = current_device();
+    std::call_once(once[dev], [dev] {
         using L = pipe_layout<K, HAS_V, SEG>;
         auto kern = merge_pipe_kernel<K, HAS_V, SEG>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::kSmem));
@@ -58,28 +75,9 @@ int pipe_grid_limit() {
             cudaGetLastError();
             per_sm = 1;
         }
-        return per_sm * sm_count();
-    }();
-    return limit;
-}
-
-// Persistent grid size for the streaming kernel (resident CTAs, cached).
-template <typename K, bool HAS_V>
-int stream_grid_limit() {
-    static const int limit = [] {
-        using L = stream_layout<K, HAS_V>;
-        auto kern = merge_stream_kernel<K, HAS_V>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L::kSmem));
-        int per_sm = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::kThreads,
-                                                          L::kSmem) != cudaSuccess ||
-            per_sm < 1) {
-            cudaGetLastError();
-            per_sm = 1;
-        }
-        return per_sm * sm_count();
-    }();
-    return limit;
+        limit[dev] = per_sm * sm_count();
+    });
+    return limit[dev];
 }
 
 void mark_before(cudaStream_t s) {
@@ -155,19 +153,28 @@ uint64_t next_tail_epoch() {
     return x ? x : 1;
 }
 
+// alignment slack of a caller workspace (see scratch::acquire)
+constexpr size_t kWsSlack = 256;
+size_t with_slack(size_t need) { return need ? need + kWsSlack : 0; }
+
 // Stream-ordered scratch: caller workspace, or the private pool when ws == NULL.
 struct scratch {
     void* ptr = nullptr;
     bool owned = false;
     cudaStream_t stream = nullptr;
+    // A caller workspace may have any alignment: the scratch starts at its
+    // first 256-byte boundary (the tail state is read with 128-bit atomics),
+    // and the *_workspace_bytes queries include that slack (kWsSlack).
     int acquire(void* ws, size_t ws_bytes, size_t need, cudaStream_t s) {
         stream = s;
         if (need == 0) return COMERGE_OK;
         if (ws) {
-            if (ws_bytes < need)
+            const uintptr_t p = reinterpret_cast<uintptr_t>(ws);
+            const size_t pad = size_t((256 - (p & 255)) & 255);
+            if (ws_bytes < pad || ws_bytes - pad < need)
                 return fail(COMERGE_E_INVALID, "comerge: workspace too small (need " +
-                                                   std::to_string(need) + " bytes)");
-            ptr = ws;
+                                                   std::to_string(need + kWsSlack) + " bytes)");
+            ptr = reinterpret_cast<void*>(p + pad);
             return COMERGE_OK;
         }
         const cudaError_t e = pool_alloc(&ptr, need, s);
@@ -354,27 +361,15 @@ int merge_device(const K* a, const uint32_t* av, size_t m, const K* b, const uin
     if (int rc = check_merge_args<K>(who, a, m, b, n, out, av, bv, outv, HAS_V)) return rc;
     const uint64_t total = uint64_t(m) + n;
     if (total == 0) return COMERGE_OK;
-    // v2: persistent streaming kernel (TMA rings) when every buffer is
-    // 16-byte aligned and there is more than one tile per resident CTA slot.
-    using SL = stream_layout<K, HAS_V>;
+    // the tile pipeline when every buffer is 16-byte aligned and there are
+    // enough tiles to fill it
     const bool aligned_all = aligned16(a) && aligned16(b) && aligned16(out) &&
                              (!HAS_V || (aligned16(av) && aligned16(bv) && aligned16(outv)));
-    const uint64_t stiles = div_up(total, SL::T);
     using PL = pipe_layout<K, HAS_V>;
     const uint64_t ptiles = div_up(total, PL::T);
     if (aligned_all && (g_path == 3 || (g_path == 0 && ptiles >= 16)))
         return launch_pipe<K, HAS_V, 0>(a, av, m, b, bv, n, out, outv, nullptr, nullptr, 0, ws,
                                             ws_bytes, s);
-    if (aligned_all && g_path == 2) {
-        const int limit = stream_grid_limit<K, HAS_V>();
-        const unsigned grid = unsigned(stiles < uint64_t(limit) ? stiles : uint64_t(limit));
-        stream_args args{a, av, m, b, bv, n, out, outv, stiles, g_trace, 0};
-        g_last_path = 2;
-        mark_before(s);
-        merge_stream_kernel<K, HAS_V><<<grid, SL::kThreads, SL::kSmem, s>>>(args);
-        mark_after(s);
-        return check_launch("comerge: streaming merge launch");
-    }
     constexpr int T = tile_cfg<K>::kTile;
     const uint64_t ntiles = div_up(total, T);
     const uint64_t nbound = ntiles + 1;
@@ -538,13 +533,12 @@ bool is_pinned_host(const void* p) {
     return attr.type == cudaMemoryTypeHost && attr.devicePointer == p;
 }
 
+// the synchronous entry points' stream (per host thread and device)
 cudaStream_t sync_stream() {
-    thread_local cudaStream_t s = [] {
-        cudaStream_t st = nullptr;
-        cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-        return st;
-    }();
-    return s;
+    thread_local cudaStream_t s[kMaxDevices] = {};
+    const int dev = current_device();
+    if (!s[dev]) cudaStreamCreateWithFlags(&s[dev], cudaStreamNonBlocking);
+    return s[dev];
 }
 
 // Device view of a possibly-host array (copied in on `s` when host).
@@ -643,9 +637,11 @@ struct host_streams {
     }
 };
 
-host_streams& hstreams() {
-    thread_local host_streams hs;
-    return hs;
+host_streams& hstreams() {  // per host thread and device
+    thread_local std::unique_ptr<host_streams> hs[kMaxDevices];
+    const int dev = current_device();
+    if (!hs[dev]) hs[dev].reset(new host_streams());
+    return *hs[dev];
 }
 
 template <typename K, bool HAS_V>
@@ -733,10 +729,14 @@ int merge_host_pipeline(const K* a, const uint32_t* av, uint64_t m, const K* b,
     // first |A window| outputs of a chunk, then the rest): 4 H2D + 4 matched
     // D2H commands per chunk measured 6.1 ms of copies on C2, 4 + 2 7.0 ms.
     auto h2d_copy = [&](void* dst, const void* src, size_t bytes) {
-        if (bytes) cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, hs.h2d);
+        if (!bytes || rc) return;
+        const cudaError_t ce = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, hs.h2d);
+        if (ce != cudaSuccess) rc = cuda_fail(ce, "comerge: host pipeline host->device copy");
     };
     auto d2h_copy = [&](void* dst, const void* src, size_t bytes) {
-        if (bytes) cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, hs.d2h);
+        if (!bytes || rc) return;
+        const cudaError_t ce = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, hs.d2h);
+        if (ce != cudaSuccess) rc = cuda_fail(ce, "comerge: host pipeline device->host copy");
     };
     for (uint64_t c = 0; c < nchunks && rc == COMERGE_OK; ++c) {
         const int sl = int(c % 3);
@@ -762,6 +762,7 @@ int merge_host_pipeline(const K* a, const uint32_t* av, uint64_t m, const K* b,
         *h2d += (i1 - i0) * (sizeof(K) + (HAS_V ? 4 : 0));
         cudaEventRecord(hs.in_done[sl], hs.h2d);
         if (trace) cudaEventRecord(tev[4 * c + 1], hs.h2d);
+        if (rc) break;
         cudaStreamWaitEvent(hs.comp, hs.in_done[sl], 0);
         if (first) {
             cudaEventRecord(hs.t0, hs.comp);
@@ -887,6 +888,13 @@ int merge_parallel_sync(const K* a, const uint32_t* av, size_t m, const K* b, co
     if (overlaps(a, m * sizeof(K), out, out_len * sizeof(K)) ||
         overlaps(b, n * sizeof(K), out, out_len * sizeof(K)))
         return fail(COMERGE_E_INVALID, std::string(who) + ": output must not alias an input");
+    if (HAS_V) {  // the payload arrays, as check_merge_args (every path below)
+        const size_t ob = out_len * sizeof(K), vb = out_len * sizeof(uint32_t);
+        if (overlaps(av, m * 4, outv, vb) || overlaps(bv, n * 4, outv, vb) ||
+            overlaps(a, m * sizeof(K), outv, vb) || overlaps(b, n * sizeof(K), outv, vb) ||
+            overlaps(av, m * 4, out, ob) || overlaps(bv, n * 4, out, ob) || overlaps(out, ob, outv, vb))
+            return fail(COMERGE_E_INVALID, std::string(who) + ": output must not alias an input");
+    }
     if (workers == 0)
         return fail(COMERGE_E_INVALID, "merge_parallel: worker count must be positive");
     const uint64_t total = m + n;
@@ -1265,12 +1273,12 @@ void comerge_cuda_set_kernel_events(void* before, void* after) {
 int comerge_cuda_abi_version(void) { return 10000; }
 
 size_t comerge_cuda_merge_workspace_bytes(size_t m, size_t n, int key_kind, int) {
-    return key_kind == COMERGE_KEY_U64 ? merge_ws_bytes<uint64_t>(m, n)
-                                       : merge_ws_bytes<uint32_t>(m, n);
+    return with_slack(key_kind == COMERGE_KEY_U64 ? merge_ws_bytes<uint64_t>(m, n)
+                                                  : merge_ws_bytes<uint32_t>(m, n));
 }
 size_t comerge_cuda_segmented_workspace_bytes(size_t total, size_t, int key_kind) {
-    return key_kind == COMERGE_KEY_U64 ? seg_ws_bytes<uint64_t>(total)
-                                       : seg_ws_bytes<uint32_t>(total);
+    return with_slack(key_kind == COMERGE_KEY_U64 ? seg_ws_bytes<uint64_t>(total)
+                                                  : seg_ws_bytes<uint32_t>(total));
 }
 
 #define COMERGE_KEYS(SUF, K)                                                                     \
@@ -1375,11 +1383,12 @@ int comerge_cuda_merge_segmented_u32(const uint32_t* a, const uint64_t* a_off, s
 }
 
 size_t comerge_cuda_sort_workspace_bytes(size_t n, int key_kind) {
-    return key_kind == COMERGE_KEY_U64 ? sort_ws_bytes<uint64_t>(n) : sort_ws_bytes<uint32_t>(n);
+    return with_slack(key_kind == COMERGE_KEY_U64 ? sort_ws_bytes<uint64_t>(n)
+                                                  : sort_ws_bytes<uint32_t>(n));
 }
 size_t comerge_cuda_sort_pairs_workspace_bytes(size_t n, int key_kind) {
-    return key_kind == COMERGE_KEY_U64 ? sort_pairs_ws_bytes<uint64_t>(n)
-                                       : sort_pairs_ws_bytes<uint32_t>(n);
+    return with_slack(key_kind == COMERGE_KEY_U64 ? sort_pairs_ws_bytes<uint64_t>(n)
+                                                  : sort_pairs_ws_bytes<uint32_t>(n));
 }
 int comerge_cuda_sort_pairs_i32(const int32_t* keys, const uint32_t* vals, size_t n,
                                 int32_t* out_keys, uint32_t* out_vals, void* ws, size_t ws_bytes,

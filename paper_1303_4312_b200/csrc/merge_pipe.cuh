@@ -39,7 +39,7 @@
 #include <cstdio>
 
 #include "corank.cuh"
-#include "merge_stream.cuh"
+#include "ptx.cuh"
 #include "merge_tile.cuh"
 #include "merge_serial.cuh"
 

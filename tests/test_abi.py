@@ -17,6 +17,15 @@ def test_library_exports_every_declared_symbol():
     missing = [s for s in names if not hasattr(N.lib, s)]
     assert not missing, missing
     assert N.lib.comerge_cuda_abi_version() == 10000
+    # the product exports no test infrastructure
+    assert not any(hasattr(N.lib, s) for s in N.declared_symbols(N.TESTKIT_HEADERS))
+
+
+def test_testkit_library_is_separate_and_complete():
+    names = N.declared_symbols(N.TESTKIT_HEADERS)
+    assert names and all(n.startswith("comerge_testkit_") for n in names)
+    missing = [s for s in names if not hasattr(N.tk(), s)]
+    assert not missing, missing
 
 
 def test_library_is_sm100a_cubin():

@@ -13,7 +13,7 @@ import paper_1303_4312_b200._native as N  # noqa: E402
 
 def keys(n, dt, width):
     raw = torch.empty(n, dtype=torch.int64, device="cuda")
-    N.check(N.lib.comerge_testkit_generate_raw(3, 0, n, width, raw.data_ptr(), None), True)
+    N.check(N.tk().comerge_testkit_generate_raw(3, 0, n, width, raw.data_ptr(), None), True)
     return raw.to(dt)
 
 
