@@ -1,23 +1,31 @@
 #!/usr/bin/env python3
 """Benchmark of the B200 stable merge on the BASELINE.json configs.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4]
+                    [--impl ours|reference] [--replicas]
 
 One "step" is one stable merge of one config's full synthetic input (already
 resident in HBM), timed with CUDA events on the launching stream; L2 is
-flushed (512 MiB write) between steps, outside the events.  The headline
-line is configs[1] of BASELINE.json (C2: key-value stability stress,
-m = n = 2^24); every other config is measured too and reported under
-"configs".  Metric: merged elements/s (+ achieved HBM GB/s vs the measured
-copy peak).
+flushed between steps (a 512 MiB read, outside the events, so no dirty flush
+lines are written back inside the timed merge).  The headline line is the
+largest BASELINE config (C4: uint64 keys + uint32 payload, m = n = 2^27;
+BASELINE's metric is per config, so the largest one is quoted); every other
+config is measured too and reported under "configs", each with its own CPU
+baseline (the reference at p = hardware_concurrency and p = 1) and its own
+end-to-end number through the host-buffer API.  Metric: merged elements/s
+(+ achieved HBM GB/s vs the measured copy peak).
 
 `--impl reference` times the reference's own CPU implementation
 (oracle/_ref/libcomerge_ref.so = /root/reference compiled unmodified:
-comerge::merge_parallel with hardware_concurrency threads) on the same
-config and prints the same JSON line with "impl": "reference".
+comerge::merge_parallel with hardware_concurrency threads, timed by its
+merge_report.wall_ns) on the same config, with inputs generated on the host by
+the reference's seeded recipe; that arm never loads this package or the GPU.
 
-Under torchrun (N > 1) every rank merges its own instance (seed + rank):
-weak scaling, no collective on the data path; times are the max over ranks.
+N > 1 (torchrun, or `--gpus N`, which relaunches itself under torchrun): by
+default ONE merge of the config is split across the N GPUs (Algorithm 2 with a
+worker per GPU; each rank merges its output range reading its peers' input
+pieces over NVLink; strong scaling); `--replicas` runs an independent instance
+per GPU instead (weak scaling).  Times are the max over ranks.
 """
 from __future__ import annotations
 
@@ -51,19 +59,9 @@ CONFIGS = {
     "C5": dict(kind="segmented", dtype="int32", nseg=2**14, maxlen=4096, width=2**20,
                desc="segmented batch: 2^14 pairs, m_s,n_s in [1,4096], int32 keys in [0,2^20)"),
 }
-# diagnostic shapes (not BASELINE configs; run only when named explicitly)
-EXTRA = {
-    "X1": dict(kind="keys", dtype="int32", m=2**26, n=2**26, width=2**31,
-               desc="diagnostic: int32 keys only, m=n=2^26, uniform [0,2^31)"),
-    "X2": dict(kind="pairs", dtype="int32", m=2**26, n=2**26, width=2**31,
-               desc="diagnostic: int32 keys + payload, m=n=2^26, uniform [0,2^31)"),
-    "X3": dict(kind="segmented", dtype="int32", nseg=2**20, maxlen=64, width=2**20,
-               desc="diagnostic: segmented batch of 2^20 small pairs, m_s,n_s in [1,64]"),
-    "X4": dict(kind="segmented", dtype="int32", nseg=2**21, maxlen=16, width=2**20,
-               desc="diagnostic: segmented batch of 2^21 tiny pairs, m_s,n_s in [1,16]"),
-}
-HEADLINE = "C2"
+HEADLINE = "C4"
 SEED = 5
+METRIC = "merged elements/s"
 
 
 def key_bytes(cfg):
@@ -75,10 +73,39 @@ def elem_bytes(cfg):
     return key_bytes(cfg) + (4 if c["kind"] == "pairs" else 0)
 
 
+def dtype_str(cfg):
+    c = CONFIGS[cfg]
+    k = {"int32": "int32", "uint64": "u64"}[c["dtype"]]
+    return k + ("+u32 payload" if c["kind"] == "pairs" else "")
+
+
+def scaling_of(world, replicas):
+    return "strong" if world > 1 and not replicas else "weak"
+
+
+def config_dict(cfg, elements, world, split):
+    """The `config` object of both arms' lines (identical by construction)."""
+    if world == 1:
+        par = "1 GPU"
+    elif split:
+        par = (f"{world} GPUs, one merge split by output rank (Algorithm 2, a worker per GPU, "
+               "peer windows over NVLink)")
+    else:
+        par = f"{world} GPUs, independent instance per GPU"
+    balg = 2 * elements * elem_bytes(cfg)
+    return dict(workload=f"{cfg}: {CONFIGS[cfg]['desc']}", elements=int(elements),
+                parallelism=par,
+                l2=(f"inputs+outputs {balg / 2**30:.2f} GiB per step (> 126 MB L2); L2 also "
+                    if balg > 126e6 else
+                    f"inputs+outputs {balg / 2**20:.1f} MiB per step (fit in L2); L2 ")
+                + "flushed between steps (512 MiB read, outside the timed events)")
+
+
 # ------------------------------------------------------------------ inputs
 
 def make_inputs(cfg, seed=SEED, device="cuda"):
-    """Seeded inputs on the device (splitmix64 recipe of generate.cpp:17-29)."""
+    """Seeded inputs on the device (splitmix64 recipe of generate.cpp:17-29,
+    the testkit library's generator, pinned to the reference's by test)."""
     import torch
     from paper_1303_4312_b200 import testkit as tk
     c = CONFIGS[cfg]
@@ -105,6 +132,36 @@ def make_inputs(cfg, seed=SEED, device="cuda"):
             inp["av"] = tk.iota(c["m"], 0, device=device)
             inp["bv"] = tk.iota(c["n"], 1 << 31, device=device)
         return inp
+
+
+def make_host_inputs(cfg, seed=SEED):
+    """The same seeded inputs generated on the host (the reference arm: no GPU,
+    no package import) by the C restatement of the reference's generator
+    (oracle/comerge_oracle.c, pinned against the reference's own generator by
+    tests/test_oracle.py)."""
+    from oracle.py import Port
+    port = Port()
+    c = CONFIGS[cfg]
+    dt = {"int32": np.int32, "uint64": np.uint64}[c["dtype"]]
+    if c["kind"] == "segmented":
+        sizes = port.generate_raw(seed, 2, 2 * c["nseg"], c["maxlen"]).astype(np.int64) + 1
+        ms, ns = sizes[0::2], sizes[1::2]
+        a_off = np.concatenate([[0], np.cumsum(ms)]).astype(np.uint64)
+        b_off = np.concatenate([[0], np.cumsum(ns)]).astype(np.uint64)
+        out = {"a_off": a_off, "b_off": b_off}
+        for side, off, lane in (("a", a_off, 0), ("b", b_off, 1)):
+            raw = port.generate_raw(seed, lane, int(off[-1]), c["width"]).astype(dt)
+            for s in range(c["nseg"]):
+                raw[int(off[s]):int(off[s + 1])].sort()
+            out[side] = raw
+        return out
+    la, lb = (1, 0) if c.get("swapped") else (0, 1)
+    h = dict(a=port.generate_sorted(dt, seed, la, c["m"], c["width"]),
+             b=port.generate_sorted(dt, seed, lb, c["n"], c["width"]))
+    if c["kind"] == "pairs":
+        h["av"] = np.arange(c["m"], dtype=np.uint32)
+        h["bv"] = np.arange(c["n"], dtype=np.uint32) | np.uint32(1 << 31)
+    return h
 
 
 def alloc_outputs(cfg, inp):
@@ -144,13 +201,14 @@ def run_config(cfg, inp, out=None):
     return out
 
 
-KERNEL_NAMES = {1: "merge_tile_kernel (+ partition_kernel)", 2: "merge_stream_kernel",
-                3: "merge_pipe_kernel", 4: "seg_merge_tile_kernel (+ seg_partition_kernel)",
-                5: "merge_pipe_kernel (segmented)"}
+KERNEL_NAMES = {1: "merge_tile_kernel (+ partition_kernel)", 3: "merge_pipe_kernel",
+                4: "seg_merge_tile_kernel (+ seg_partition_kernel)",
+                5: "merge_pipe_kernel (segmented)", 7: "merge_pipe_kernel (pieced range)",
+                8: "merge_small_kernel"}
 
 
 def launches_per_step(path):
-    return 1 if path in (2, 3, 5) else 2  # persistent kernels: one launch; tile paths: two
+    return 2 if path in (1, 4) else 1  # persistent / single kernels: one launch
 
 
 # ------------------------------------------------------------------ clocks
@@ -265,22 +323,36 @@ def traffic_for(cfg):
         return None
 
 
-def time_config(cfg, steps, warmup, device, seed=SEED, dist_ctx=None, clocks=False):
+class L2Flush:
+    """Evicts L2 (126 MB) between steps by READING a 512 MiB buffer: the lines
+    left in L2 are clean, so the next merge does not pay for writing back
+    dirty flush lines (a write-based flush left up to ~126 MB dirty)."""
+
+    def __init__(self, device):
+        import torch
+        self.buf = torch.zeros(512 * 2**20 // 8, dtype=torch.int64, device=device)
+        self.sink = torch.zeros((), dtype=torch.int64, device=device)
+
+    def __call__(self):
+        import torch
+        torch.sum(self.buf, dim=0, out=self.sink)
+
+
+def time_steps(step, steps, warmup, device, flush, dist_ctx=None, clocks=False,
+               kernel_events=True):
+    """Device time of `step` (enqueues one unit of work on the current stream):
+    per-step events on the launching stream, L2 flushed outside them; then the
+    same steps with events recorded by the library right around the merge
+    kernel (the roofline's kernel time)."""
     import torch
     import paper_1303_4312_b200._native as N
-    inp = make_inputs(cfg, seed=seed, device=device)
-    out = alloc_outputs(cfg, inp)
-    total = inp["a"].numel() + inp["b"].numel()
-    flush = torch.empty(512 * 2**20 // 4, dtype=torch.int32, device=device)
     stream = torch.cuda.current_stream(device)
-    # warm-up steps are the timed step exactly (flush, events, merge), untimed:
-    # the first flush launch of a process otherwise lands in timed step 0
-    # (seen: +113 us on the first step of a fresh process, lazy module load)
     wev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    for k in range(max(warmup, 0)):
-        flush.fill_(k)
+    # warm-up steps are the timed step exactly (flush, events, merge), untimed
+    for _ in range(max(warmup, 0)):
+        flush()
         wev[0].record(stream)
-        run_config(cfg, inp, out)
+        step()
         wev[1].record(stream)
     torch.cuda.synchronize(device)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] + list(raw_events(2))
@@ -295,36 +367,41 @@ def time_config(cfg, steps, warmup, device, seed=SEED, dist_ctx=None, clocks=Fal
     # device starts them: step events then time device work, not host enqueue
     torch.cuda._sleep(int(2e8))
     for k in range(steps):
-        flush.fill_(k)  # evict L2 (> 126 MB) outside the timed events
-        s0, s1 = ev[k][0], ev[k][1]
-        s0.record(stream)
-        run_config(cfg, inp, out)
-        s1.record(stream)
+        flush()
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
     torch.cuda.synchronize(device)
     if dist_ctx:
         dist_ctx.barrier()
     if sampler:
         sampler.__exit__()
-    # the same steps again with events recorded by the library right around
-    # the merge kernel (the roofline's kernel time; kept out of the steps
-    # above because every extra event costs ~2.7 us on this platform)
-    torch.cuda._sleep(int(2e8))
-    for k in range(steps):
-        flush.fill_(k)
-        k0, k1 = ev[k][2], ev[k][3]
-        N.lib.comerge_cuda_set_kernel_events(k0, k1)
-        run_config(cfg, inp, out)
-        N.lib.comerge_cuda_set_kernel_events(None, None)
-    torch.cuda.synchronize(device)
-    path = N.lib.comerge_cuda_last_path()
+    kern_ms = None
+    if kernel_events:
+        torch.cuda._sleep(int(2e8))
+        for k in range(steps):
+            flush()
+            N.lib.comerge_cuda_set_kernel_events(ev[k][2], ev[k][3])
+            step()
+            N.lib.comerge_cuda_set_kernel_events(None, None)
+        torch.cuda.synchronize(device)
+        kern_ms = [raw_elapsed_ms(e[2], e[3]) for e in ev]
     step_ms = [e[0].elapsed_time(e[1]) for e in ev]
-    kern_ms = [raw_elapsed_ms(e[2], e[3]) for e in ev]
-    res = dict(total=total, step_ms=step_ms, kern_ms=kern_ms, path=path,
-               clocks=sampler.summary() if sampler else None, inp=inp, out=out)
+    return dict(step_ms=step_ms, kern_ms=kern_ms, path=N.lib.comerge_cuda_last_path(),
+                clocks=sampler.summary() if sampler else None)
+
+
+def time_config(cfg, steps, warmup, device, flush, seed=SEED, dist_ctx=None, clocks=False):
+    inp = make_inputs(cfg, seed=seed, device=device)
+    out = alloc_outputs(cfg, inp)
+    res = time_steps(lambda: run_config(cfg, inp, out), steps, warmup, device, flush, dist_ctx,
+                     clocks)
+    res.update(total=inp["a"].numel() + inp["b"].numel(), inp=inp, out=out)
     return res
 
 
-def summarize(cfg, res, peak, n_gpus=1, max_step_total_ms=None):
+def summarize(cfg, res, peak, n_units=1, max_step_total_ms=None):
+    """n_units: instances merged per step over the whole job (replicas)."""
     total = res["total"]
     balg = 2 * total * elem_bytes(cfg)
     step_total = max_step_total_ms if max_step_total_ms is not None else sum(res["step_ms"])
@@ -332,9 +409,8 @@ def summarize(cfg, res, peak, n_gpus=1, max_step_total_ms=None):
     ms_step = step_total / steps
     kern = statistics.mean(res["kern_ms"])
     return dict(
-        workload=CONFIGS[cfg]["desc"], m=int(res["inp"]["a"].numel()),
-        n=int(res["inp"]["b"].numel()), elements=total,
-        elements_per_s=n_gpus * total * steps / (step_total * 1e-3),
+        workload=CONFIGS[cfg]["desc"], elements=total,
+        elements_per_s=n_units * total * steps / (step_total * 1e-3),
         ms_per_step=ms_step, step_gbs=balg / (ms_step * 1e-3) / 1e9,
         merge_kernel_ms=kern, merge_kernel_gbs=balg / (kern * 1e-3) / 1e9,
         frac_of_peak=balg / (kern * 1e-3) / 1e9 / peak,
@@ -345,28 +421,42 @@ def summarize(cfg, res, peak, n_gpus=1, max_step_total_ms=None):
 
 # ------------------------------------------------------------- CPU legs
 
-def host_arrays(cfg, inp):
-    """Device inputs -> host numpy (+ AoS {key,val} for key-value configs)."""
-    from oracle.py import to_aos
-    h = {k: v.cpu().numpy() for k, v in inp.items()}
-    if CONFIGS[cfg]["kind"] == "pairs":
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def with_aos(cfg, h):
+    """Key-value configs in the reference's own call shape: {key, val} structs
+    with a key-only less (oracle.hpp:22-37)."""
+    if CONFIGS[cfg]["kind"] == "pairs" and "a_aos" not in h:
+        from oracle.py import to_aos
         h["a_aos"] = to_aos(h["a"], h["av"])
         h["b_aos"] = to_aos(h["b"], h["bv"])
     return h
 
 
 def cpu_reference_run(cfg, h, threads):
-    """One run of the reference's CPU path on host arrays; returns wall ns
-    (merge_report.wall_ns: the parallel region only, parallel.hpp:252-267)."""
+    """One run of the reference's CPU path on host arrays; returns (wall ns,
+    kind): merge_report.wall_ns, the parallel region only (parallel.hpp:252-267).
+    C5: the reference has no batched API -- pairs round-robin over `threads`
+    std::threads, each calling comerge::stable_merge (merge.hpp:52-68)."""
     from oracle.py import Ref, available_ref, Port
     kind = CONFIGS[cfg]["kind"]
     if available_ref():
         ref = Ref()
         if kind == "segmented":
+            o = h.setdefault("out", np.empty(len(h["a"]) + len(h["b"]), h["a"].dtype))
             return ref.merge_segmented(h["a"], h["a_off"], h["b"], h["b_off"], threads=threads,
-                                       out=h.setdefault("out", np.empty(len(h["a"]) + len(h["b"]),
-                                                                        h["a"].dtype)))[1], "reference"
+                                       out=o)[1], "reference"
         if kind == "pairs":
+            with_aos(cfg, h)
             o = h.setdefault("out_aos", np.zeros(len(h["a_aos"]) + len(h["b_aos"]),
                                                  h["a_aos"].dtype))
             return ref.merge_parallel_kv(h["a_aos"], h["b_aos"], threads, out=o)[1].wall_ns, \
@@ -391,36 +481,46 @@ def cpu_threads():
     return os.cpu_count() or 1
 
 
-def cpu_baseline(cfg, inp, budget_s=20.0, min_reps=3, max_reps=15):
-    h = host_arrays(cfg, inp)
-    threads = cpu_threads()
-    cpu_reference_run(cfg, h, threads)  # touch output pages
+def cpu_sample(cfg, h, threads, budget_s, min_reps=3, max_reps=15):
+    cpu_reference_run(cfg, h, threads)  # warm: touch output pages
     walls, kind = [], "reference"
     t_start = time.time()
-    while len(walls) < max_reps and (len(walls) < min_reps or time.time() - t_start < budget_s / 4):
+    while len(walls) < max_reps and (len(walls) < min_reps or time.time() - t_start < budget_s):
         w, kind = cpu_reference_run(cfg, h, threads)
         walls.append(w)
-        if time.time() - t_start > budget_s:
-            break
+    return walls, kind
+
+
+def cpu_baseline(cfg, h, budget_s=4.0, p1_budget_s=8.0):
+    """The reference at p = hardware_concurrency (the baseline) and p = 1 on
+    the full workload: median (primary) and min of >= 3
+    runs of merge_report.wall_ns."""
     total = len(h["a"]) + len(h["b"])
-    med = statistics.median(walls)
+    threads = cpu_threads()
+    walls, kind = cpu_sample(cfg, h, threads, budget_s)
+    walls1, _ = cpu_sample(cfg, h, 1, p1_budget_s, min_reps=1, max_reps=5)
+    med, med1 = statistics.median(walls), statistics.median(walls1)
     return dict(value=total / (med * 1e-9), unit="elements/s", cores=threads, kind=kind,
                 sample=f"full {cfg} workload ({total} elements), median of {len(walls)} runs of "
-                       f"the reference's merge_report.wall_ns, {threads} threads "
-                       f"(std::thread::hardware_concurrency)",
-                median_ms=med / 1e6, min_ms=min(walls) / 1e6)
+                       f"the reference's merge_report.wall_ns at {threads} threads "
+                       "(std::thread::hardware_concurrency)"
+                       + ("; pairs round-robin over the threads, stable_merge each (no batched "
+                          "reference API)" if CONFIGS[cfg]["kind"] == "segmented" else ""),
+                median_ms=med / 1e6, min_ms=min(walls) / 1e6,
+                p1=dict(value=total / (med1 * 1e-9), median_ms=med1 / 1e6,
+                        min_ms=min(walls1) / 1e6, runs=len(walls1)),
+                cpu_model=cpu_model())
 
 
 # ------------------------------------------------------------------- e2e
 
 def e2e_measure(cfg, inp, steps, warmup):
-    """Same metric through the host-buffer C ABI (comerge_merge_parallel_*):
-    pinned host inputs, H2D + merge + D2H inside every timed call."""
+    """The same metric through the host-buffer C ABI (comerge_merge_parallel_*
+    / comerge_merge_segmented_host_*): pinned host inputs, H2D + merge + D2H
+    inside every timed call; the result must equal the device path's."""
     import torch
     import paper_1303_4312_b200._native as N
     c = CONFIGS[cfg]
-    if c["kind"] == "segmented":
-        return None
     suf = {"int32": "i32", "uint64": "u64"}[c["dtype"]]
     pin = {k: v.cpu().pin_memory() for k, v in inp.items()}
     total = inp["a"].numel() + inp["b"].numel()
@@ -429,16 +529,30 @@ def e2e_measure(cfg, inp, steps, warmup):
     rep = N.MergeReport()
     p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
 
-    def call():
-        if c["kind"] == "pairs":
-            rc = getattr(N.lib, f"comerge_merge_parallel_pairs_{suf}")(
+    if c["kind"] == "segmented":
+        fn = getattr(N.lib, f"comerge_merge_segmented_host_{suf}", None)
+        if fn is None:
+            return None
+        nseg = pin["a_off"].numel() - 1
+        path = f"comerge_merge_segmented_host_{suf} (host pinned buffers)"
+
+        def call():
+            N.check(fn(p(pin["a"]), p(pin["a_off"]), pin["a"].numel(), p(pin["b"]),
+                       p(pin["b_off"]), pin["b"].numel(), nseg, p(ok), total, C.byref(rep)))
+    elif c["kind"] == "pairs":
+        path = f"comerge_merge_parallel_pairs_{suf} (host pinned buffers)"
+
+        def call():
+            N.check(getattr(N.lib, f"comerge_merge_parallel_pairs_{suf}")(
                 p(pin["a"]), p(pin["av"]), pin["a"].numel(), p(pin["b"]), p(pin["bv"]),
-                pin["b"].numel(), p(ok), p(ov), total, 1, C.byref(rep))
-        else:
-            rc = getattr(N.lib, f"comerge_merge_parallel_{suf}")(
-                p(pin["a"]), pin["a"].numel(), p(pin["b"]), pin["b"].numel(), p(ok), total, 1, 0,
-                C.byref(rep), None, None)
-        N.check(rc)
+                pin["b"].numel(), p(ok), p(ov), total, 1, C.byref(rep)))
+    else:
+        path = f"comerge_merge_parallel_{suf} (host pinned buffers)"
+
+        def call():
+            N.check(getattr(N.lib, f"comerge_merge_parallel_{suf}")(
+                p(pin["a"]), pin["a"].numel(), p(pin["b"]), pin["b"].numel(), p(ok), total, 1,
+                0, C.byref(rep), None, None))
 
     for _ in range(max(1, warmup)):
         call()
@@ -447,16 +561,15 @@ def e2e_measure(cfg, inp, steps, warmup):
         t0 = time.perf_counter()
         call()
         times.append(time.perf_counter() - t0)
-    # the e2e result must equal the device-path result
-    dev_keys = run_config(cfg, inp)["keys"].cpu()
-    assert bool((ok.view(torch.uint8) == dev_keys.view(torch.uint8)).all()), "e2e mismatch"
-    # median call: one slow call (a PCIe hiccup, seen up to +20%) would move a
-    # mean of a handful of calls by several percent
-    return dict(value=total / statistics.median(times), unit="elements/s", stat=f"median of {steps} calls",
+    dev = run_config(cfg, inp)
+    torch.cuda.synchronize()
+    assert bool((ok.view(torch.uint8) == dev["keys"].cpu().view(torch.uint8)).all()), "e2e keys"
+    if ov is not None:
+        assert bool((ov == dev["vals"].cpu()).all()), "e2e payloads"
+    med = statistics.median(times)
+    return dict(value=total / med, unit="elements/s", stat=f"median of {steps} calls",
                 h2d_bytes_per_step=int(rep.h2d_bytes), d2h_bytes_per_step=int(rep.d2h_bytes),
-                ms_per_step=1e3 * statistics.median(times),
-                path=f"comerge_merge_parallel{'_pairs' if c['kind'] == 'pairs' else ''}_{suf} "
-                     "(host pinned buffers)")
+                ms_per_step=1e3 * med, path=path)
 
 
 # ------------------------------------------------------------------ main
@@ -473,18 +586,26 @@ def dist_setup():
     return dist, dist.get_rank(), world, local
 
 
+def relaunch_under_torchrun(n):
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def reference_arm(args):
-    dist, rank, world, local = dist_setup()
+    """CPU only: the compiled reference on host-generated inputs (this arm
+    never imports the package, torch or CUDA)."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
-        if dist:
-            dist.barrier()
-            dist.destroy_process_group()
         return
-    import torch
-    device = torch.device("cuda", local)
     cfg = args.config
-    inp = make_inputs(cfg, device=device)
-    h = host_arrays(cfg, inp)
+    h = make_host_inputs(cfg)
     threads = cpu_threads()
     for _ in range(max(args.warmup, 1)):
         cpu_reference_run(cfg, h, threads)
@@ -493,29 +614,32 @@ def reference_arm(args):
         w, kind = cpu_reference_run(cfg, h, threads)
         walls.append(w)
     total = len(h["a"]) + len(h["b"])
+    # same statistic as the GPU arm: total work / total time of the K steps
     value = total * len(walls) / (sum(walls) * 1e-9)
-    line = dict(metric="merged elements/s", value=value, unit="elements/s", n_gpus=world,
+    line = dict(metric=METRIC, value=value, unit="elements/s", n_gpus=world,
                 steps=args.steps, warmup=args.warmup,
                 ms_per_step=sum(walls) / len(walls) / 1e6, higher_is_better=True,
-                scaling="weak", vs_baseline=None, dtype=CONFIGS[cfg]["dtype"], data="synthetic",
-                impl="reference",
-                config=dict(workload=f"{cfg}: {CONFIGS[cfg]['desc']}", elements=total,
-                            l2="n/a (CPU)"),
+                scaling=scaling_of(world, args.replicas),
+                vs_baseline=None, dtype=dtype_str(cfg), data="synthetic (seeded splitmix64, "
+                "generate.cpp recipe)", impl="reference",
+                config=config_dict(cfg, total, world, world > 1 and not args.replicas),
                 cpu_baseline=dict(value=value, unit="elements/s", cores=threads, kind=kind,
-                                  sample=f"full {cfg} workload per step, reference "
-                                         "comerge::merge_parallel, merge_report.wall_ns"),
+                                  sample=f"full {cfg} workload per step: reference "
+                                         "comerge::merge_parallel"
+                                         + (" ({key,val} structs, key-only less)"
+                                            if CONFIGS[cfg]["kind"] == "pairs" else "")
+                                         + f" at {threads} threads, merge_report.wall_ns",
+                                  cpu_model=cpu_model()),
                 e2e=dict(value=value, unit="elements/s", h2d_bytes_per_step=0,
                          d2h_bytes_per_step=0))
     print(json.dumps(line), flush=True)
-    if dist:
-        dist.barrier()
-        dist.destroy_process_group()
 
 
-def sort_extras(device, reps=5):
+def sort_extras(device, flush, reps=5):
     """SURVEY 8f row 1 (not a BASELINE config): the stable merge sorts on
     2^26 int32 keys (uniform 31-bit, seeded) with and without uint32 payloads,
-    median device time (events, L2 flushed before each rep)."""
+    median device time (events, L2 flushed before each rep), next to CUB's
+    merge and radix sorts of the same keys (library baselines, testkit)."""
     import torch
     import paper_1303_4312_b200 as P
     import paper_1303_4312_b200._native as N
@@ -529,12 +653,11 @@ def sort_extras(device, reps=5):
     ws = torch.empty(max(P.sort_workspace_bytes(n, torch.int32),
                          P.sort_pairs_workspace_bytes(n, torch.int32)), dtype=torch.uint8,
                      device=device)
-    flush = torch.empty(512 * 2**20 // 4, dtype=torch.int32, device=device)
 
     def med(fn):
         ts = []
         for r in range(reps + 2):
-            flush.fill_(r)
+            flush()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             fn()
@@ -549,9 +672,75 @@ def sort_extras(device, reps=5):
     out = {"workload": "2^26 int32 keys, uniform [0, 2^31), seeded; stable merge sort",
            "keys_ms": t_keys, "keys_per_s": n / (t_keys * 1e-3),
            "pairs_ms": t_pairs, "pairs_per_s": n / (t_pairs * 1e-3)}
-    del k, v, ok, ov, ws, flush
+    # library baselines on the same keys (CUB, in the testkit library)
+    tkl = N.tk()
+    need = int(tkl.comerge_testkit_cub_sort_bytes(n))
+    tmp = torch.empty(max(need, 1), dtype=torch.uint8, device=device)
+    for alg, name in {0: "cub_radix_keys", 1: "cub_radix_pairs", 2: "cub_merge_keys",
+                      3: "cub_merge_pairs"}.items():
+        def run(alg=alg):
+            N.check(tkl.comerge_testkit_cub_sort(
+                alg, C.c_void_p(k.data_ptr()), C.c_void_p(v.data_ptr()), C.c_void_p(ok.data_ptr()),
+                C.c_void_p(ov.data_ptr()), n, C.c_void_p(tmp.data_ptr()), need, None), True)
+        out[f"{name}_ms"] = med(run)
+    del tmp
+    del k, v, ok, ov, ws
     torch.cuda.empty_cache()
     return out
+
+
+def run_split(args, dist, rank, world, device, peak, flush):
+    """ONE merge of the config split across the ranks (Algorithm 2 with a
+    worker per GPU): rank r holds the r-th piece of A and B (cut at r/world,
+    a multiple of 4 elements) and merges its output range, reading the peers'
+    pieces over NVLink.  value = the whole merge / the max over ranks."""
+    import torch
+    from paper_1303_4312_b200.shard import DistributedMerge
+    cfg = args.config
+    if CONFIGS[cfg]["kind"] == "segmented":
+        raise SystemExit("--split: plain merges only (C5 is a batch: use --replicas)")
+    full = make_inputs(cfg, seed=SEED, device=device)
+
+    def piece(t, length):
+        lo = (length * rank // world) // 4 * 4
+        hi = length if rank == world - 1 else (length * (rank + 1) // world) // 4 * 4
+        return t[lo:hi].clone()
+
+    m, n = full["a"].numel(), full["b"].numel()
+    pa, pb = piece(full["a"], m), piece(full["b"], n)
+    pav = piece(full["av"], m) if "av" in full else None
+    pbv = piece(full["bv"], n) if "bv" in full else None
+    del full
+    torch.cuda.empty_cache()
+    dm = DistributedMerge(pa, pb, a_vals=pav, b_vals=pbv)
+
+    class Ctx:
+        def barrier(self):
+            dist.barrier()
+
+    res = time_steps(dm.run, args.steps, args.warmup, device, flush, Ctx(), clocks=(rank == 0))
+    t = torch.tensor([sum(res["step_ms"]), statistics.mean(res["kern_ms"])],
+                     dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_total, kern = float(t[0].item()), float(t[1].item())
+    dm.close()
+    total = m + n
+    balg = 2 * total * elem_bytes(cfg)
+    if rank == 0:
+        ms = step_total / args.steps
+        line = dict(
+            metric=METRIC, value=total * args.steps / (step_total * 1e-3), unit="elements/s",
+            n_gpus=world, steps=args.steps, warmup=args.warmup, ms_per_step=ms,
+            higher_is_better=True, scaling="strong", vs_baseline=None, dtype=dtype_str(cfg),
+            data="synthetic (seeded splitmix64, generate.cpp recipe)",
+            config=config_dict(cfg, total, world, True),
+            roofline=dict(bound="hbm", achieved=balg / world / (kern * 1e-3) / 1e9, peak=peak,
+                          unit="GB/s", frac=balg / world / (kern * 1e-3) / 1e9 / peak,
+                          traffic=None, kernel="merge_pipe_kernel (pieced range, per rank)",
+                          algorithmic_bytes_per_launch=balg // world),
+            cpu_baseline=None, e2e=None, clocks=res["clocks"],
+            gpu_launches=args.steps * launches_per_step(res["path"]))
+        print(json.dumps(line), flush=True)
 
 
 def main():
@@ -561,20 +750,33 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default=HEADLINE, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--only-headline", action="store_true",
-                    help="skip the per-config table")
-    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: an independent instance per GPU instead of one split merge")
+    ap.add_argument("--only-headline", action="store_true", help="skip the per-config table")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline legs")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sorts", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return reference_arm(args)
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1:
+        return sys.exit(relaunch_under_torchrun(args.gpus))
+    if env_world is not None and int(env_world) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_world}")
 
     import torch
     dist, rank, world, local = dist_setup()
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
     peak, peak_src = peak_hbm()
+    flush = L2Flush(device)
+    if world > 1 and not args.replicas:
+        run_split(args, dist, rank, world, device, peak, flush)
+        dist.barrier()
+        dist.destroy_process_group()
+        return
 
     class Ctx:
         def barrier(self):
@@ -583,48 +785,56 @@ def main():
 
     ctx = Ctx() if dist else None
     cfg = args.config
-    res = time_config(cfg, args.steps, args.warmup, device, seed=SEED + rank, dist_ctx=ctx,
-                      clocks=(rank == 0))
+    res = time_config(cfg, args.steps, args.warmup, device, flush, seed=SEED + rank,
+                      dist_ctx=ctx, clocks=(rank == 0))
     step_total = sum(res["step_ms"])
     if dist:
         t = torch.tensor([step_total], dtype=torch.float64, device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         step_total = float(t.item())
-    head = summarize(cfg, res, peak, n_gpus=world, max_step_total_ms=step_total)
+    head = summarize(cfg, res, peak, n_units=world, max_step_total_ms=step_total)
+    legs = rank == 0 and world == 1  # CPU / e2e legs: rank 0 at N = 1 only
 
+    def extras(c, r):
+        d = {}
+        if legs and not args.no_e2e:
+            d["e2e"] = e2e_measure(c, r["inp"], max(5, min(args.steps, 9)), 1)
+        if legs and not args.no_cpu:
+            d["cpu_baseline"] = cpu_baseline(c, {k: v.cpu().numpy() for k, v in r["inp"].items()})
+        return d
+
+    head_extras = extras(cfg, res)
     per_config = {}
     if not args.only_headline:
         for other in CONFIGS:
             if other == cfg:
-                per_config[other] = {k: v for k, v in head.items()}
-                per_config[other]["elements_per_s"] = head["elements_per_s"] / world
+                per_config[other] = dict(head, elements_per_s=head["elements_per_s"] / world,
+                                         **head_extras)
                 continue
-            r = time_config(other, min(args.steps, 10), 3, device, seed=SEED + rank)
-            per_config[other] = summarize(other, r, peak)
+            r = time_config(other, min(args.steps, 10), 3, device, flush, seed=SEED + rank)
+            per_config[other] = dict(summarize(other, r, peak), **extras(other, r))
             del r
             torch.cuda.empty_cache()
-
-    sorts = None if args.only_headline else sort_extras(device)
-    e2e = None if args.no_e2e or rank != 0 else e2e_measure(cfg, res["inp"], max(5, min(args.steps, 9)), 1)
-    cpu = None if args.no_cpu or rank != 0 else cpu_baseline(cfg, res["inp"])
+    del res["inp"], res["out"]
+    torch.cuda.empty_cache()
+    sorts = None if args.only_headline or args.no_sorts else sort_extras(device, flush)
     if rank == 0:
         line = dict(
-            metric="merged elements/s", value=head["elements_per_s"], unit="elements/s",
+            metric=METRIC, value=head["elements_per_s"], unit="elements/s",
             n_gpus=world, steps=args.steps, warmup=args.warmup, ms_per_step=head["ms_per_step"],
-            higher_is_better=True, scaling="weak", vs_baseline=None,
-            dtype=CONFIGS[cfg]["dtype"] + ("+u32 payload" if CONFIGS[cfg]["kind"] == "pairs" else ""),
+            higher_is_better=True, scaling="weak", vs_baseline=None, dtype=dtype_str(cfg),
             data="synthetic (seeded splitmix64, generate.cpp recipe)",
-            config=dict(workload=f"{cfg}: {CONFIGS[cfg]['desc']}", elements=head["elements"],
-                        parallelism=f"{world} GPU(s), independent instance per GPU",
-                        l2="flushed between steps (512 MiB write, outside the events)"),
+            config=config_dict(cfg, head["elements"], world, False),
             roofline=dict(bound="hbm", achieved=head["merge_kernel_gbs"], peak=peak,
                           unit="GB/s", frac=head["frac_of_peak"], traffic=traffic_for(cfg),
                           kernel=head["kernel"], peak_source=peak_src,
                           algorithmic_bytes_per_launch=head["algorithmic_bytes"],
                           step_gbs=head["step_gbs"], frac_of_8tbs=head["frac_of_8tbs"]),
-            cpu_baseline=cpu, e2e=e2e, clocks=res["clocks"],
-            gpu_launches=args.steps * head["launches_per_step"],
+            cpu_baseline=head_extras.get("cpu_baseline"), e2e=head_extras.get("e2e"),
+            clocks=res["clocks"], gpu_launches=args.steps * head["launches_per_step"],
             configs=per_config, sorts=sorts)
+        if world > 1:
+            line["scaling_note"] = "replicas: an independent instance per GPU (seed + rank)"
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()

@@ -62,6 +62,15 @@ int comerge_testkit_checksum(int key_kind, const void* keys, size_t len,
 int comerge_testkit_count_unsorted(int key_kind, const void* keys, size_t len,
                                    unsigned long long* acc, comerge_stream_t stream);
 
+/* Library baselines for the merge sort (bench.py "sorts"): CUB on int32 keys
+ * (+ uint32 payloads).  alg 0: DeviceRadixSort::SortKeys, 1: SortPairs,
+ * 2: DeviceMergeSort::SortKeysCopy (std::less), 3: SortPairsCopy.  tmp holds
+ * comerge_testkit_cub_sort_bytes(n) bytes (the largest of the four). */
+size_t comerge_testkit_cub_sort_bytes(size_t n);
+int comerge_testkit_cub_sort(int alg, const int32_t* keys, const uint32_t* vals,
+                             int32_t* out_keys, uint32_t* out_vals, size_t n, void* tmp,
+                             size_t tmp_bytes, comerge_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

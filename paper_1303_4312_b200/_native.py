@@ -119,6 +119,9 @@ def tk():
         t.comerge_testkit_verify_pairs.argtypes = [_i, _p, _sz, _p, _sz, _p, _p, _p, _p]
         t.comerge_testkit_checksum.argtypes = [_i, _p, _sz, _p, _p]
         t.comerge_testkit_count_unsorted.argtypes = [_i, _p, _sz, _p, _p]
+        t.comerge_testkit_cub_sort_bytes.argtypes = [_sz]
+        t.comerge_testkit_cub_sort_bytes.restype = _sz
+        t.comerge_testkit_cub_sort.argtypes = [_i, _p, _p, _p, _p, _sz, _p, _sz, _p]
         _tk = t
     return _tk
 

@@ -11,6 +11,7 @@
 // it equals the reference's std::sort, generate.cpp:27).
 #include <cuda_runtime.h>
 
+#include <cub/device/device_merge_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_segmented_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
@@ -378,6 +379,47 @@ int comerge_testkit_count_unsorted(int key_kind, const void* keys, size_t len,
     }
     const cudaError_t e = cudaGetLastError();
     return e ? tk_fail(e, "testkit: unsorted") : COMERGE_OK;
+}
+
+namespace {
+struct less_i32 {
+    __device__ bool operator()(int32_t x, int32_t y) const { return x < y; }
+};
+
+cudaError_t cub_sort(int alg, const int32_t* k, const uint32_t* v, int32_t* ok, uint32_t* ov,
+                     size_t n, void* tmp, size_t& bytes, cudaStream_t s) {
+    const int nn = int(n);
+    switch (alg) {
+        case 0: return cub::DeviceRadixSort::SortKeys(tmp, bytes, k, ok, nn, 0, 32, s);
+        case 1: return cub::DeviceRadixSort::SortPairs(tmp, bytes, k, ok, v, ov, nn, 0, 32, s);
+        case 2:
+            return cub::DeviceMergeSort::SortKeysCopy(tmp, bytes, k, ok, nn, less_i32(), s);
+        default:
+            return cub::DeviceMergeSort::SortPairsCopy(tmp, bytes, k, v, ok, ov, nn, less_i32(), s);
+    }
+}
+}  // namespace
+
+size_t comerge_testkit_cub_sort_bytes(size_t n) {
+    size_t most = 0;
+    for (int alg = 0; alg < 4; ++alg) {
+        size_t b = 0;
+        if (cub_sort(alg, nullptr, nullptr, nullptr, nullptr, n, nullptr, b, nullptr) == cudaSuccess)
+            most = b > most ? b : most;
+    }
+    return most;
+}
+
+int comerge_testkit_cub_sort(int alg, const int32_t* keys, const uint32_t* vals,
+                             int32_t* out_keys, uint32_t* out_vals, size_t n, void* tmp,
+                             size_t tmp_bytes, comerge_stream_t stream) {
+    if (n > (size_t(1) << 31) - 1 || alg < 0 || alg > 3) {
+        g_tk_error = "testkit: cub_sort arguments";
+        return COMERGE_E_INVALID;
+    }
+    size_t b = tmp_bytes;
+    const cudaError_t e = cub_sort(alg, keys, vals, out_keys, out_vals, n, tmp, b, stream);
+    return e ? tk_fail(e, "testkit: cub sort") : COMERGE_OK;
 }
 
 }  // extern "C"

@@ -325,6 +325,16 @@ def _config_inputs(cfg, cuda):
 
 @pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C3s", "C4", "C5"])
 def test_baseline_config_full_size(cuda, port, cfg):
+    """Every BASELINE config at full size, byte-for-byte against the REFERENCE
+    itself (oracle/_ref: comerge::merge_parallel at hardware_concurrency
+    workers, parallel.hpp:304-317; key-value configs in its own call shape,
+    {key, val} structs with a key-only less, oracle.hpp:22-37; C5 as
+    comerge::stable_merge per pair, merge.hpp:52-68), plus the size-independent
+    properties as extra guards."""
+    from oracle.py import Ref, available_ref, to_aos
+    assert available_ref(), "oracle/_ref/libcomerge_ref.so (the compiled reference) is missing"
+    ref = Ref()
+    threads = ref.hardware_concurrency()
     P().set_kernel_path("auto")
     import bench
     from paper_1303_4312_b200 import testkit as tk
@@ -332,38 +342,30 @@ def test_baseline_config_full_size(cuda, port, cfg):
     out = bench.run_config(cfg, inp)
     torch.cuda.synchronize()
     a, b = inp["a"], inp["b"]
-    total = a.numel() + b.numel()
-    # size-independent properties at full size (C5 is sorted per pair only)
+    # size-independent properties (C5 is sorted per pair only)
     if cfg != "C5":
         assert tk.count_unsorted(out["keys"]) == 0
     assert tk.checksum(out["keys"]) == (tk.checksum(a) + tk.checksum(b)) % 2**64
     if "vals" in out:
         assert tk.verify_pairs(a, b, out["keys"], out["vals"]) == [0, 0, 0, 0]
-    # exact comparison with the oracle where the host finishes in seconds
-    if total <= 2**26 + 2**25:
-        ha, hb = host(a), host(b)
-        if cfg == "C5":
-            expect = port.merge_segmented(ha, host(inp["a_off"]), hb, host(inp["b_off"]),
-                                          threads=8)
-            assert np.array_equal(host(out["keys"]), expect)
-        elif "vals" in out:
-            ek, ev, _, _ = port.merge_parallel(ha, hb, 64, host(inp["av"]), host(inp["bv"]),
-                                               threads=8)
-            assert np.array_equal(host(out["keys"]), ek) and np.array_equal(host(out["vals"]), ev)
-        else:
-            ek, _, _, _ = port.merge_parallel(ha, hb, 64, threads=8)
-            assert np.array_equal(host(out["keys"]), ek)
+    # the reference's own output on the same inputs, compared byte for byte
+    ha, hb = host(a), host(b)
+    got = host(out["keys"])
+    if cfg == "C5":
+        expect, _ = ref.merge_segmented(ha, host(inp["a_off"]), hb, host(inp["b_off"]),
+                                        threads=threads)
+        assert got.tobytes() == expect.tobytes()
+    elif "vals" in out:
+        a_aos, b_aos = to_aos(ha, host(inp["av"])), to_aos(hb, host(inp["bv"]))
+        del ha, hb
+        expect, rep = ref.merge_parallel_kv(a_aos, b_aos, threads)
+        del a_aos, b_aos
+        assert rep.m + rep.n == len(got)
+        assert got.tobytes() == np.ascontiguousarray(expect["key"]).tobytes()
+        assert host(out["vals"]).tobytes() == np.ascontiguousarray(expect["val"]).tobytes()
     else:
-        # spot-check tile boundaries of the huge configs against Algorithm 1
-        ha, hb = host(a), host(b)
-        rng = np.random.default_rng(1)
-        hk = out["keys"]
-        for i in rng.integers(0, total + 1, 16):
-            j, k = port.co_rank(int(i), ha, hb)
-            lo = max(0, int(i) - 64)
-            window = host(hk[lo:int(i)])
-            pref = np.sort(np.concatenate([ha[max(0, j - 64):j], hb[max(0, k - 64):k]]))
-            assert np.array_equal(window, pref[len(pref) - len(window):])
+        expect, rep, _, _ = ref.merge_parallel(ha, hb, threads)
+        assert got.tobytes() == expect.tobytes()
 
 
 def test_host_buffers_pipelined(cuda, port):
