@@ -17,8 +17,15 @@
 // types: int32_t, uint32_t, uint64_t with std::less<> -- any other comparator
 // or type is a compile-time error: there is no CPU fallback.  Ranges may live
 // in host memory (copied through the device inside the call) or be device
-// spans (comerge::cuda::device_span).  Key-value merges use the SoA overload
-// merge_parallel_pairs (payload uint32_t moves with its key; ties A-first).
+// spans (comerge::cuda::device_span).  Key-value merges take the reference's
+// own shape -- ranges of a {key, payload} struct with a key-only comparator
+// (merge_parallel(a, b, out, workers, key_less{}); the pattern of tagged<K> /
+// tagged_key_less, oracle.hpp:22-37): any trivially copyable standard-layout
+// struct whose first member `key` is int32_t / uint32_t (8-byte struct) or
+// uint64_t (16-byte struct), the rest of the struct moving with its key byte
+// for byte.  A caller's own key-only comparator is accepted once declared
+// key-only by specialising comerge::cuda::is_key_less.  The SoA overload
+// merge_parallel_pairs (payload uint32_t arrays) is the other form.
 #pragma once
 
 #include <cstddef>
@@ -138,6 +145,57 @@ concept key_range = std::ranges::contiguous_range<R> && std::ranges::sized_range
 
 template <typename R>
 using key_of = std::remove_cv_t<std::ranges::range_value_t<R>>;
+
+// key-value records (see the header comment)
+template <typename T>
+concept record_type =
+    std::is_trivially_copyable_v<T> && std::is_standard_layout_v<T> &&
+    requires(T t) { t.key; } && key_type<std::remove_cv_t<decltype(T::key)>> &&
+    (offsetof(T, key) == 0) &&
+    ((sizeof(T) == 8 && sizeof(T::key) == 4) || (sizeof(T) == 16 && sizeof(T::key) == 8));
+
+template <typename R>
+concept record_range = std::ranges::contiguous_range<R> && std::ranges::sized_range<R> &&
+                       record_type<std::remove_cv_t<std::ranges::range_value_t<R>>>;
+
+template <typename R>
+using elem_of = std::remove_cv_t<std::ranges::range_value_t<R>>;
+
+template <typename K>
+struct rec_abi;
+template <>
+struct rec_abi<std::int32_t> {
+    static int merge(const void* a, std::size_t m, const void* b, std::size_t n, void* out,
+                     std::size_t len, std::size_t w, int synced, comerge_merge_report* rep,
+                     std::uint64_t* bs, std::uint32_t* its) {
+        return comerge_merge_parallel_records_i32(static_cast<const comerge_rec_i32*>(a), m,
+                                                  static_cast<const comerge_rec_i32*>(b), n,
+                                                  static_cast<comerge_rec_i32*>(out), len, w,
+                                                  synced, rep, bs, its);
+    }
+};
+template <>
+struct rec_abi<std::uint32_t> {
+    static int merge(const void* a, std::size_t m, const void* b, std::size_t n, void* out,
+                     std::size_t len, std::size_t w, int synced, comerge_merge_report* rep,
+                     std::uint64_t* bs, std::uint32_t* its) {
+        return comerge_merge_parallel_records_u32(static_cast<const comerge_rec_u32*>(a), m,
+                                                  static_cast<const comerge_rec_u32*>(b), n,
+                                                  static_cast<comerge_rec_u32*>(out), len, w,
+                                                  synced, rep, bs, its);
+    }
+};
+template <>
+struct rec_abi<std::uint64_t> {
+    static int merge(const void* a, std::size_t m, const void* b, std::size_t n, void* out,
+                     std::size_t len, std::size_t w, int synced, comerge_merge_report* rep,
+                     std::uint64_t* bs, std::uint32_t* its) {
+        return comerge_merge_parallel_records_u64(static_cast<const comerge_rec_u64*>(a), m,
+                                                  static_cast<const comerge_rec_u64*>(b), n,
+                                                  static_cast<comerge_rec_u64*>(out), len, w,
+                                                  synced, rep, bs, its);
+    }
+};
 
 template <typename K>
 struct abi;
@@ -286,6 +344,80 @@ template <detail::key_range A, detail::key_range B, std::ranges::contiguous_rang
 merge_report merge_parallel_synced(const A& a, const B& b, Out&& out, std::size_t workers,
                                    std::less<> = {}, merge_options opts = {}) {
     return detail::run_merge_parallel(a, b, out, workers, opts, true);
+}
+
+/// A key-value record (the shape of the reference's tagged<K>, oracle.hpp:22-37).
+template <typename K>
+struct record {
+    K key{};
+    std::uint32_t val = 0;
+    friend bool operator==(const record&, const record&) = default;
+};
+
+/// Key-only ordering of records (the reference's tagged_key_less).
+struct key_less {
+    template <typename T>
+    bool operator()(const T& x, const T& y) const {
+        return x.key < y.key;
+    }
+};
+
+/// Comparators the device may run as "compare the keys only": key_less, plus
+/// any caller comparator declared key-only by specialising this trait, e.g.
+///   template <> struct comerge::cuda::is_key_less<comerge::tagged_key_less>
+///       : std::true_type {};
+template <typename C>
+struct is_key_less : std::false_type {};
+template <>
+struct is_key_less<key_less> : std::true_type {};
+
+namespace detail {
+template <typename A, typename B, typename Out>
+merge_report run_merge_records(const A& a, const B& b, Out& out, std::size_t workers,
+                               bool synced) {
+    using T = elem_of<A>;
+    using K = std::remove_cv_t<decltype(T::key)>;
+    comerge_merge_report rep{};
+    std::vector<std::uint64_t> bs(workers ? workers : 1);
+    std::vector<std::uint32_t> its(2 * (workers ? workers : 1));
+    check(rec_abi<K>::merge(std::ranges::data(a), std::ranges::size(a), std::ranges::data(b),
+                            std::ranges::size(b), std::ranges::data(out), std::ranges::size(out),
+                            workers, synced ? 1 : 0, &rep, bs.data(), its.data()));
+    merge_report r = to_report(rep);
+    r.block_sizes.assign(bs.begin(), bs.begin() + workers);
+    r.corank_iterations.assign(its.begin(), its.begin() + 2 * workers);
+    return r;
+}
+}  // namespace detail
+
+/// comerge::merge_parallel over key-value records with a key-only comparator
+/// (parallel.hpp:304-317 instantiated with tagged<K> / tagged_key_less): ties
+/// keep A first, then input order; records move whole.
+template <detail::record_range A, detail::record_range B, std::ranges::contiguous_range Out,
+          typename Less>
+    requires std::same_as<detail::elem_of<A>, detail::elem_of<B>> &&
+             std::same_as<detail::elem_of<A>, std::ranges::range_value_t<Out>> &&
+             is_key_less<Less>::value
+merge_report merge_parallel(const A& a, const B& b, Out&& out, std::size_t workers, Less,
+                            merge_options = {}) {
+    return detail::run_merge_records(a, b, out, workers, false);
+}
+
+/// comerge::stable_merge over records (merge.hpp:52-68).
+template <detail::record_range A, detail::record_range B, std::ranges::contiguous_range Out,
+          typename Less>
+    requires std::same_as<detail::elem_of<A>, detail::elem_of<B>> &&
+             std::same_as<detail::elem_of<A>, std::ranges::range_value_t<Out>> &&
+             is_key_less<Less>::value
+void stable_merge(const A& a, const B& b, Out&& out, Less) {
+    try {
+        detail::run_merge_records(a, b, out, 1, false);
+    } catch (const std::invalid_argument& e) {
+        std::string msg = e.what();
+        const auto pos = msg.find("merge_parallel");
+        if (pos != std::string::npos) msg.replace(pos, 14, "stable_merge");
+        throw std::invalid_argument(msg);
+    }
 }
 
 /// Key-value merge over SoA arrays (keys + uint32 payload).

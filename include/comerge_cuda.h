@@ -62,16 +62,16 @@ int comerge_cuda_abi_version(void);
 void comerge_cuda_set_kernel_events(void* before, void* after);
 
 /* Kernel selection on the calling thread (testing / benchmarking every
- * device path): 0 = automatic (default: 3 when all buffers are 16-byte
- * aligned and there are >= 16 tiles, else 1), 1 = tile kernel (partition +
- * one CTA per tile, any alignment), 2 = ring-streaming kernel, 3 = persistent
- * tile-pipeline kernel (2 and 3 need 16-byte aligned buffers, else 1 runs). */
+ * device path): 0 = automatic (default: 3 when there are >= 16 pipeline
+ * tiles, else 1), 1 = tile kernel (partition + one CTA per tile),
+ * 3 = persistent tile-pipeline kernel.  Both take arrays at any element
+ * offset (the pipeline stages windows at their address offset modulo 16). */
 void comerge_cuda_set_path(int path);
 /* Kernel used by the last merge on this thread: 1 = tile kernel (partition
- * + merge launches), 2 = ring-streaming kernel (one launch), 3 = tile
- * pipeline (one launch), 4 = segmented tile kernel (partition + merge),
- * 5 = segmented tile pipeline (one launch), 6 = merge pass of the sort
- * (tile pipeline over runs), 7 = pieced-input range merge, 0 = none yet. */
+ * + merge launches), 3 = tile pipeline (one launch), 4 = segmented tile
+ * kernel (partition + merge), 5 = segmented tile pipeline (one launch),
+ * 6 = merge pass of the sort (tile pipeline over runs), 7 = pieced-input
+ * range merge, 8 = small-merge kernel (one launch), 0 = none yet. */
 int comerge_cuda_last_path(void);
 /* Host-buffer strategy of the synchronous entry points on this thread
  * (testing / benchmarking): 0 = chunked pipeline (default: output chunks
@@ -135,6 +135,31 @@ int comerge_cuda_merge_pairs_u64(const uint64_t* a_keys, const uint32_t* a_vals,
                                  const uint64_t* b_keys, const uint32_t* b_vals, size_t n,
                                  uint64_t* out_keys, uint32_t* out_vals, void* ws,
                                  size_t ws_bytes, comerge_stream_t stream);
+
+/* Key-value RECORDS merged by key -- the reference's own key-value call
+ * shape: merge_parallel<T>(a, b, out, workers, less) over a struct with a
+ * key-only less (tagged<K> / tagged_key_less, oracle.hpp:22-37;
+ * parallel.hpp:304-317).  A record is the key at offset 0 followed by its
+ * payload bytes, which travel with it untouched (padding included):
+ *   comerge_rec_i32 / _u32  8 bytes  {key, uint32 val}
+ *   comerge_rec_u64        16 bytes  {uint64 key, uint32 val, uint32 pad}
+ *                                    (the C/C++ layout of {uint64_t, uint32_t})
+ * Ties go to A (stable).  Arrays may start at any record offset into an
+ * allocation (4-byte aligned for 8-byte records, 8-byte aligned for 16-byte
+ * ones).  Workspace from comerge_cuda_records_workspace_bytes. */
+typedef struct comerge_rec_i32 { int32_t key; uint32_t val; } comerge_rec_i32;
+typedef struct comerge_rec_u32 { uint32_t key; uint32_t val; } comerge_rec_u32;
+typedef struct comerge_rec_u64 { uint64_t key; uint32_t val; uint32_t pad; } comerge_rec_u64;
+size_t comerge_cuda_records_workspace_bytes(size_t m, size_t n, int key_kind);
+int comerge_cuda_merge_records_i32(const comerge_rec_i32* a, size_t m, const comerge_rec_i32* b,
+                                   size_t n, comerge_rec_i32* out, void* ws, size_t ws_bytes,
+                                   comerge_stream_t stream);
+int comerge_cuda_merge_records_u32(const comerge_rec_u32* a, size_t m, const comerge_rec_u32* b,
+                                   size_t n, comerge_rec_u32* out, void* ws, size_t ws_bytes,
+                                   comerge_stream_t stream);
+int comerge_cuda_merge_records_u64(const comerge_rec_u64* a, size_t m, const comerge_rec_u64* b,
+                                   size_t n, comerge_rec_u64* out, void* ws, size_t ws_bytes,
+                                   comerge_stream_t stream);
 
 /* Segmented batch: pair s merges a[a_off[s], a_off[s+1]) with
  * b[b_off[s], b_off[s+1]) into out[a_off[s]+b_off[s], ...).  a_off / b_off
@@ -245,6 +270,24 @@ int comerge_merge_parallel_pairs_u64(const uint64_t* a_keys, const uint32_t* a_v
                                      const uint64_t* b_keys, const uint32_t* b_vals, size_t n,
                                      uint64_t* out_keys, uint32_t* out_vals, size_t out_len,
                                      size_t workers, comerge_merge_report* report);
+
+/* comerge::merge_parallel over key-value records (see comerge_rec_*): host or
+ * device pointers, the report as comerge_merge_parallel_*. */
+int comerge_merge_parallel_records_i32(const comerge_rec_i32* a, size_t m,
+                                       const comerge_rec_i32* b, size_t n, comerge_rec_i32* out,
+                                       size_t out_len, size_t workers, int synced,
+                                       comerge_merge_report* report, uint64_t* block_sizes,
+                                       uint32_t* corank_iterations);
+int comerge_merge_parallel_records_u32(const comerge_rec_u32* a, size_t m,
+                                       const comerge_rec_u32* b, size_t n, comerge_rec_u32* out,
+                                       size_t out_len, size_t workers, int synced,
+                                       comerge_merge_report* report, uint64_t* block_sizes,
+                                       uint32_t* corank_iterations);
+int comerge_merge_parallel_records_u64(const comerge_rec_u64* a, size_t m,
+                                       const comerge_rec_u64* b, size_t n, comerge_rec_u64* out,
+                                       size_t out_len, size_t workers, int synced,
+                                       comerge_merge_report* report, uint64_t* block_sizes,
+                                       uint32_t* corank_iterations);
 
 /* merge_options (parallel.hpp:38-42) for the full-report entry points. */
 typedef struct comerge_merge_options {

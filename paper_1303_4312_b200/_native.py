@@ -71,6 +71,13 @@ def _load():
         getattr(lib, f"comerge_co_rank_{suf}").argtypes = [
             _u64, _p, _sz, _p, _sz, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(C.c_uint32),
             C.POINTER(C.c_uint32)]
+    lib.comerge_cuda_records_workspace_bytes.argtypes = [_sz, _sz, _i]
+    lib.comerge_cuda_records_workspace_bytes.restype = _sz
+    for suf in ("i32", "u32", "u64"):
+        getattr(lib, f"comerge_cuda_merge_records_{suf}").argtypes = [_p, _sz, _p, _sz, _p, _p,
+                                                                      _sz, _p]
+        getattr(lib, f"comerge_merge_parallel_records_{suf}").argtypes = [
+            _p, _sz, _p, _sz, _p, _sz, _sz, _i, C.POINTER(MergeReport), _p, _p]
     lib.comerge_cuda_sort_workspace_bytes.argtypes = [_sz, _i]
     lib.comerge_cuda_sort_workspace_bytes.restype = _sz
     lib.comerge_cuda_sort_pairs_workspace_bytes.argtypes = [_sz, _i]

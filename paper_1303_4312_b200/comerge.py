@@ -358,6 +358,92 @@ def merge_pairs(a_keys, a_vals, b_keys, b_vals, out_keys=None, out_vals=None, wo
     return out_keys, out_vals
 
 
+# ------------------------------------------------------------ records
+
+_REC_SUFFIX = {"int32": "i32", "uint32": "u32", "uint64": "u64"}
+_REC_SIZE = {"i32": 8, "u32": 8, "u64": 16}
+
+
+def record_dtype(key_dtype):
+    """numpy dtype of one key-value record (comerge_rec_* in
+    include/comerge_cuda.h): the key at offset 0, a uint32 `val`, and for
+    uint64 keys a uint32 `pad` (the C layout of {uint64_t key; uint32_t val;})."""
+    name = _dtype_name_of(key_dtype)
+    if name == "uint64":
+        return np.dtype({"names": ["key", "val", "pad"], "formats": [np.uint64, np.uint32, np.uint32],
+                         "offsets": [0, 8, 12], "itemsize": 16})
+    if name not in ("int32", "uint32"):
+        raise TypeError(f"records: unsupported key dtype {name} (int32, uint32, uint64)")
+    return np.dtype([("key", np.dtype(name)), ("val", np.uint32)])
+
+
+def _dtype_name_of(dtype):
+    if torch is not None and isinstance(dtype, torch.dtype):
+        return str(dtype).replace("torch.", "")
+    return np.dtype(dtype).name
+
+
+def _rec_count(x, size):
+    nbytes = int(x.numel() * x.element_size()) if _is_torch(x) else int(x.nbytes)
+    if nbytes % size:
+        raise ValueError(f"records: buffer of {nbytes} bytes is not a whole number of "
+                         f"{size}-byte records")
+    return nbytes // size
+
+
+def records_workspace_bytes(m: int, n: int, key_dtype) -> int:
+    suf = _REC_SUFFIX[_dtype_name_of(key_dtype)]
+    return int(N.lib.comerge_cuda_records_workspace_bytes(m, n, _KIND[suf]))
+
+
+def merge_records(a, b, out=None, key_dtype=None, workers: int = 1, workspace=None):
+    """Stable merge of key-value records by key alone -- the reference's own
+    key-value call shape: merge_parallel<T>(a, b, out, workers, key_less) over
+    {key, val} structs (tagged<K> / tagged_key_less, oracle.hpp:22-37;
+    parallel.hpp:304-317).  Ties keep A first, then input order; every record
+    is copied whole (payload and padding bytes).
+
+    Host: numpy structured arrays of record_dtype(key) (synchronous; returns
+    (out, MergeReport)).  Device: CUDA tensors of any dtype holding whole
+    records (e.g. int64 of shape (n, 2) for uint64-key records), `key_dtype`
+    given (asynchronous on the current stream; returns out)."""
+    if _is_torch(a) and a.is_cuda:
+        if key_dtype is None:
+            raise TypeError("merge_records: key_dtype is required for device tensors")
+        suf = _REC_SUFFIX[_dtype_name_of(key_dtype)]
+        size = _REC_SIZE[suf]
+        m, n = _rec_count(a, size), _rec_count(b, size)
+        if out is None:
+            out = torch.empty((m + n) * size // a.element_size(), dtype=a.dtype, device=a.device)
+        if _rec_count(out, size) != m + n:
+            raise ValueError("merge_records: output length must equal |a| + |b|")
+        wsp, wsb = _ws(workspace)
+        with _on(a):
+            N.check(getattr(N.lib, f"comerge_cuda_merge_records_{suf}")(
+                _ptr(a), m, _ptr(b), n, _ptr(out), wsp, wsb, _stream(a)))
+        return out
+    kd = a.dtype["key"] if a.dtype.names else key_dtype
+    suf = _REC_SUFFIX[_dtype_name_of(kd)]
+    size = _REC_SIZE[suf]
+    if a.dtype.itemsize != size or b.dtype != a.dtype:
+        raise TypeError(f"merge_records: a and b must be {size}-byte records of one dtype")
+    m, n = len(a), len(b)
+    if out is None:
+        out = np.empty(m + n, dtype=a.dtype)
+    if workers <= 0:
+        raise ValueError("merge_parallel: worker count must be positive")
+    rep = N.MergeReport()
+    bs = np.zeros(workers, np.uint64)
+    its = np.zeros(2 * workers, np.uint32)
+    N.check(getattr(N.lib, f"comerge_merge_parallel_records_{suf}")(
+        _ptr(a), m, _ptr(b), n, _ptr(out), len(out), workers, 0, C.byref(rep),
+        C.c_void_p(bs.ctypes.data), C.c_void_p(its.ctypes.data)))
+    return out, MergeReport(m=rep.m, n=rep.n, workers=rep.workers, wall_ns=rep.wall_ns,
+                            block_sizes=[int(x) for x in bs], corank_iterations=[int(x) for x in its],
+                            e2e_ns=rep.e2e_ns, h2d_bytes=rep.h2d_bytes, d2h_bytes=rep.d2h_bytes,
+                            tiles=rep.tiles)
+
+
 def merge_segmented(a, a_off, b, b_off, out=None, workspace=None):
     """Merge every pair s (a[a_off[s]:a_off[s+1]], b[b_off[s]:b_off[s+1]]) into
     out[a_off[s]+b_off[s]:...] in one device launch (device tensors)."""

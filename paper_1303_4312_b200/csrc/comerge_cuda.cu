@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstddef>
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
@@ -227,6 +228,14 @@ int check_merge_args(const char* who, const K* a, size_t m, const K* b, size_t n
                                           ": combined input length exceeds the device index range");
     if ((m && !a) || (n && !b) || (total && !out))
         return fail(COMERGE_E_INVALID, std::string(who) + ": null data pointer");
+    // any element offset into an allocation, but elements naturally aligned
+    constexpr uintptr_t al = alignof(K) - 1;
+    if ((m && (reinterpret_cast<uintptr_t>(a) & al)) || (n && (reinterpret_cast<uintptr_t>(b) & al)) ||
+        (total && (reinterpret_cast<uintptr_t>(out) & al)) ||
+        (has_v && ((m && (reinterpret_cast<uintptr_t>(av) & 3)) ||
+                   (n && (reinterpret_cast<uintptr_t>(bv) & 3)) ||
+                   (total && (reinterpret_cast<uintptr_t>(outv) & 3)))))
+        return fail(COMERGE_E_INVALID, std::string(who) + ": arrays must be aligned to their element type");
     if (has_v && ((m && !av) || (n && !bv) || (total && !outv)))
         return fail(COMERGE_E_INVALID, std::string(who) + ": null payload pointer");
     const size_t ob = total * sizeof(K);
@@ -341,7 +350,7 @@ int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const ui
     // streamed output out of L2's way keeps them resident until the load
     // (C4 1051 -> 1028 us); for 32-bit keys the hint costs more than it saves
     // (the output left dirty in L2 at kernel end is written back after it)
-    args.store_evict_first = sizeof(K) == 8 ? 1u : 0u;
+    args.store_evict_first = sizeof(typename key_of<K>::type) == 8 ? 1u : 0u;
     if (const uint32_t c = (uint32_t(g_tune_flags) >> 2) & 3u) args.sched_cap = 4u << c;
     if (const uint32_t a = (uint32_t(g_tune_flags) >> 4) & 15u) args.sched_ahead = 4u * a;
     if (args.sched_ahead < args.sched_cap) args.sched_ahead = args.sched_cap;
@@ -361,36 +370,76 @@ int merge_device(const K* a, const uint32_t* av, size_t m, const K* b, const uin
     if (int rc = check_merge_args<K>(who, a, m, b, n, out, av, bv, outv, HAS_V)) return rc;
     const uint64_t total = uint64_t(m) + n;
     if (total == 0) return COMERGE_OK;
-    // the tile pipeline when every buffer is 16-byte aligned and there are
-    // enough tiles to fill it
-    const bool aligned_all = aligned16(a) && aligned16(b) && aligned16(out) &&
-                             (!HAS_V || (aligned16(av) && aligned16(bv) && aligned16(outv)));
+    // the tile pipeline (any element offsets: byte-space windows) when there
+    // are enough tiles to fill it; records always take it
     using PL = pipe_layout<K, HAS_V>;
     const uint64_t ptiles = div_up(total, PL::T);
-    if (aligned_all && (g_path == 3 || (g_path == 0 && ptiles >= 16)))
+    if (is_rec<K>::value || g_path == 3 || (g_path == 0 && ptiles >= 16))
         return launch_pipe<K, HAS_V, 0>(a, av, m, b, bv, n, out, outv, nullptr, nullptr, 0, ws,
                                             ws_bytes, s);
-    constexpr int T = tile_cfg<K>::kTile;
-    const uint64_t ntiles = div_up(total, T);
-    const uint64_t nbound = ntiles + 1;
-    scratch sc;
-    if (int rc = sc.acquire(ws, ws_bytes, merge_ws_bytes<K>(m, n), s)) return rc;
-    uint64_t* bj = static_cast<uint64_t*>(sc.ptr);
-    partition_kernel<K><<<unsigned(div_up(nbound, 256)), 256, 0, s>>>(a, m, b, n, T, nbound, bj);
-    if (int rc = check_launch("comerge: partition launch")) return rc;
-    int flags = 0;
-    flags |= aligned16(a) ? kAAligned : 0;
-    flags |= aligned16(b) ? kBAligned : 0;
-    flags |= aligned16(out) ? kOutAligned : 0;
-    flags |= aligned16(av) ? kAVAligned : 0;
-    flags |= aligned16(bv) ? kBVAligned : 0;
-    flags |= aligned16(outv) ? kOutVAligned : 0;
-    g_last_path = 1;
-    mark_before(s);
-    merge_tile_kernel<K, HAS_V><<<unsigned(ntiles), tile_cfg<K>::kThreads, 0, s>>>(
-        a, av, m, b, bv, n, out, outv, bj, flags);
-    mark_after(s);
-    return check_launch("comerge: merge launch");
+    if constexpr (is_rec<K>::value) {
+        return COMERGE_OK;  // (unreachable: records always take the pipeline)
+    } else {
+        constexpr int T = tile_cfg<K>::kTile;
+        const uint64_t ntiles = div_up(total, T);
+        const uint64_t nbound = ntiles + 1;
+        scratch sc;
+        if (int rc = sc.acquire(ws, ws_bytes, merge_ws_bytes<K>(m, n), s)) return rc;
+        uint64_t* bj = static_cast<uint64_t*>(sc.ptr);
+        partition_kernel<K><<<unsigned(div_up(nbound, 256)), 256, 0, s>>>(a, m, b, n, T, nbound, bj);
+        if (int rc = check_launch("comerge: partition launch")) return rc;
+        int flags = 0;
+        flags |= aligned16(a) ? kAAligned : 0;
+        flags |= aligned16(b) ? kBAligned : 0;
+        flags |= aligned16(out) ? kOutAligned : 0;
+        flags |= aligned16(av) ? kAVAligned : 0;
+        flags |= aligned16(bv) ? kBVAligned : 0;
+        flags |= aligned16(outv) ? kOutVAligned : 0;
+        g_last_path = 1;
+        mark_before(s);
+        merge_tile_kernel<K, HAS_V><<<unsigned(ntiles), tile_cfg<K>::kThreads, 0, s>>>(
+            a, av, m, b, bv, n, out, outv, bj, flags);
+        mark_after(s);
+        return check_launch("comerge: merge launch");
+    }
+}
+
+// Key-value records (records.cuh): the arrays' common alignment picks the
+// instantiation (vector shared-memory accesses need it), then the pipeline.
+template <typename KT, int S>
+int records_align_class(const void* a, size_t m, const void* b, size_t n, const void* out) {
+    uintptr_t x = 0;
+    if (m) x |= reinterpret_cast<uintptr_t>(a);
+    if (n) x |= reinterpret_cast<uintptr_t>(b);
+    if (m + n) x |= reinterpret_cast<uintptr_t>(out);
+    constexpr uintptr_t nat = S == 16 ? 8 : 4;  // the record struct's own alignment
+    if (x & (nat - 1)) return 0;
+    return (x & 15) == 0 ? 16 : ((x & 7) == 0 ? 8 : 4);
+}
+
+template <typename KT, int S>
+int merge_records_device(const void* a, size_t m, const void* b, size_t n, void* out, void* ws,
+                         size_t ws_bytes, cudaStream_t s) {
+    const int A = records_align_class<KT, S>(a, m, b, n, out);
+    if (A == 0)
+        return fail(COMERGE_E_INVALID, "merge_records: arrays must be aligned to their record type");
+    auto run = [&](auto tag) {
+        using R = decltype(tag);
+        return merge_device<R, false>(static_cast<const R*>(a), nullptr, m,
+                                      static_cast<const R*>(b), nullptr, n, static_cast<R*>(out),
+                                      nullptr, ws, ws_bytes, s);
+    };
+    if constexpr (S == 16) {
+        return A >= 16 ? run(rec<KT, 16, 16>{}) : run(rec<KT, 16, 8>{});
+    } else {
+        return A >= 8 ? run(rec<KT, 8, 8>{}) : run(rec<KT, 8, 4>{});
+    }
+}
+
+template <typename KT, int S>
+size_t records_ws_bytes(size_t m, size_t n) {
+    if (m > SIZE_MAX - n || m + n == 0) return 0;
+    return round256(32 * (div_up(m + n, pipe_layout<rec<KT, S, 8>, false>::T) + 4));
 }
 
 // Output ranks [out_begin, out_end) of the stable merge of A and B, each
@@ -457,8 +506,7 @@ int merge_segmented_device(const K* a, const uint64_t* a_off, size_t m, const K*
     const uint64_t total = m + n;
     if (total == 0) return COMERGE_OK;
     using PL = pipe_layout<K, false>;
-    if (aligned16(a) && aligned16(b) && aligned16(out) && g_path != 1 &&
-        (g_path == 3 || div_up(total, PL::T) >= 16))
+    if (g_path != 1 && (g_path == 3 || div_up(total, PL::T) >= 16))
         return launch_pipe<K, false, 1>(a, nullptr, m, b, nullptr, n, out, nullptr, a_off, b_off,
                                            nseg, ws, ws_bytes, s);
     constexpr int T = seg_cfg<K>::kTile;
@@ -492,7 +540,7 @@ __global__ void block_comparisons_kernel(const K* __restrict__ a, const K* __res
     const uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (r >= workers) return;
     out[r] = merge_comparisons(a, js[r], js[r + 1], b, ranks[r] - js[r], ranks[r + 1] - js[r + 1],
-                               [](const K* p) { return ldg_key(p); });
+                               [](const K* p) { return ldg_elem(p); });
 }
 
 template <typename K>
@@ -1123,6 +1171,29 @@ int plan_sync(const K* a, size_t m, const K* b, size_t n, size_t workers, uint64
     return COMERGE_OK;
 }
 
+// comerge::merge_parallel over records (host or device pointers)
+template <typename KT, int S>
+int merge_parallel_records_sync(const void* a, size_t m, const void* b, size_t n, void* out,
+                                size_t out_len, size_t workers, int synced,
+                                comerge_merge_report* rep, uint64_t* block_sizes,
+                                uint32_t* corank_iterations) {
+    const int A = records_align_class<KT, S>(a, m, b, n, out);
+    if (A == 0)
+        return fail(COMERGE_E_INVALID, "merge_parallel: arrays must be aligned to their record type");
+    auto run = [&](auto tag) {
+        using R = decltype(tag);
+        return merge_parallel_sync<R, false>(static_cast<const R*>(a), nullptr, m,
+                                             static_cast<const R*>(b), nullptr, n,
+                                             static_cast<R*>(out), nullptr, out_len, workers,
+                                             synced, rep, block_sizes, corank_iterations);
+    };
+    if constexpr (S == 16) {
+        return A >= 16 ? run(rec<KT, 16, 16>{}) : run(rec<KT, 16, 8>{});
+    } else {
+        return A >= 8 ? run(rec<KT, 8, 8>{}) : run(rec<KT, 8, 4>{});
+    }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------ merge sort
@@ -1417,6 +1488,35 @@ int comerge_cuda_sort_keys_u64(const uint64_t* keys, size_t n, uint64_t* out, vo
                                size_t ws_bytes, comerge_stream_t stream) {
     return sort_device<uint64_t>(keys, n, out, ws, ws_bytes, stream);
 }
+
+size_t comerge_cuda_records_workspace_bytes(size_t m, size_t n, int key_kind) {
+    return with_slack(key_kind == COMERGE_KEY_U64 ? records_ws_bytes<uint64_t, 16>(m, n)
+                                                  : records_ws_bytes<uint32_t, 8>(m, n));
+}
+
+#define COMERGE_RECORDS(SUF, KT, S)                                                              \
+    int comerge_cuda_merge_records_##SUF(const comerge_rec_##SUF* a, size_t m,                   \
+                                         const comerge_rec_##SUF* b, size_t n,                   \
+                                         comerge_rec_##SUF* out, void* ws, size_t ws_bytes,      \
+                                         comerge_stream_t stream) {                              \
+        return merge_records_device<KT, S>(a, m, b, n, out, ws, ws_bytes, stream);              \
+    }                                                                                            \
+    int comerge_merge_parallel_records_##SUF(                                                    \
+        const comerge_rec_##SUF* a, size_t m, const comerge_rec_##SUF* b, size_t n,              \
+        comerge_rec_##SUF* out, size_t out_len, size_t workers, int synced,                      \
+        comerge_merge_report* report, uint64_t* block_sizes, uint32_t* corank_iterations) {      \
+        return merge_parallel_records_sync<KT, S>(a, m, b, n, out, out_len, workers, synced,     \
+                                                  report, block_sizes, corank_iterations);       \
+    }
+
+COMERGE_RECORDS(i32, int32_t, 8)
+COMERGE_RECORDS(u32, uint32_t, 8)
+COMERGE_RECORDS(u64, uint64_t, 16)
+
+static_assert(sizeof(comerge_rec_i32) == sizeof(rec<int32_t, 8, 8>) &&
+                  sizeof(comerge_rec_u64) == sizeof(rec<uint64_t, 16, 16>) &&
+                  offsetof(comerge_rec_u64, val) == 8,
+              "record layouts");
 
 int comerge_partition_output(uint64_t total, uint64_t workers, uint64_t r, uint64_t* out) {
     if (!out) return fail(COMERGE_E_INVALID, "partition_output: null result pointer");

@@ -42,6 +42,7 @@
 #include "ptx.cuh"
 #include "merge_tile.cuh"
 #include "merge_serial.cuh"
+#include "records.cuh"
 
 namespace comerge_b200 {
 
@@ -84,6 +85,13 @@ struct pipe_cfg<uint64_t, false> {
 template <>
 struct pipe_cfg<uint64_t, true> {
     static constexpr int NC = 256, VT = 11, NST = 3;
+};
+
+// key-value records (records.cuh): 8-byte records as the 32-bit key-value
+// tile (3840 outputs), 16-byte records 1792 outputs, 3 stages of ~29 KB
+template <typename KT, int S, int A>
+struct pipe_cfg<rec<KT, S, A>, false> {
+    static constexpr int NC = 256, VT = S == 8 ? 15 : 7, NST = 3;
 };
 
 // SEG: 0 plain merge, 1 segmented batch (explicit offsets), 2 merge pass
@@ -245,6 +253,76 @@ __device__ __forceinline__ uint32_t stage_copy_plan(const E* __restrict__ src, u
     return uint32_t((hi_al - lo_al) * sizeof(E));
 }
 
+// Byte-space staging of window [lo, hi) of an array of S-byte elements at
+// `base` (any 4-byte aligned address; S a multiple of 4) into the 16-byte
+// aligned stage slot `dst`, whose byte 0 stands for the 16-byte boundary at or
+// below the window's first byte -- so a window keeps its address offset
+// modulo 16 in shared memory, and misaligned arrays (any element offset into
+// an allocation) stream through the same TMA copies as aligned ones.  The
+// 16-byte blocks wholly inside the array form the bulk copy (planned here,
+// issued by the caller); the words of the partial blocks at the array's two
+// ends are copied here (at most 3 per end).
+struct win_plan {
+    const unsigned char* src;  // bulk source (16-byte aligned)
+    uint32_t dst_off;          // its offset in dst
+    uint32_t bytes;            // bulk bytes (a multiple of 16, may be 0)
+    uint32_t first;            // offset of element lo in dst (0..15)
+    uint32_t span;             // bytes of dst the window occupies, rounded up to 16
+};
+
+__device__ __forceinline__ win_plan plan_window(const void* base, uint64_t len, uint32_t S,
+                                                uint64_t lo, uint64_t hi, unsigned char* dst) {
+    const uintptr_t B = reinterpret_cast<uintptr_t>(base);
+    const uintptr_t W0 = B + lo * S, W1 = B + (hi > lo ? hi : lo) * S;
+    const uintptr_t A0 = W0 & ~uintptr_t(15);
+    const uintptr_t in0 = (B + 15) & ~uintptr_t(15), in1 = (B + len * S) & ~uintptr_t(15);
+    uintptr_t b0 = A0 > in0 ? A0 : in0;
+    uintptr_t b1 = (W1 + 15) & ~uintptr_t(15);
+    if (b1 > in1) b1 = in1;
+    if (b1 < b0) b1 = b0;
+    const uintptr_t h1 = b0 > W0 ? (b0 < W1 ? b0 : W1) : W0;  // head words [W0, h1)
+    for (uintptr_t x = W0; x < h1; x += 4)
+        *reinterpret_cast<uint32_t*>(dst + (x - A0)) = *reinterpret_cast<const uint32_t*>(x);
+    for (uintptr_t x = b1 > h1 ? b1 : h1; x < W1; x += 4)  // tail words
+        *reinterpret_cast<uint32_t*>(dst + (x - A0)) = *reinterpret_cast<const uint32_t*>(x);
+    win_plan p;
+    p.src = reinterpret_cast<const unsigned char*>(b0);
+    p.dst_off = uint32_t(b0 - A0);
+    p.bytes = uint32_t(b1 - b0);
+    p.first = uint32_t(W0 - A0);
+    p.span = uint32_t(((W1 + 15) & ~uintptr_t(15)) - A0);
+    return p;
+}
+
+// Byte-space store of `len` S-byte elements to out + pos*S (any 4-byte aligned
+// address) from the stage, where the consumers wrote element 0 at
+// src_al + (destination address mod 16) (src_al 16-byte aligned): the 16-byte
+// blocks wholly inside the range are one TMA bulk store, the words of the
+// partial blocks at its ends plain stores (tiles of neighbouring CTAs write
+// the other words of those blocks).
+__device__ __forceinline__ void store_window(void* out, uint64_t pos, int len, uint32_t S,
+                                             const unsigned char* src_al, bool hint,
+                                             uint64_t policy) {
+    if (len <= 0) return;
+    const uintptr_t W0 = reinterpret_cast<uintptr_t>(out) + pos * S, W1 = W0 + uint64_t(len) * S;
+    const uintptr_t A0 = W0 & ~uintptr_t(15);
+    uintptr_t b0 = (W0 + 15) & ~uintptr_t(15), b1 = W1 & ~uintptr_t(15);
+    if (b1 < b0) b1 = b0;
+    if (b1 > b0) {
+        void* d = reinterpret_cast<void*>(b0);
+        const unsigned char* sp = src_al + (b0 - A0);
+        if (hint)
+            tma_store_1d_hint(d, sp, uint32_t(b1 - b0), policy);
+        else
+            tma_store_1d(d, sp, uint32_t(b1 - b0));
+    }
+    const uintptr_t h1 = b0 < W1 ? b0 : W1;
+    for (uintptr_t x = W0; x < h1; x += 4)
+        *reinterpret_cast<uint32_t*>(x) = *reinterpret_cast<const uint32_t*>(src_al + (x - A0));
+    for (uintptr_t x = b1 > h1 ? b1 : h1; x < W1; x += 4)
+        *reinterpret_cast<uint32_t*>(x) = *reinterpret_cast<const uint32_t*>(src_al + (x - A0));
+}
+
 // merge-pass runs: L is a power of two (sort.cuh's base runs, doubled every
 // pass; checked at launch), so run arithmetic is shifts, not 64-bit divisions
 // (the producer lane stages every window through stage_runs)
@@ -301,8 +379,9 @@ __device__ __forceinline__ uint64_t run_pos_b(uint64_t y, uint64_t L) {
 
 // SEG == 3: element x of a pieced input (linear scan: at most kMaxPieces)
 template <typename K>
-__device__ __forceinline__ K piece_probe(const void* const* p, const uint64_t* st, uint32_t np,
-                                         uint64_t x) {
+__device__ __forceinline__ typename key_of<K>::type piece_probe(const void* const* p,
+                                                                const uint64_t* st, uint32_t np,
+                                                                uint64_t x) {
     uint32_t q = 0;
     while (q + 1 < np && st[q + 1] <= x) ++q;
     return probe_elem(static_cast<const K*>(p[q]) + (x - st[q]));
@@ -692,11 +771,11 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         // pull this CTA's share of an array into L2 (cp.async.bulk.prefetch)
         auto pull = [&](const void* base, uint64_t len, uint32_t esz) {
             const uint64_t x0 = len * c / G, x1 = len * (c + 1) / G;
-            uint64_t b0 = (x0 * esz) & ~uint64_t(15), b1 = (x1 * esz) & ~uint64_t(15);
-            const unsigned char* p = static_cast<const unsigned char*>(base);
+            const uintptr_t B = reinterpret_cast<uintptr_t>(base);
+            uintptr_t b0 = (B + x0 * esz) & ~uintptr_t(15), b1 = (B + x1 * esz) & ~uintptr_t(15);
             while (b1 > b0) {
-                const uint64_t chunk = b1 - b0 < (uint64_t(1) << 20) ? b1 - b0 : (uint64_t(1) << 20);
-                prefetch_l2(p + b0, uint32_t(chunk));
+                const uintptr_t chunk = b1 - b0 < (uintptr_t(1) << 20) ? b1 - b0 : (uintptr_t(1) << 20);
+                prefetch_l2(reinterpret_cast<const void*>(b0), uint32_t(chunk));
                 b0 += chunk;
             }
         };
@@ -983,11 +1062,11 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
 
     if (warp == W_STORE) {
         // ------------------------------------------------------ store warp
-        // Stores each merged tile from its stage with one TMA bulk store and
-        // releases the stage to the producer once the store has read it, so
-        // the consumer warps never wait on a store.
+        // Stores each merged tile from its stage (one TMA bulk store of its
+        // whole 16-byte blocks, plain word stores at misaligned ends:
+        // store_window) and releases the stage to the producer once the store
+        // has read it, so the consumer warps never wait on a store.
         if (lane != 0) return;
-        K* __restrict__ out = static_cast<K*>(args.out);
         uint32_t* __restrict__ outv = args.outv;
         const bool store_hint = args.store_evict_first != 0;
         const uint64_t spolicy = policy_evict_first();
@@ -1000,22 +1079,9 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
             const uint64_t lens = mt[2];
             const int len = int(lens >> 32) + int(lens & 0xffffffffu);
             unsigned char* stage = smem + L::oStages + size_t(st) * L::kStage;
-            const K* sk = reinterpret_cast<const K*>(stage);
-            const uint32_t* sv = reinterpret_cast<const uint32_t*>(stage + L::kStageKeys);
-            const uint32_t kb_bytes = uint32_t(len * sizeof(K)) & ~15u;
-            if (kb_bytes) {
-                if (store_hint) tma_store_1d_hint(out + i0, sk, kb_bytes, spolicy);
-                else tma_store_1d(out + i0, sk, kb_bytes);
-            }
-            for (int x = kb_bytes / sizeof(K); x < len; ++x) out[i0 + x] = sk[x];
-            if constexpr (HAS_V) {
-                const uint32_t vb_bytes = uint32_t(len * 4) & ~15u;
-                if (vb_bytes) {
-                    if (store_hint) tma_store_1d_hint(outv + i0, sv, vb_bytes, spolicy);
-                    else tma_store_1d(outv + i0, sv, vb_bytes);
-                }
-                for (int x = vb_bytes / 4; x < len; ++x) outv[i0 + x] = sv[x];
-            }
+            store_window(args.out, i0, len, uint32_t(sizeof(K)), stage, store_hint, spolicy);
+            if constexpr (HAS_V)
+                store_window(outv, i0, len, 4u, stage + L::kStageKeys, store_hint, spolicy);
             tma_store_commit();
             tma_store_wait_read<0>();  // the stage has been read by the store
             mbar_arrive(&empty[st]);
@@ -1088,73 +1154,118 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
                 unsigned char* stage = smem + L::oStages + size_t(st) * L::kStage;
                 K* sk = reinterpret_cast<K*>(stage);
                 uint32_t* sv = reinterpret_cast<uint32_t*>(stage + L::kStageKeys);
-                const uint32_t a_off = uint32_t(j0 % VECE);
-                const uint32_t b_base = (a_off + a_len + VECE - 1) / VECE * VECE;
-                const uint32_t b_off = uint32_t(k0 % VECE);
-                const uint64_t RL = SEG == 2 ? args.run_len : 0;  // merge pass (see pipe_args)
-                uint32_t ab, bb;
-                if constexpr (SEG == 3) {
-                    ab = stage_pieces(args.pa, args.pa_start, args.npa, j0, j1, sk, VECE, false,
-                                      nullptr, 0);
-                    bb = stage_pieces(args.pb, args.pb_start, args.npb, k0, k1, sk + b_base, VECE,
-                                      false, nullptr, 0);
+                unsigned char* svb = stage + L::kStageKeys;
+                // window byte offsets in the stage: A's first element, B's
+                // slot, B's first element (and the same for the payloads)
+                uint32_t a_first, b_base, b_first, av_first = 0, bv_base = 0, bv_first = 0;
+                uint32_t ab, bb, avb = 0, bvb = 0;
+                win_plan pa{}, pb{}, pav{}, pbv{};
+                if constexpr (SEG == 0 || SEG == 1) {
+                    // one array per side, any 4-byte alignment: byte-space windows
+                    pa = plan_window(a, m, sizeof(K), j0, j1, stage);
+                    pb = plan_window(b, n, sizeof(K), k0, k1, stage + pa.span);
+                    a_first = pa.first;
+                    b_base = pa.span;
+                    b_first = pb.first;
+                    ab = pa.bytes;
+                    bb = pb.bytes;
+                    if constexpr (HAS_V) {
+                        pav = plan_window(args.av, m, 4, j0, j1, svb);
+                        pbv = plan_window(args.bv, n, 4, k0, k1, svb + pav.span);
+                        av_first = pav.first;
+                        bv_base = pav.span;
+                        bv_first = pbv.first;
+                        avb = pav.bytes;
+                        bvb = pbv.bytes;
+                    }
                 } else {
-                    ab = RL ? stage_runs(a, m + n, j0, j1, RL, 0, sk, VECE, false, nullptr, 0)
-                            : stage_copy_plan(a, m, j0, j1, sk, VECE);
-                    bb = RL ? stage_runs(b, m + n, k0, k1, RL, 1, sk + b_base, VECE, false, nullptr, 0)
-                            : stage_copy_plan(b, n, k0, k1, sk + b_base, VECE);
-                }
-                uint32_t avb = 0, bvb = 0, av_off = 0, bv_base = 0;
-                if constexpr (HAS_V) {
-                    av_off = uint32_t(j0 % 4);
-                    bv_base = (av_off + a_len + 3) / 4 * 4;
+                    // merge passes / pieced inputs: 16-byte aligned pieces, index space
+                    const uint32_t ao = uint32_t(j0 % VECE);
+                    const uint32_t bbe = (ao + a_len + VECE - 1) / VECE * VECE;
+                    const uint32_t bo = uint32_t(k0 % VECE);
+                    a_first = ao * uint32_t(sizeof(K));
+                    b_base = bbe * uint32_t(sizeof(K));
+                    b_first = bo * uint32_t(sizeof(K));
+                    const uint64_t RL = SEG == 2 ? args.run_len : 0;  // merge pass (see pipe_args)
                     if constexpr (SEG == 3) {
-                        avb = stage_pieces(reinterpret_cast<const void* const*>(args.pav),
-                                           args.pa_start, args.npa, j0, j1, sv, 4, false, nullptr, 0);
-                        bvb = stage_pieces(reinterpret_cast<const void* const*>(args.pbv),
-                                           args.pb_start, args.npb, k0, k1, sv + bv_base, 4, false,
-                                           nullptr, 0);
+                        ab = stage_pieces(args.pa, args.pa_start, args.npa, j0, j1, sk, VECE, false,
+                                          nullptr, 0);
+                        bb = stage_pieces(args.pb, args.pb_start, args.npb, k0, k1, sk + bbe, VECE,
+                                          false, nullptr, 0);
                     } else {
-                        avb = RL ? stage_runs(args.av, m + n, j0, j1, RL, 0, sv, 4, false, nullptr, 0)
-                                 : stage_copy_plan(args.av, m, j0, j1, sv, 4);
-                        bvb = RL ? stage_runs(args.bv, m + n, k0, k1, RL, 1, sv + bv_base, 4, false,
-                                              nullptr, 0)
-                                 : stage_copy_plan(args.bv, n, k0, k1, sv + bv_base, 4);
+                        ab = stage_runs(a, m + n, j0, j1, RL, 0, sk, VECE, false, nullptr, 0);
+                        bb = stage_runs(b, m + n, k0, k1, RL, 1, sk + bbe, VECE, false, nullptr, 0);
+                    }
+                    if constexpr (HAS_V) {
+                        const uint32_t avo = uint32_t(j0 % 4);
+                        const uint32_t bvbe = (avo + a_len + 3) / 4 * 4;
+                        av_first = avo * 4;
+                        bv_base = bvbe * 4;
+                        bv_first = uint32_t(k0 % 4) * 4;
+                        if constexpr (SEG == 3) {
+                            avb = stage_pieces(reinterpret_cast<const void* const*>(args.pav),
+                                               args.pa_start, args.npa, j0, j1, sv, 4, false,
+                                               nullptr, 0);
+                            bvb = stage_pieces(reinterpret_cast<const void* const*>(args.pbv),
+                                               args.pb_start, args.npb, k0, k1, sv + bvbe, 4, false,
+                                               nullptr, 0);
+                        } else {
+                            avb = stage_runs(args.av, m + n, j0, j1, RL, 0, sv, 4, false, nullptr, 0);
+                            bvb = stage_runs(args.bv, m + n, k0, k1, RL, 1, sv + bvbe, 4, false,
+                                             nullptr, 0);
+                        }
                     }
                 }
+                // the merged tile's placement: element 0 at the output
+                // position's address offset modulo 16 (byte-space stores)
+                const uint64_t opos = i0 - out_base;
+                const uint32_t o_shift =
+                    uint32_t((reinterpret_cast<uintptr_t>(args.out) + opos * sizeof(K)) & 15u);
+                const uint32_t ov_shift =
+                    HAS_V ? uint32_t((reinterpret_cast<uintptr_t>(args.outv) + opos * 4) & 15u) : 0u;
                 mt[0] = i0;
                 mt[1] = k0;
                 mt[2] = (uint64_t(a_len) << 32) | b_len;
-                mt[3] = (uint64_t(a_off) << 48) | (uint64_t(b_base) << 24) | (uint64_t(b_off) << 8) |
-                        uint64_t(av_off);
+                mt[3] = uint64_t(a_first) | (uint64_t(b_first) << 8) | (uint64_t(b_base) << 16) |
+                        (uint64_t(o_shift) << 40);
+                mt[7] = uint64_t(av_first) | (uint64_t(bv_first) << 8) | (uint64_t(bv_base) << 16) |
+                        (uint64_t(ov_shift) << 40);
                 if constexpr (SEGM) mt[6] = seg1 - seg0 + 1 <= uint64_t(L::SEGCAP) ? 1 : 0;  // table?
                 mbar_arrive_expect_tx(&full[st], ab + bb + avb + bvb);
-                if constexpr (SEG == 3) {
-                    stage_pieces(args.pa, args.pa_start, args.npa, j0, j1, sk, VECE, true, &full[st],
-                                 policy);
-                    stage_pieces(args.pb, args.pb_start, args.npb, k0, k1, sk + b_base, VECE, true,
-                                 &full[st], policy);
-                } else if (RL) {
-                    stage_runs(a, m + n, j0, j1, RL, 0, sk, VECE, true, &full[st], policy);
-                    stage_runs(b, m + n, k0, k1, RL, 1, sk + b_base, VECE, true, &full[st], policy);
-                } else {
-                    if (ab) tma_load_1d(sk, a + (j0 - j0 % VECE), ab, &full[st], policy);
-                    if (bb) tma_load_1d(sk + b_base, b + (k0 - k0 % VECE), bb, &full[st], policy);
-                }
-                if constexpr (HAS_V && SEG == 3) {
-                    stage_pieces(reinterpret_cast<const void* const*>(args.pav), args.pa_start,
-                                 args.npa, j0, j1, sv, 4, true, &full[st], policy);
-                    stage_pieces(reinterpret_cast<const void* const*>(args.pbv), args.pb_start,
-                                 args.npb, k0, k1, sv + bv_base, 4, true, &full[st], policy);
-                } else if constexpr (HAS_V) {
-                    if (RL) {
-                        stage_runs(args.av, m + n, j0, j1, RL, 0, sv, 4, true, &full[st], policy);
-                        stage_runs(args.bv, m + n, k0, k1, RL, 1, sv + bv_base, 4, true, &full[st],
-                                   policy);
-                    } else {
-                        if (avb) tma_load_1d(sv, args.av + (j0 - j0 % 4), avb, &full[st], policy);
+                if constexpr (SEG == 0 || SEG == 1) {
+                    if (ab) tma_load_1d(stage + pa.dst_off, pa.src, ab, &full[st], policy);
+                    if (bb) tma_load_1d(stage + b_base + pb.dst_off, pb.src, bb, &full[st], policy);
+                    if constexpr (HAS_V) {
+                        if (avb) tma_load_1d(svb + pav.dst_off, pav.src, avb, &full[st], policy);
                         if (bvb)
-                            tma_load_1d(sv + bv_base, args.bv + (k0 - k0 % 4), bvb, &full[st], policy);
+                            tma_load_1d(svb + bv_base + pbv.dst_off, pbv.src, bvb, &full[st], policy);
+                    }
+                } else {
+                    const uint32_t bbe = b_base / uint32_t(sizeof(K));
+                    const uint64_t RL = SEG == 2 ? args.run_len : 0;
+                    if constexpr (SEG == 3) {
+                        stage_pieces(args.pa, args.pa_start, args.npa, j0, j1, sk, VECE, true,
+                                     &full[st], policy);
+                        stage_pieces(args.pb, args.pb_start, args.npb, k0, k1, sk + bbe, VECE, true,
+                                     &full[st], policy);
+                    } else {
+                        stage_runs(a, m + n, j0, j1, RL, 0, sk, VECE, true, &full[st], policy);
+                        stage_runs(b, m + n, k0, k1, RL, 1, sk + bbe, VECE, true, &full[st], policy);
+                    }
+                    if constexpr (HAS_V) {
+                        const uint32_t bvbe = bv_base / 4;
+                        if constexpr (SEG == 3) {
+                            stage_pieces(reinterpret_cast<const void* const*>(args.pav),
+                                         args.pa_start, args.npa, j0, j1, sv, 4, true, &full[st],
+                                         policy);
+                            stage_pieces(reinterpret_cast<const void* const*>(args.pbv),
+                                         args.pb_start, args.npb, k0, k1, sv + bvbe, 4, true,
+                                         &full[st], policy);
+                        } else {
+                            stage_runs(args.av, m + n, j0, j1, RL, 0, sv, 4, true, &full[st], policy);
+                            stage_runs(args.bv, m + n, k0, k1, RL, 1, sv + bvbe, 4, true, &full[st],
+                                       policy);
+                        }
                     }
                 }
             }
@@ -1210,18 +1321,19 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         const uint64_t lens = mt[2];
         const int a_len = int(lens >> 32), b_len = int(lens & 0xffffffffu);
         const int len = a_len + b_len;
-        const int a_off = int((packed >> 48) & 0xff), b_base = int((packed >> 24) & 0xffffff);
-        const int b_off = int((packed >> 8) & 0xff), av_off = int(packed & 0xff);
+        // byte offsets in the stage (producer): windows, output placement
+        const uint32_t a_first = uint32_t(packed & 0xff), b_first = uint32_t((packed >> 8) & 0xff);
+        const uint32_t b_base = uint32_t((packed >> 16) & 0xffffff);
+        const uint32_t o_shift = uint32_t((packed >> 40) & 0xff);
         unsigned char* stage = smem + L::oStages + size_t(st) * L::kStage;
-        K* sk = reinterpret_cast<K*>(stage);
-        uint32_t* sv = reinterpret_cast<uint32_t*>(stage + L::kStageKeys);
+        unsigned char* svb = stage + L::kStageKeys;
 
         const int diag = min(tid * VT, len);
         K keys[VT];
         uint32_t src[VT];
         const unsigned long long p0 = args.trace && tid == 0 ? globaltimer_ns() : 0;
-        const K* sA = sk + a_off;
-        const K* sB = sk + b_base + b_off;
+        const K* sA = reinterpret_cast<const K*>(stage + a_first);
+        const K* sB = reinterpret_cast<const K*>(stage + b_base + b_first);
         if constexpr (SEGM) {
             const uint64_t k0 = mt[1];
             const uint64_t s_lo = mt[4], s_hi = mt[5];
@@ -1248,11 +1360,13 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         } else {
             merge_thread_lean<K, VT, HAS_V>(sA, a_len, sB, b_len, diag, keys, src);
         }
+        uint32_t ov_shift = 0;
         if constexpr (HAS_V) {  // source element address -> its payload
-            const int bv_base = (av_off + a_len + 3) / 4 * 4;
-            const int bv_off = int(mt[1] & 3);
-            const uint32_t* sav = sv + av_off;
-            const uint32_t* sbv = sv + bv_base + bv_off;
+            const uint64_t pv = mt[7];
+            ov_shift = uint32_t((pv >> 40) & 0xff);
+            const uint32_t* sav = reinterpret_cast<const uint32_t*>(svb + (pv & 0xff));
+            const uint32_t* sbv = reinterpret_cast<const uint32_t*>(
+                svb + ((pv >> 16) & 0xffffff) + ((pv >> 8) & 0xff));
             const uint32_t aA = smem_addr(sA), aB = smem_addr(sB);
             constexpr int SH = sizeof(K) == 8 ? 3 : 2;
 #pragma unroll
@@ -1267,11 +1381,14 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         named_bar_sync(1, NC);  // every thread is done reading the windows
         const unsigned long long p2 = args.trace && tid == 0 ? globaltimer_ns() : 0;
         const int cnt = len - diag < VT ? len - diag : VT;
+        // element x of the tile at stage + o_shift + x * sizeof(K) (store_window)
+        const uint32_t ko = smem_addr(stage) + o_shift + uint32_t(tid * VT) * uint32_t(sizeof(K));
+        const uint32_t vo = smem_addr(svb) + ov_shift + uint32_t(tid * VT) * 4u;
 #pragma unroll
         for (int v = 0; v < VT; ++v)
             if (v < cnt) {
-                sk[tid * VT + v] = keys[v];
-                if constexpr (HAS_V) sv[tid * VT + v] = src[v];
+                smem_io<K>::st(ko + uint32_t(v) * uint32_t(sizeof(K)), keys[v]);
+                if constexpr (HAS_V) smem_io<uint32_t>::st(vo + uint32_t(v) * 4u, src[v]);
             }
         fence_proxy_async_smem();
         named_bar_sync(1, NC);

@@ -27,31 +27,18 @@
 #include <cstdint>
 #include <cstdio>
 
+#include "records.cuh"
+
 namespace comerge_b200 {
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// element load from a shared-window address (records: records.cuh)
 template <typename K>
-__device__ __forceinline__ K lds(uint32_t addr);
-template <>
-__device__ __forceinline__ int32_t lds<int32_t>(uint32_t addr) {
-    int32_t v;
-    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
-    return v;
-}
-template <>
-__device__ __forceinline__ uint32_t lds<uint32_t>(uint32_t addr) {
-    uint32_t v;
-    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
-    return v;
-}
-template <>
-__device__ __forceinline__ uint64_t lds<uint64_t>(uint32_t addr) {
-    unsigned long long v;
-    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr));
-    return uint64_t(v);
+__device__ __forceinline__ K lds(uint32_t addr) {
+    return smem_io<K>::ld(addr);
 }
 
 #ifndef COMERGE_SERIAL_LOOKAHEAD

@@ -22,6 +22,7 @@
 #include <cstdint>
 
 #include "corank.cuh"
+#include "records.cuh"
 
 namespace comerge_b200 {
 
@@ -58,7 +59,11 @@ __device__ __forceinline__ void st_vec_na(void* p, uint4 v) {
 
 template <typename T>
 __device__ __forceinline__ T ldg_elem(const T* p) {
-    if constexpr (sizeof(T) == 8)
+    if constexpr (is_rec<T>::value) {  // records compare by key: load the key only
+        T r{};
+        r.key = ldg_elem(&p->key);
+        return r;
+    } else if constexpr (sizeof(T) == 8)
         return static_cast<T>(__ldg(reinterpret_cast<const unsigned long long*>(p)));
     else
         return __ldg(p);
@@ -67,9 +72,12 @@ __device__ __forceinline__ T ldg_elem(const T* p) {
 // A co-rank probe: one scattered element, cached in L2 only.  (Through the
 // read-only L1 path every probe fetched a whole 128-byte line -- ncu: L2
 // requests of C4 exceeded the window bytes by 3.5 sectors per probe.)
+// Records (records.cuh) probe their key only.
 template <typename T>
-__device__ __forceinline__ T probe_elem(const T* p) {
-    if constexpr (sizeof(T) == 8)
+__device__ __forceinline__ typename key_of<T>::type probe_elem(const T* p) {
+    if constexpr (is_rec<T>::value)
+        return probe_elem(&p->key);
+    else if constexpr (sizeof(T) == 8)
         return static_cast<T>(__ldcg(reinterpret_cast<const unsigned long long*>(p)));
     else
         return __ldcg(p);

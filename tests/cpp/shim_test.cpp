@@ -14,6 +14,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "comerge/cuda.hpp"
@@ -209,9 +210,90 @@ static void sweep(std::uint64_t seed) {
     }
 }
 
+// The reference's key-value shape as a caller holds it: tagged<K> with a
+// key-only comparator (oracle.hpp:22-37), declared key-only for the device.
+enum class origin : std::uint8_t { from_a, from_b };
+template <typename K>
+struct tagged {
+    K key{};
+    origin from = origin::from_a;
+    std::uint32_t index = 0;
+    friend bool operator==(const tagged&, const tagged&) = default;
+};
+struct tagged_key_less {
+    template <typename K>
+    bool operator()(const tagged<K>& x, const tagged<K>& y) const {
+        return x.key < y.key;
+    }
+};
+template <>
+struct comerge::cuda::is_key_less<tagged_key_less> : std::true_type {};
+
+template <typename T>
+static std::vector<T> naive_merge_by_key(const std::vector<T>& a, const std::vector<T>& b) {
+    std::vector<T> out;
+    std::size_t x = 0, y = 0;
+    while (x < a.size() && y < b.size()) out.push_back(b[y].key < a[x].key ? b[y++] : a[x++]);
+    while (x < a.size()) out.push_back(a[x++]);
+    while (y < b.size()) out.push_back(b[y++]);
+    return out;
+}
+
+static void records() {
+    std::mt19937_64 rng(77);
+    // acceptance_test.cpp:213-235 shape: tagged elements, the tagged oracle
+    for (auto [m, n, alphabet] : {std::tuple<std::size_t, std::size_t, unsigned>{0, 0, 3},
+                                  {1, 0, 3}, {0, 5, 3}, {1000, 999, 4}, {5000, 3, 50},
+                                  {200003, 150001, 100}, {1 << 20, (1 << 20) + 3, 1000}}) {
+        std::vector<tagged<std::uint64_t>> ta(m), tb(n);
+        std::vector<std::uint64_t> ka(m), kb(n);
+        for (auto& x : ka) x = rng() % alphabet;
+        for (auto& x : kb) x = rng() % alphabet;
+        std::sort(ka.begin(), ka.end());
+        std::sort(kb.begin(), kb.end());
+        for (std::size_t i = 0; i < m; ++i) ta[i] = {ka[i], origin::from_a, std::uint32_t(i)};
+        for (std::size_t i = 0; i < n; ++i) tb[i] = {kb[i], origin::from_b, std::uint32_t(i)};
+        const auto expect = naive_merge_by_key(ta, tb);
+        for (std::size_t workers : {1, 4, 33}) {
+            std::vector<tagged<std::uint64_t>> out(m + n);
+            const auto rep = cm::merge_parallel(ta, tb, out, workers, tagged_key_less{});
+            CHECK(out == expect);
+            CHECK(rep.block_sizes.size() == workers);
+        }
+        // 8-byte records with 32-bit keys, on the device
+        std::vector<cm::record<std::int32_t>> ra(m), rb(n);
+        for (std::size_t i = 0; i < m; ++i) ra[i] = {std::int32_t(ka[i]) - 7, std::uint32_t(i)};
+        for (std::size_t i = 0; i < n; ++i) rb[i] = {std::int32_t(kb[i]) - 7, std::uint32_t(i) | 1u << 31};
+        const auto rexpect = naive_merge_by_key(ra, rb);
+        using R = cm::record<std::int32_t>;
+        R *da = nullptr, *db = nullptr, *dout = nullptr;
+        cudaMalloc(&da, (m + 1) * sizeof(R));
+        cudaMalloc(&db, (n + 1) * sizeof(R));
+        cudaMalloc(&dout, (m + n + 1) * sizeof(R));
+        cudaMemcpy(da + 1, ra.data(), m * sizeof(R), cudaMemcpyHostToDevice);  // offset views
+        cudaMemcpy(db, rb.data(), n * sizeof(R), cudaMemcpyHostToDevice);
+        cm::device_span<const R> sa{da + 1, m}, sb{db, n};
+        cm::device_span<R> so{dout + 1, m + n};
+        cm::stable_merge(sa, sb, so, cm::key_less{});
+        std::vector<R> back(m + n);
+        cudaMemcpy(back.data(), dout + 1, (m + n) * sizeof(R), cudaMemcpyDeviceToHost);
+        CHECK(back == rexpect);
+        cudaFree(da);
+        cudaFree(db);
+        cudaFree(dout);
+    }
+    // merge.hpp:62-66 contract through the record overloads
+    std::vector<cm::record<std::uint32_t>> x(3), y(2), bad(4);
+    CHECK(throws_with<std::invalid_argument>(
+        [&] { cm::stable_merge(x, y, bad, cm::key_less{}); }, "output length must equal"));
+    CHECK(throws_with<std::invalid_argument>(
+        [&] { cm::merge_parallel(x, y, bad, 2, cm::key_less{}); }, "output length must equal"));
+}
+
 int main() {
     kats();
     comparisons();
+    records();
     sweep<std::int32_t>(1);
     sweep<std::uint32_t>(2);
     sweep<std::uint64_t>(3);

@@ -231,6 +231,55 @@ def test_misaligned_views(cuda, path, port, dt):
         assert np.array_equal(host(vo), port.merge(a, b)), (shift_a, shift_b, shift_o)
 
 
+@pytest.mark.parametrize("dt", [np.int32, np.uint64])
+def test_misaligned_pairs_and_segmented_pipeline(cuda, port, dt):
+    """The tile pipeline at every element offset mod 16 bytes of keys,
+    payloads and outputs (byte-space windows and stores: no alignment cliff),
+    large enough for the persistent grid and its dynamic tail."""
+    P().set_kernel_path("auto")
+    rng = np.random.default_rng(8)
+    tdt = TDT[np.dtype(dt)]
+    vece = 16 // np.dtype(dt).itemsize
+    m, n = 300_001, 250_003
+    a, b = _draw(rng, dt, m, 20), _draw(rng, dt, n, 20)
+    av, bv = tagged(m, n)
+    ek, ev = port.merge(a, b, av, bv)
+
+    def view(x, t, shift):
+        buf = torch.zeros(len(x) + 8, dtype=t, device=cuda)
+        v = buf[shift:shift + len(x)]
+        v.copy_(dev(x, cuda))
+        return v
+
+    for sh in [(1, 0, 0, 0, 0, 0), (0, 1, 2, 3, 1, 2), (vece - 1, 1, 0, 1, 3, 1),
+               (1, vece - 1, 3, 0, 2, 3), (0, 0, 0, 0, 0, 1)]:
+        va, vb = view(a, tdt, sh[0] % vece), view(b, tdt, sh[1] % vece)
+        vav, vbv = view(av, torch.uint32, sh[2]), view(bv, torch.uint32, sh[3])
+        ok = torch.zeros(m + n + 8, dtype=tdt, device=cuda)[sh[4] % vece:][:m + n]
+        ov = torch.zeros(m + n + 8, dtype=torch.uint32, device=cuda)[sh[5]:][:m + n]
+        P().merge_pairs(va, vav, vb, vbv, ok, ov)
+        P().stable_merge(va, vb, ok2 := torch.zeros(m + n + 3, dtype=tdt, device=cuda)[3 % vece:][:m + n])
+        torch.cuda.synchronize()
+        assert P()._native.lib.comerge_cuda_last_path() == 3
+        assert np.array_equal(host(ok), ek) and np.array_equal(host(ov), ev), sh
+        assert np.array_equal(host(ok2), ek), sh
+    if dt == np.int32:  # segmented batch, misaligned runs and output
+        la, lb = rng.integers(0, 3000, 500), rng.integers(0, 3000, 500)
+        sa = np.concatenate([np.sort(rng.integers(0, 99, x)) for x in la]).astype(np.int32)
+        sb = np.concatenate([np.sort(rng.integers(0, 99, x)) for x in lb]).astype(np.int32)
+        ao = np.concatenate([[0], np.cumsum(la)]).astype(np.uint64)
+        bo = np.concatenate([[0], np.cumsum(lb)]).astype(np.uint64)
+        expect = port.merge_segmented(sa, ao, sb, bo)
+        for s0, s1, s2 in [(1, 2, 3), (3, 0, 1), (0, 0, 2)]:
+            out = torch.zeros(len(sa) + len(sb) + 4, dtype=torch.int32, device=cuda)[s2:]
+            out = out[:len(sa) + len(sb)]
+            P().merge_segmented(view(sa, torch.int32, s0), dev(ao, cuda), view(sb, torch.int32, s1),
+                                dev(bo, cuda), out)
+            torch.cuda.synchronize()
+            assert P()._native.lib.comerge_cuda_last_path() == 5
+            assert np.array_equal(host(out), expect), (s0, s1, s2)
+
+
 def test_random_segmented(cuda, path, port):
     rng = np.random.default_rng(99)
     for dt in (np.int32, np.uint32):
