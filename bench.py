@@ -59,6 +59,14 @@ CONFIGS = {
     "C5": dict(kind="segmented", dtype="int32", nseg=2**14, maxlen=4096, width=2**20,
                desc="segmented batch: 2^14 pairs, m_s,n_s in [1,4096], int32 keys in [0,2^20)"),
 }
+# the key-value configs in the reference's own call shape: records {key, val}
+# (8 bytes; 16 with the uint64 key's padding) merged by key (oracle.hpp:22-37)
+CONFIGS["C2r"] = dict(kind="records", base="C2", dtype="int32", m=2**24, n=2**24, width=16,
+                      desc="C2 as 8-byte {int32 key, uint32 val} records (the reference's "
+                           "struct + key-only less)")
+CONFIGS["C4r"] = dict(kind="records", base="C4", dtype="uint64", m=2**27, n=2**27, width=0,
+                      desc="C4 as 16-byte {uint64 key, uint32 val, pad} records (the "
+                           "reference's struct + key-only less)")
 HEADLINE = "C4"
 SEED = 5
 METRIC = "merged elements/s"
@@ -70,13 +78,33 @@ def key_bytes(cfg):
 
 def elem_bytes(cfg):
     c = CONFIGS[cfg]
+    if c["kind"] == "records":
+        return 2 * key_bytes(cfg)
     return key_bytes(cfg) + (4 if c["kind"] == "pairs" else 0)
 
 
 def dtype_str(cfg):
     c = CONFIGS[cfg]
     k = {"int32": "int32", "uint64": "u64"}[c["dtype"]]
+    if c["kind"] == "records":
+        return f"{elem_bytes(cfg)}-byte records ({k} key + u32 payload)"
     return k + ("+u32 payload" if c["kind"] == "pairs" else "")
+
+
+def count(cfg, inp):
+    """Elements (records) of one merge of the config."""
+    if CONFIGS[cfg]["kind"] == "records":
+        return inp["m"] + inp["n"]
+    return inp["a"].numel() + inp["b"].numel()
+
+
+def pack_records(keys, vals):
+    """Device {key, val} records as a (len, 2) tensor: int32 words for 32-bit
+    keys, int64 words {key, val | pad << 32} (pad 0) for uint64 keys."""
+    import torch
+    if keys.dtype == torch.uint64:
+        return torch.stack([keys.view(torch.int64), vals.to(torch.int64)], 1).contiguous()
+    return torch.stack([keys.view(torch.int32), vals.view(torch.int32)], 1).contiguous()
 
 
 def scaling_of(world, replicas):
@@ -110,6 +138,12 @@ def make_inputs(cfg, seed=SEED, device="cuda"):
     from paper_1303_4312_b200 import testkit as tk
     c = CONFIGS[cfg]
     tdt = {"int32": torch.int32, "uint64": torch.uint64}[c["dtype"]]
+    if c["kind"] == "records":
+        base = make_inputs(c["base"], seed, device)
+        rec = dict(a=pack_records(base["a"], base["av"]), b=pack_records(base["b"], base["bv"]),
+                   m=base["a"].numel(), n=base["b"].numel())
+        del base
+        return rec
     with torch.cuda.device(device):
         if c["kind"] == "segmented":
             sizes = tk.generate_raw(seed, 2, 2 * c["nseg"], c["maxlen"], device=device)
@@ -142,6 +176,8 @@ def make_host_inputs(cfg, seed=SEED):
     from oracle.py import Port
     port = Port()
     c = CONFIGS[cfg]
+    if c["kind"] == "records":  # the reference's own form of the key-value configs
+        return make_host_inputs(c["base"], seed)
     dt = {"int32": np.int32, "uint64": np.uint64}[c["dtype"]]
     if c["kind"] == "segmented":
         sizes = port.generate_raw(seed, 2, 2 * c["nseg"], c["maxlen"]).astype(np.int64) + 1
@@ -168,10 +204,14 @@ def alloc_outputs(cfg, inp):
     """Outputs plus the merge's scratch workspace (queried, CUB-style)."""
     import torch
     import paper_1303_4312_b200._native as N
-    total = inp["a"].numel() + inp["b"].numel()
+    total = count(cfg, inp)
     dev = inp["a"].device
-    out = dict(keys=torch.empty(total, dtype=inp["a"].dtype, device=dev))
     kind = {"int32": N.KEY_I32, "uint64": N.KEY_U64}[CONFIGS[cfg]["dtype"]]
+    if CONFIGS[cfg]["kind"] == "records":
+        wsb = N.lib.comerge_cuda_records_workspace_bytes(inp["m"], inp["n"], kind)
+        return dict(keys=torch.empty((total, 2), dtype=inp["a"].dtype, device=dev),
+                    ws=torch.empty(max(int(wsb), 256), dtype=torch.uint8, device=dev))
+    out = dict(keys=torch.empty(total, dtype=inp["a"].dtype, device=dev))
     if CONFIGS[cfg]["kind"] == "segmented":
         wsb = N.lib.comerge_cuda_segmented_workspace_bytes(total, inp["a_off"].numel() - 1, kind)
     else:
@@ -195,6 +235,9 @@ def run_config(cfg, inp, out=None):
     elif kind == "pairs":
         P.merge_pairs(inp["a"], inp["av"], inp["b"], inp["bv"], out["keys"], out["vals"],
                       workspace=ws)
+    elif kind == "records":
+        P.merge_records(inp["a"], inp["b"], out["keys"], key_dtype=CONFIGS[cfg]["dtype"],
+                        workspace=ws)
     else:
         P.merge_segmented(inp["a"], inp["a_off"], inp["b"], inp["b_off"], out["keys"],
                           workspace=ws)
@@ -396,7 +439,7 @@ def time_config(cfg, steps, warmup, device, flush, seed=SEED, dist_ctx=None, clo
     out = alloc_outputs(cfg, inp)
     res = time_steps(lambda: run_config(cfg, inp, out), steps, warmup, device, flush, dist_ctx,
                      clocks)
-    res.update(total=inp["a"].numel() + inp["b"].numel(), inp=inp, out=out)
+    res.update(total=count(cfg, inp), inp=inp, out=out)
     return res
 
 
@@ -435,7 +478,7 @@ def cpu_model():
 def with_aos(cfg, h):
     """Key-value configs in the reference's own call shape: {key, val} structs
     with a key-only less (oracle.hpp:22-37)."""
-    if CONFIGS[cfg]["kind"] == "pairs" and "a_aos" not in h:
+    if CONFIGS[cfg]["kind"] in ("pairs", "records") and "a_aos" not in h:
         from oracle.py import to_aos
         h["a_aos"] = to_aos(h["a"], h["av"])
         h["b_aos"] = to_aos(h["b"], h["bv"])
@@ -449,6 +492,8 @@ def cpu_reference_run(cfg, h, threads):
     std::threads, each calling comerge::stable_merge (merge.hpp:52-68)."""
     from oracle.py import Ref, available_ref, Port
     kind = CONFIGS[cfg]["kind"]
+    if kind == "records":
+        kind = "pairs"
     if available_ref():
         ref = Ref()
         if kind == "segmented":
@@ -522,14 +567,23 @@ def e2e_measure(cfg, inp, steps, warmup):
     import paper_1303_4312_b200._native as N
     c = CONFIGS[cfg]
     suf = {"int32": "i32", "uint64": "u64"}[c["dtype"]]
-    pin = {k: v.cpu().pin_memory() for k, v in inp.items()}
+    pin = {k: v.cpu().pin_memory() for k, v in inp.items() if hasattr(v, "cpu")}
     total = inp["a"].numel() + inp["b"].numel()
     ok = torch.empty(total, dtype=inp["a"].dtype).pin_memory()
     ov = torch.empty(total, dtype=torch.uint32).pin_memory() if c["kind"] == "pairs" else None
     rep = N.MergeReport()
     p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
 
-    if c["kind"] == "segmented":
+    if c["kind"] == "records":
+        total = count(cfg, inp)
+        path = f"comerge_merge_parallel_records_{suf} (host pinned buffers)"
+        ok = torch.empty((total, 2), dtype=inp["a"].dtype).pin_memory()
+
+        def call():
+            N.check(getattr(N.lib, f"comerge_merge_parallel_records_{suf}")(
+                p(pin["a"]), inp["m"], p(pin["b"]), inp["n"], p(ok), total, 1, 0, C.byref(rep),
+                None, None))
+    elif c["kind"] == "segmented":
         fn = getattr(N.lib, f"comerge_merge_segmented_host_{suf}", None)
         if fn is None:
             return None
@@ -697,8 +751,8 @@ def run_split(args, dist, rank, world, device, peak, flush):
     import torch
     from paper_1303_4312_b200.shard import DistributedMerge
     cfg = args.config
-    if CONFIGS[cfg]["kind"] == "segmented":
-        raise SystemExit("--split: plain merges only (C5 is a batch: use --replicas)")
+    if CONFIGS[cfg]["kind"] in ("segmented", "records"):
+        raise SystemExit("--split: plain keys / key-value merges only (use --replicas)")
     full = make_inputs(cfg, seed=SEED, device=device)
 
     def piece(t, length):
@@ -800,7 +854,12 @@ def main():
         if legs and not args.no_e2e:
             d["e2e"] = e2e_measure(c, r["inp"], max(5, min(args.steps, 9)), 1)
         if legs and not args.no_cpu:
-            d["cpu_baseline"] = cpu_baseline(c, {k: v.cpu().numpy() for k, v in r["inp"].items()})
+            if CONFIGS[c]["kind"] == "records":  # the reference's call is this record form
+                d["cpu_baseline"] = f"same as {CONFIGS[c]['base']} (the reference merges its " \
+                                    "{key, val} structs there)"
+            else:
+                d["cpu_baseline"] = cpu_baseline(c, {k: v.cpu().numpy()
+                                                     for k, v in r["inp"].items()})
         return d
 
     head_extras = extras(cfg, res)

@@ -289,6 +289,24 @@ int comerge_merge_parallel_records_u64(const comerge_rec_u64* a, size_t m,
                                        comerge_merge_report* report, uint64_t* block_sizes,
                                        uint32_t* corank_iterations);
 
+/* Segmented batch with HOST (or device) buffers -- the reference's C5
+ * baseline is a loop of comerge::stable_merge over independent pairs
+ * (merge.hpp:52-68); this is the same batch in one call: pair s merges
+ * a[a_off[s], a_off[s+1]) with b[b_off[s], b_off[s+1]) into
+ * out[a_off[s] + b_off[s], ...).  Offsets (nseg + 1 each, host or device)
+ * must be nondecreasing, start at 0 and end within the inputs (E_INVALID
+ * otherwise).  Host inputs of >= 2^20 elements stream through a chunked
+ * H2D / merge / D2H pipeline; report fields as comerge_merge_parallel_*
+ * (workers = 1, no block sizes). */
+int comerge_merge_segmented_host_i32(const int32_t* a, const uint64_t* a_off, size_t m,
+                                     const int32_t* b, const uint64_t* b_off, size_t n,
+                                     size_t nseg, int32_t* out, size_t out_len,
+                                     comerge_merge_report* report);
+int comerge_merge_segmented_host_u32(const uint32_t* a, const uint64_t* a_off, size_t m,
+                                     const uint32_t* b, const uint64_t* b_off, size_t n,
+                                     size_t nseg, uint32_t* out, size_t out_len,
+                                     comerge_merge_report* report);
+
 /* merge_options (parallel.hpp:38-42) for the full-report entry points. */
 typedef struct comerge_merge_options {
     int synced;             /* merge_parallel_synced semantics (parallel.hpp:323-336)  */

@@ -87,6 +87,8 @@ def _load():
         getattr(lib, f"comerge_cuda_sort_pairs_{suf}").argtypes = [_p, _p, _sz, _p, _p, _p, _sz,
                                                                    _p]
     for suf in ("i32", "u32"):
+        getattr(lib, f"comerge_merge_segmented_host_{suf}").argtypes = [
+            _p, _p, _sz, _p, _p, _sz, _sz, _p, _sz, C.POINTER(MergeReport)]
         getattr(lib, f"comerge_cuda_merge_segmented_{suf}").argtypes = [
             _p, _p, _sz, _p, _p, _sz, _sz, _p, _p, _sz, _p]
     lib.comerge_cuda_set_kernel_events.argtypes = [_p, _p]

@@ -444,16 +444,31 @@ def merge_records(a, b, out=None, key_dtype=None, workers: int = 1, workspace=No
                             tiles=rep.tiles)
 
 
-def merge_segmented(a, a_off, b, b_off, out=None, workspace=None):
+def merge_segmented(a, a_off, b, b_off, out=None, workspace=None, report=False):
     """Merge every pair s (a[a_off[s]:a_off[s+1]], b[b_off[s]:b_off[s+1]]) into
-    out[a_off[s]+b_off[s]:...] in one device launch (device tensors)."""
+    out[a_off[s]+b_off[s]:...]: device tensors in one asynchronous launch;
+    host (numpy) arrays synchronously through a chunked H2D / merge / D2H
+    pipeline (comerge_merge_segmented_host_*; `report=True` also returns the
+    MergeReport).  The reference has no batched call: its equivalent is a
+    loop of comerge::stable_merge over the pairs (merge.hpp:52-68)."""
     suf = _suffix(a)
     if suf == "u64":
         raise TypeError("merge_segmented: int32 / uint32 keys")
-    nseg = int(a_off.numel()) - 1
+    nseg = int(_len(a_off)) - 1
     if out is None:
         out = _empty_like_merge(a, _len(a) + _len(b))
     _check_out("merge_segmented", a, b, out)
+    if not (_is_torch(a) and a.is_cuda):
+        rep = N.MergeReport()
+        with _on(out):
+            N.check(getattr(N.lib, f"comerge_merge_segmented_host_{suf}")(
+                _ptr(a), _ptr(a_off), _len(a), _ptr(b), _ptr(b_off), _len(b), max(nseg, 0),
+                _ptr(out), _len(out), C.byref(rep)))
+        if report:
+            return out, MergeReport(m=rep.m, n=rep.n, workers=rep.workers, wall_ns=rep.wall_ns,
+                                    e2e_ns=rep.e2e_ns, h2d_bytes=rep.h2d_bytes,
+                                    d2h_bytes=rep.d2h_bytes, tiles=rep.tiles)
+        return out
     wsp, wsb = _ws(workspace)
     with _on(a):
         N.check(getattr(N.lib, f"comerge_cuda_merge_segmented_{suf}")(

@@ -864,6 +864,261 @@ int merge_host_pipeline(const K* a, const uint32_t* av, uint64_t m, const K* b,
     return COMERGE_OK;
 }
 
+// Chunk offsets of a segmented batch, rebased onto the chunk's windows:
+// out_a[q] = clamp(a_off[s0 + q] - sa, 0, la) for q in [0, ns] (and b).
+__global__ void rebase_offsets_kernel(const uint64_t* __restrict__ a_off,
+                                      const uint64_t* __restrict__ b_off, uint64_t s0, uint64_t ns,
+                                      uint64_t sa, uint64_t la, uint64_t sb, uint64_t lb,
+                                      uint64_t* __restrict__ out_a, uint64_t* __restrict__ out_b) {
+    const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q > ns) return;
+    const uint64_t x = a_off[s0 + q], y = b_off[s0 + q];
+    out_a[q] = x <= sa ? 0 : (x - sa < la ? x - sa : la);
+    out_b[q] = y <= sb ? 0 : (y - sb < lb ? y - sb : lb);
+}
+
+// Host buffers, segmented batch (no reference counterpart: the reference's C5
+// baseline is a loop of stable_merge, merge.hpp:52-68): the batch is one
+// stable merge over (segment, key) composites, so it is cut into output
+// chunks on the 256-byte grid exactly like merge_host_pipeline -- each cut
+// co-ranked on the host (its segment by a binary search over the offsets, then
+// the co-rank inside that segment) -- and each chunk is the output range
+// [r0, r0 + len) of the segmented merge of its aligned windows, the segments
+// it touches rebased onto them on the device.  H2D / merge / D2H overlap on
+// three streams.  Requires offsets nondecreasing with a_off[nseg] <= m,
+// b_off[nseg] <= n (checked).
+template <typename K>
+int merge_segmented_host_pipeline(const K* a, const uint64_t* a_off, uint64_t m, const K* b,
+                                  const uint64_t* b_off, uint64_t n, uint64_t nseg, K* out,
+                                  uint64_t* h2d, uint64_t* d2h, uint64_t* merge_ns) {
+    host_streams& hs = hstreams();
+    const uint64_t total = m + n;
+    constexpr uint64_t G = 64;
+    const uint64_t parts = std::max<uint64_t>(1, std::min<uint64_t>(8, total >> 18));
+    std::vector<uint64_t> cuts(1, 0);
+    for (uint64_t q = 1; q <= parts; ++q) {
+        const uint64_t c = q == parts ? total : total * q / parts / G * G;
+        if (c > cuts.back()) cuts.push_back(c);
+    }
+    const uint64_t nchunks = cuts.size() - 1;
+    uint64_t chunk = 0;
+    for (uint64_t c = 0; c < nchunks; ++c) chunk = std::max(chunk, cuts[c + 1] - cuts[c]);
+    // composite co-rank of output rank i: (j, segment)
+    auto seg_of = [&](uint64_t i) {  // largest s < nseg with a_off[s] + b_off[s] <= i
+        uint64_t lo = 0, hi = nseg - 1;
+        while (lo < hi) {
+            const uint64_t mid = lo + (hi - lo + 1) / 2;
+            if (a_off[mid] + b_off[mid] <= i)
+                lo = mid;
+            else
+                hi = mid - 1;
+        }
+        return lo;
+    };
+    auto split = [&](uint64_t i, uint64_t& j, uint64_t& sg) {
+        sg = seg_of(i);
+        const uint64_t as = a_off[sg], bs = b_off[sg];
+        const uint64_t li = i - as - bs;
+        j = as + co_rank_split<K, uint64_t>(li, a + as, a_off[sg + 1] - as, b + bs,
+                                            b_off[sg + 1] - bs, [](const K* p) { return *p; });
+    };
+    auto first_seg = [&](const uint64_t* off, uint64_t x) {  // a segment holding index x (or before)
+        const uint64_t* p = std::upper_bound(off, off + nseg + 1, x);
+        const uint64_t s = uint64_t(p - off);
+        return s == 0 ? 0 : std::min<uint64_t>(s - 1, nseg - 1);
+    };
+    // device: the offsets once, then three slots of windows + rebased offsets
+    const uint64_t wcap = chunk + 2 * G;
+    const size_t kb = round256(wcap * sizeof(K)), ob = round256((nseg + 1) * 8);
+    const size_t slot_bytes = 3 * kb + 2 * ob;
+    void* buf = nullptr;
+    cudaError_t e = pool_alloc(&buf, 2 * ob + 3 * slot_bytes, hs.comp);
+    if (e != cudaSuccess) return cuda_fail(e, "comerge: segmented host pipeline staging");
+    uint64_t* dAoff = static_cast<uint64_t*>(buf);
+    uint64_t* dBoff = reinterpret_cast<uint64_t*>(static_cast<unsigned char*>(buf) + ob);
+    unsigned char* slots = static_cast<unsigned char*>(buf) + 2 * ob;
+    cudaEventRecord(hs.in_done[0], hs.comp);
+    cudaStreamWaitEvent(hs.h2d, hs.in_done[0], 0);
+    int rc = COMERGE_OK;
+    auto h2d_copy = [&](void* dst, const void* src, size_t bytes) {
+        if (!bytes || rc) return;
+        const cudaError_t ce = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, hs.h2d);
+        if (ce != cudaSuccess) rc = cuda_fail(ce, "comerge: host pipeline host->device copy");
+    };
+    auto d2h_copy = [&](void* dst, const void* src, size_t bytes) {
+        if (!bytes || rc) return;
+        const cudaError_t ce = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, hs.d2h);
+        if (ce != cudaSuccess) rc = cuda_fail(ce, "comerge: host pipeline device->host copy");
+    };
+    h2d_copy(dAoff, a_off, (nseg + 1) * 8);
+    h2d_copy(dBoff, b_off, (nseg + 1) * 8);
+    std::vector<uint64_t> js(nchunks + 1), ss(nchunks + 1);
+    js[0] = 0;
+    ss[0] = 0;
+    bool first = true;
+    for (uint64_t c = 0; c < nchunks && rc == COMERGE_OK; ++c) {
+        const int sl = int(c % 3);
+        unsigned char* base = slots + sl * slot_bytes;
+        K* dA = reinterpret_cast<K*>(base);
+        K* dB = reinterpret_cast<K*>(base + kb);
+        K* dO = reinterpret_cast<K*>(base + 2 * kb);
+        uint64_t* dAo = reinterpret_cast<uint64_t*>(base + 3 * kb);
+        uint64_t* dBo = reinterpret_cast<uint64_t*>(base + 3 * kb + ob);
+        const uint64_t i0 = cuts[c], i1 = cuts[c + 1];
+        if (c + 1 < nchunks)
+            split(i1, js[c + 1], ss[c + 1]);
+        else
+            js[c + 1] = m, ss[c + 1] = nseg - 1;
+        const uint64_t j0 = js[c], j1 = js[c + 1], k0 = i0 - j0, k1 = i1 - j1;
+        const uint64_t sa = j0 / G * G, ea = std::min(m, div_up(j1, G) * G);
+        const uint64_t sb = k0 / G * G, eb = std::min(n, div_up(k1, G) * G);
+        if (c >= 3) cudaStreamWaitEvent(hs.h2d, hs.out_done[sl], 0);
+        h2d_copy(dA, a + sa, (ea - sa) * sizeof(K));
+        h2d_copy(dB, b + sb, (eb - sb) * sizeof(K));
+        *h2d += (i1 - i0) * sizeof(K);
+        cudaEventRecord(hs.in_done[sl], hs.h2d);
+        if (rc) break;
+        cudaStreamWaitEvent(hs.comp, hs.in_done[sl], 0);
+        if (first) {
+            cudaEventRecord(hs.t0, hs.comp);
+            first = false;
+        }
+        // the segments the windows touch, rebased onto them
+        const uint64_t s_lo = std::min(first_seg(a_off, sa), first_seg(b_off, sb));
+        const uint64_t s_hi = std::max(ss[c + 1], s_lo);
+        const uint64_t ns = s_hi - s_lo + 1;
+        const uint64_t la = j1 - sa, lb = k1 - sb;
+        rebase_offsets_kernel<<<unsigned(div_up(ns + 1, 256)), 256, 0, hs.comp>>>(
+            dAoff, dBoff, s_lo, ns, sa, la, sb, lb, dAo, dBo);
+        if ((rc = check_launch("comerge: offsets rebase launch"))) break;
+        pipe_pieces range;
+        range.out_base = (j0 - sa) + (k0 - sb);
+        range.out_end = range.out_base + (i1 - i0);
+        rc = launch_pipe<K, false, 1>(dA, nullptr, la, dB, nullptr, lb, dO, nullptr, dAo, dBo, ns,
+                                      nullptr, 0, hs.comp, 0, &range);
+        cudaEventRecord(hs.merged[sl], hs.comp);
+        cudaStreamWaitEvent(hs.d2h, hs.merged[sl], 0);
+        const uint64_t h = std::min(i1, i0 + (j1 - j0 + G / 2) / G * G) - i0;
+        d2h_copy(out + i0, dO, h * sizeof(K));
+        d2h_copy(out + i0 + h, dO + h, (i1 - i0 - h) * sizeof(K));
+        *d2h += (i1 - i0) * sizeof(K);
+        cudaEventRecord(hs.out_done[sl], hs.d2h);
+    }
+    cudaEventRecord(hs.t1, hs.comp);
+    cudaEventRecord(hs.in_done[0], hs.d2h);
+    cudaStreamWaitEvent(hs.comp, hs.in_done[0], 0);
+    cudaFreeAsync(buf, hs.comp);
+    e = cudaStreamSynchronize(hs.d2h);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(hs.comp);
+    if (e != cudaSuccess) return cuda_fail(e, "comerge: segmented host pipeline");
+    if (rc) return rc;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, hs.t0, hs.t1);
+    *merge_ns = uint64_t(double(ms) * 1e6);
+    return COMERGE_OK;
+}
+
+// comerge_merge_segmented_host_*: host (or device) buffers, synchronous
+template <typename K>
+int merge_segmented_sync(const K* a, const uint64_t* a_off, size_t m, const K* b,
+                         const uint64_t* b_off, size_t n, size_t nseg, K* out, size_t out_len,
+                         comerge_merge_report* rep) {
+    if (m > SIZE_MAX - n)
+        return fail(COMERGE_E_LENGTH, "comerge: combined input length exceeds index range");
+    if (out_len != m + n)
+        return fail(COMERGE_E_INVALID, "merge_segmented: output length must equal |a| + |b|");
+    if (int rc = check_merge_args<K>("merge_segmented", a, m, b, n, out, nullptr, nullptr, nullptr,
+                                     false))
+        return rc;
+    const uint64_t total = uint64_t(m) + n;
+    if (nseg == 0) {
+        if (total) return fail(COMERGE_E_INVALID, "merge_segmented: no segments for nonempty input");
+        if (rep) *rep = comerge_merge_report{};
+        return COMERGE_OK;
+    }
+    if (!a_off || !b_off) return fail(COMERGE_E_INVALID, "merge_segmented: null offsets");
+    const bool dev_off = is_device_ptr(a_off) || is_device_ptr(b_off);
+    std::vector<uint64_t> ha, hb;
+    const uint64_t* pa = a_off;
+    const uint64_t* pb = b_off;
+    if (dev_off) {  // offsets on the device: a host copy for the checks and cuts
+        ha.resize(nseg + 1);
+        hb.resize(nseg + 1);
+        cudaError_t e = cudaMemcpy(ha.data(), a_off, (nseg + 1) * 8, cudaMemcpyDefault);
+        if (e == cudaSuccess) e = cudaMemcpy(hb.data(), b_off, (nseg + 1) * 8, cudaMemcpyDefault);
+        if (e != cudaSuccess) return cuda_fail(e, "comerge: segment offsets copy");
+        pa = ha.data();
+        pb = hb.data();
+    }
+    for (size_t q = 0; q < nseg; ++q)
+        if (pa[q] > pa[q + 1] || pb[q] > pb[q + 1])
+            return fail(COMERGE_E_INVALID, "merge_segmented: offsets must be nondecreasing");
+    if (pa[nseg] > m || pb[nseg] > n || pa[0] != 0 || pb[0] != 0)
+        return fail(COMERGE_E_INVALID,
+                    "merge_segmented: offsets must start at 0 and end within the inputs");
+    const bool all_host = total >= (uint64_t(1) << 20) && !dev_off && !is_device_ptr(a) &&
+                          !is_device_ptr(b) && !is_device_ptr(out) && pa[nseg] == m &&
+                          pb[nseg] == n;
+    if (all_host) {
+        const auto w0 = std::chrono::steady_clock::now();
+        uint64_t h2d = 0, d2h = 0, merge_ns = 0;
+        if (int rc = merge_segmented_host_pipeline<K>(a, pa, m, b, pb, n, nseg, out, &h2d, &d2h,
+                                                      &merge_ns))
+            return rc;
+        const auto w1 = std::chrono::steady_clock::now();
+        if (rep) {
+            *rep = comerge_merge_report{};
+            rep->m = m;
+            rep->n = n;
+            rep->workers = 1;
+            rep->wall_ns = merge_ns;
+            rep->e2e_ns = uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(w1 - w0).count());
+            rep->h2d_bytes = h2d;
+            rep->d2h_bytes = d2h;
+            rep->tiles = div_up(total, pipe_layout<K, false, 1>::T);
+        }
+        return COMERGE_OK;
+    }
+    // small or mixed: stage, merge on the device, copy back
+    cudaStream_t s = sync_stream();
+    event_pair e2e, dv;
+    uint64_t h2d = 0, d2h = 0;
+    cudaEventRecord(e2e.a, s);
+    {
+        staged da, db, dao, dbo, dout;
+        int rc;
+        if ((rc = da.in(a, m * sizeof(K), s, &h2d))) return rc;
+        if ((rc = db.in(b, n * sizeof(K), s, &h2d))) return rc;
+        if ((rc = dao.in(a_off, (nseg + 1) * 8, s, &h2d))) return rc;
+        if ((rc = dbo.in(b_off, (nseg + 1) * 8, s, &h2d))) return rc;
+        if ((rc = dout.out_alloc(out, total * sizeof(K), s))) return rc;
+        cudaEventRecord(dv.a, s);
+        if ((rc = merge_segmented_device<K>(static_cast<const K*>(da.dev),
+                                            static_cast<const uint64_t*>(dao.dev), m,
+                                            static_cast<const K*>(db.dev),
+                                            static_cast<const uint64_t*>(dbo.dev), n, nseg,
+                                            static_cast<K*>(dout.dev), nullptr, 0, s)))
+            return rc;
+        cudaEventRecord(dv.b, s);
+        if ((rc = dout.back(out, total * sizeof(K), &d2h))) return rc;
+        cudaEventRecord(e2e.b, s);
+        const cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return cuda_fail(e, "comerge: merge_segmented");
+    }
+    if (rep) {
+        *rep = comerge_merge_report{};
+        rep->m = m;
+        rep->n = n;
+        rep->workers = 1;
+        rep->wall_ns = total ? dv.ns() : 0;
+        rep->e2e_ns = e2e.ns();
+        rep->h2d_bytes = h2d;
+        rep->d2h_bytes = d2h;
+        rep->tiles = div_up(total, pipe_layout<K, false, 1>::T);
+    }
+    return COMERGE_OK;
+}
+
 // The reference's merge_report bookkeeping (parallel.hpp:262-281) from the
 // co-ranks of every worker-block boundary r = 0..workers: block sizes, the
 // co_rank_stats iterations (begin and end per worker; synced: begin only,
@@ -1451,6 +1706,19 @@ int comerge_cuda_merge_segmented_u32(const uint32_t* a, const uint64_t* a_off, s
                                      comerge_stream_t stream) {
     return merge_segmented_device<uint32_t>(a, a_off, m, b, b_off, n, nseg, out, ws, ws_bytes,
                                             stream);
+}
+
+int comerge_merge_segmented_host_i32(const int32_t* a, const uint64_t* a_off, size_t m,
+                                     const int32_t* b, const uint64_t* b_off, size_t n,
+                                     size_t nseg, int32_t* out, size_t out_len,
+                                     comerge_merge_report* report) {
+    return merge_segmented_sync<int32_t>(a, a_off, m, b, b_off, n, nseg, out, out_len, report);
+}
+int comerge_merge_segmented_host_u32(const uint32_t* a, const uint64_t* a_off, size_t m,
+                                     const uint32_t* b, const uint64_t* b_off, size_t n,
+                                     size_t nseg, uint32_t* out, size_t out_len,
+                                     comerge_merge_report* report) {
+    return merge_segmented_sync<uint32_t>(a, a_off, m, b, b_off, n, nseg, out, out_len, report);
 }
 
 size_t comerge_cuda_sort_workspace_bytes(size_t n, int key_kind) {

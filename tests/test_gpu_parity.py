@@ -280,6 +280,53 @@ def test_misaligned_pairs_and_segmented_pipeline(cuda, port, dt):
             assert np.array_equal(host(out), expect), (s0, s1, s2)
 
 
+def _seg_batch(rng, nseg, lo, hi, alphabet, empty_every=0):
+    la, lb = rng.integers(lo, hi + 1, nseg), rng.integers(lo, hi + 1, nseg)
+    if empty_every:
+        la[::empty_every] = 0
+        lb[1::empty_every] = 0
+    sa = np.concatenate([np.sort(rng.integers(0, alphabet, x)) for x in la] +
+                        [np.zeros(0, np.int64)]).astype(np.int32)
+    sb = np.concatenate([np.sort(rng.integers(0, alphabet, x)) for x in lb] +
+                        [np.zeros(0, np.int64)]).astype(np.int32)
+    ao = np.concatenate([[0], np.cumsum(la)]).astype(np.uint64)
+    bo = np.concatenate([[0], np.cumsum(lb)]).astype(np.uint64)
+    return sa, ao, sb, bo
+
+
+def test_segmented_host_buffers(cuda, port):
+    """Host segmented batches (comerge_merge_segmented_host_*): >= 2^20
+    elements through the chunked H2D / merge / D2H pipeline (cuts co-ranked
+    in (segment, key) order, chunk segments rebased on the device), smaller
+    ones staged; pageable and pinned buffers; bit-exact vs the oracle."""
+    rng = np.random.default_rng(31)
+    cases = [_seg_batch(rng, 2000, 1, 4096, 1 << 20),          # C5 shape, 8 M elements
+             _seg_batch(rng, 60000, 0, 40, 50, empty_every=7),  # tiny pairs, empty ones
+             _seg_batch(rng, 1, 1_500_000, 1_500_000, 1000),    # one huge pair
+             _seg_batch(rng, 3, 400_000, 700_000, 3),           # few pairs, heavy ties
+             _seg_batch(rng, 300, 0, 2000, 100)]                # small: staged
+    for sa, ao, sb, bo in cases:
+        expect = port.merge_segmented(sa, ao, sb, bo)
+        out, rep = P().merge_segmented(sa, ao, sb, bo, report=True)
+        assert np.array_equal(out, expect), (len(sa), len(ao))
+        total = len(sa) + len(sb)
+        assert rep.h2d_bytes >= total * 4 and rep.d2h_bytes == total * 4
+    # pinned buffers (page-locked host memory)
+    sa, ao, sb, bo = cases[0]
+    pa = torch.from_numpy(sa).pin_memory().numpy()
+    pb = torch.from_numpy(sb).pin_memory().numpy()
+    po = torch.empty(len(sa) + len(sb), dtype=torch.int32).pin_memory().numpy()
+    P().merge_segmented(pa, ao, pb, bo, out=po)
+    assert np.array_equal(po, port.merge_segmented(sa, ao, sb, bo))
+    # contract
+    with pytest.raises(ValueError, match="nondecreasing"):
+        P().merge_segmented(sa, ao[::-1].copy(), sb, bo)
+    bad = ao.copy()
+    bad[0] = 1
+    with pytest.raises(ValueError, match="start at 0"):
+        P().merge_segmented(sa, bad, sb, bo)
+
+
 def test_random_segmented(cuda, path, port):
     rng = np.random.default_rng(99)
     for dt in (np.int32, np.uint32):
