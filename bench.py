@@ -67,6 +67,17 @@ CONFIGS["C2r"] = dict(kind="records", base="C2", dtype="int32", m=2**24, n=2**24
 CONFIGS["C4r"] = dict(kind="records", base="C4", dtype="uint64", m=2**27, n=2**27, width=0,
                       desc="C4 as 16-byte {uint64 key, uint32 val, pad} records (the "
                            "reference's struct + key-only less)")
+# diagnostic shapes (not BASELINE configs; tools/run_config.py only)
+EXTRA = {
+    "X1": dict(kind="keys", dtype="int32", m=2**26, n=2**26, width=2**31,
+               desc="diagnostic: int32 keys only, m=n=2^26, uniform [0,2^31)"),
+    "X2": dict(kind="pairs", dtype="int32", m=2**26, n=2**26, width=2**31,
+               desc="diagnostic: int32 keys + payload, m=n=2^26, uniform [0,2^31)"),
+    "X3": dict(kind="segmented", dtype="int32", nseg=2**20, maxlen=64, width=2**20,
+               desc="diagnostic: segmented batch of 2^20 small pairs, m_s,n_s in [1,64]"),
+    "X4": dict(kind="segmented", dtype="int32", nseg=2**21, maxlen=16, width=2**20,
+               desc="diagnostic: segmented batch of 2^21 tiny pairs, m_s,n_s in [1,16]"),
+}
 HEADLINE = "C4"
 SEED = 5
 METRIC = "merged elements/s"

@@ -62,10 +62,11 @@ int comerge_cuda_abi_version(void);
 void comerge_cuda_set_kernel_events(void* before, void* after);
 
 /* Kernel selection on the calling thread (testing / benchmarking every
- * device path): 0 = automatic (default: 3 when there are >= 16 pipeline
- * tiles, else 1), 1 = tile kernel (partition + one CTA per tile),
- * 3 = persistent tile-pipeline kernel.  Both take arrays at any element
- * offset (the pipeline stages windows at their address offset modulo 16). */
+ * device path): 0 = automatic (default: 4 up to one wave of tiles, i.e.
+ * 2 x #SMs pipeline tiles, else 3), 1 = tile kernel (partition + one CTA per
+ * tile), 3 = persistent tile-pipeline kernel, 4 = one-wave small-merge kernel
+ * (one CTA per tile, both boundaries co-ranked in the CTA).  All take arrays
+ * at any element offset.  Segmented batches: 1 or else the pipeline. */
 void comerge_cuda_set_path(int path);
 /* Kernel used by the last merge on this thread: 1 = tile kernel (partition
  * + merge launches), 3 = tile pipeline (one launch), 4 = segmented tile

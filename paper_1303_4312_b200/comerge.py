@@ -159,13 +159,14 @@ def co_rank_batch(ranks, a, b, with_stats: bool = False):
 
 # ------------------------------------------------------------------- merges
 
-KERNEL_PATHS = {"auto": 0, "tile": 1, "pipe": 3}
+KERNEL_PATHS = {"auto": 0, "tile": 1, "pipe": 3, "small": 4}
 
 
 def set_kernel_path(path: str = "auto") -> None:
     """Select the device kernel for merges issued from this thread: "auto",
-    "tile" (partition + one CTA per tile; any alignment) or "pipe" (persistent
-    tile pipeline; the default, segmented batches included)."""
+    "tile" (partition + one CTA per tile), "pipe" (persistent tile pipeline;
+    the default above one wave of tiles, segmented batches included) or
+    "small" (one-wave kernel, one CTA per tile; the default up to one wave)."""
     N.lib.comerge_cuda_set_path(KERNEL_PATHS[path])
 
 

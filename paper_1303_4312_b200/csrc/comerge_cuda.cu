@@ -19,6 +19,7 @@
 
 #include "../../include/comerge_cuda.h"
 #include "merge_pipe.cuh"
+#include "merge_small.cuh"
 #include "merge_tile.cuh"
 #include "sort.cuh"
 
@@ -28,7 +29,7 @@ namespace {
 
 thread_local std::string g_error;
 thread_local cudaEvent_t g_ev_before = nullptr, g_ev_after = nullptr;
-thread_local int g_path = 0;  // 0 auto, 1 tile (v1), 3 tile pipeline
+thread_local int g_path = 0;  // 0 auto, 1 tile (v1), 3 tile pipeline, 4 small (one wave)
 thread_local int g_last_path = 0;  // kernel of the last merge: 1 tile, 3 pipe, 4 segmented tile, 5-7 pipe modes
 thread_local unsigned long long* g_trace = nullptr;  // debug: per-CTA timestamps
 // tuning knobs of the tile pipeline (0 = default)
@@ -363,6 +364,33 @@ int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const ui
     return check_launch("comerge: pipeline merge launch");
 }
 
+// One-wave merge of small inputs (merge_small.cuh): one CTA per tile.
+template <typename K, bool HAS_V>
+int launch_small(const K* a, const uint32_t* av, uint64_t m, const K* b, const uint32_t* bv,
+                 uint64_t n, K* out, uint32_t* outv, cudaStream_t s) {
+    using SL = small_layout<K, HAS_V>;
+    static std::once_flag once[kMaxDevices];
+    const int dev = current_device();
+    std::call_once(once[dev], [] {
+        cudaFuncSetAttribute(merge_small_kernel<K, HAS_V>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(SL::kSmem));
+    });
+    const uint64_t ntiles = div_up(m + n, SL::T);
+    small_args args{a, av, m, b, bv, n, out, outv, g_tune_flags & 4096 ? 0u : 1u,
+                    g_tune_flags & 16384 ? 0u : uint32_t(SL::kStop), g_trace};
+    g_last_path = 8;
+    mark_before(s);
+    merge_small_kernel<K, HAS_V><<<unsigned(ntiles), SL::kThreads, SL::kSmem, s>>>(args);
+    mark_after(s);
+    return check_launch("comerge: small merge launch");
+}
+
+// tiles up to which the one-wave small-merge kernel is used (auto path)
+template <typename K, bool HAS_V>
+uint64_t small_tiles_limit() {
+    return 2ull * uint64_t(sm_count());
+}
+
 template <typename K, bool HAS_V>
 int merge_device(const K* a, const uint32_t* av, size_t m, const K* b, const uint32_t* bv,
                  size_t n, K* out, uint32_t* outv, void* ws, size_t ws_bytes, cudaStream_t s) {
@@ -374,7 +402,9 @@ int merge_device(const K* a, const uint32_t* av, size_t m, const K* b, const uin
     // are enough tiles to fill it; records always take it
     using PL = pipe_layout<K, HAS_V>;
     const uint64_t ptiles = div_up(total, PL::T);
-    if (is_rec<K>::value || g_path == 3 || (g_path == 0 && ptiles >= 16))
+    if (g_path == 4 || (g_path == 0 && ptiles <= small_tiles_limit<K, HAS_V>()))
+        return launch_small<K, HAS_V>(a, av, m, b, bv, n, out, outv, s);
+    if (is_rec<K>::value || g_path == 3 || g_path == 0)
         return launch_pipe<K, HAS_V, 0>(a, av, m, b, bv, n, out, outv, nullptr, nullptr, 0, ws,
                                             ws_bytes, s);
     if constexpr (is_rec<K>::value) {

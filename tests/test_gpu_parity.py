@@ -35,9 +35,9 @@ def P():
     return mod
 
 
-@pytest.fixture(params=["tile", "pipe"])
+@pytest.fixture(params=["tile", "pipe", "small"])
 def path(request):
-    """Run a test through each device kernel (v1 tile, the tile pipeline)."""
+    """Run a test through each device kernel (v1 tile, the tile pipeline, the small-merge kernel)."""
     P().set_kernel_path(request.param)
     yield request.param
     P().set_kernel_path("auto")

@@ -1,6 +1,6 @@
 """Run one BASELINE config a few times (for ncu / tracing on the GPU box).
 
-    python tools/run_config.py C2 [--path auto|tile|stream] [--reps 3] [--trace]
+    python tools/run_config.py C2 [--path auto|tile|pipe] [--reps 3] [--trace]
 """
 import argparse
 import ctypes as C
@@ -33,10 +33,10 @@ def main():
     out = bench.alloc_outputs(args.config, inp)
     P.set_kernel_path(args.path)
     N.lib.comerge_cuda_set_tuning(args.static_pct, args.flags, args.lookahead)
-    flush = torch.empty(512 * 2**20 // 4, dtype=torch.int32, device=dev)
+    flush = bench.L2Flush(dev)
     trace = torch.zeros(20 * 4096, dtype=torch.int64, device=dev) if args.trace else None
     for r in range(args.reps):
-        flush.fill_(r)
+        flush()
         if trace is not None and r == args.reps - 1:
             N.lib.comerge_cuda_set_trace(C.c_void_p(trace.data_ptr()))
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
