@@ -640,15 +640,43 @@ def e2e_measure(cfg, inp, steps, warmup):
 # ------------------------------------------------------------------ main
 
 def dist_setup():
+    """One process per GPU (NCCL for the control plane: barriers and the
+    max-over-ranks of the step times; the data path has no collective).  With
+    fewer GPUs than ranks (a test run of the multi-GPU line on one GPU) ranks
+    share devices and the control plane runs over gloo (NCCL refuses two ranks
+    on one device); the ranks' kernels never wait on each other."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world <= 1:
         return None, 0, 1, 0
     import torch
     import torch.distributed as dist
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    return dist, dist.get_rank(), world, local
+    ndev = torch.cuda.device_count()
+    dev_index = local % ndev
+    torch.cuda.set_device(dev_index)
+    if ndev >= world:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+    else:
+        dist.init_process_group("gloo")
+    return dist, dist.get_rank(), world, dev_index
+
+
+def shared_devices(dist):
+    """Ranks share GPUs (fewer devices than ranks: a functional run of the
+    multi-GPU line).  Their kernels then time-slice one device, so a job time
+    is the SUM of the ranks' times, not the max."""
+    import torch
+    return dist is not None and torch.cuda.device_count() < dist.get_world_size()
+
+
+def allreduce_time(dist, values, device):
+    """Job time of a few per-rank times: max over ranks, or the sum when ranks
+    share a device (on the device under NCCL, host under gloo)."""
+    import torch
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor(values, dtype=torch.float64, device=device if on_dev else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM if shared_devices(dist) else dist.ReduceOp.MAX)
+    return [float(x) for x in t.cpu().tolist()]
 
 
 def relaunch_under_torchrun(n):
@@ -784,10 +812,10 @@ def run_split(args, dist, rank, world, device, peak, flush):
             dist.barrier()
 
     res = time_steps(dm.run, args.steps, args.warmup, device, flush, Ctx(), clocks=(rank == 0))
-    t = torch.tensor([sum(res["step_ms"]), statistics.mean(res["kern_ms"])],
-                     dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    step_total, kern = float(t[0].item()), float(t[1].item())
+    step_total, kern = allreduce_time(dist, [sum(res["step_ms"]), statistics.mean(res["kern_ms"])],
+                                      device)
+    if shared_devices(dist):  # per-rank kernel time: the summed one over the ranks
+        kern /= world
     dm.close()
     total = m + n
     balg = 2 * total * elem_bytes(cfg)
@@ -805,6 +833,9 @@ def run_split(args, dist, rank, world, device, peak, flush):
                           algorithmic_bytes_per_launch=balg // world),
             cpu_baseline=None, e2e=None, clocks=res["clocks"],
             gpu_launches=args.steps * launches_per_step(res["path"]))
+        if shared_devices(dist):
+            line["note"] = (f"{world} ranks on {torch.cuda.device_count()} GPU(s): a functional run "
+                            "of the split; ranks time-slice the device, job time = sum of ranks")
         print(json.dumps(line), flush=True)
 
 
@@ -854,9 +885,7 @@ def main():
                       dist_ctx=ctx, clocks=(rank == 0))
     step_total = sum(res["step_ms"])
     if dist:
-        t = torch.tensor([step_total], dtype=torch.float64, device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        step_total = float(t.item())
+        step_total = allreduce_time(dist, [step_total], device)[0]
     head = summarize(cfg, res, peak, n_units=world, max_step_total_ms=step_total)
     legs = rank == 0 and world == 1  # CPU / e2e legs: rank 0 at N = 1 only
 
@@ -905,6 +934,9 @@ def main():
             configs=per_config, sorts=sorts)
         if world > 1:
             line["scaling_note"] = "replicas: an independent instance per GPU (seed + rank)"
+            if shared_devices(dist):
+                line["note"] = (f"{world} ranks on {torch.cuda.device_count()} GPU(s): a functional "
+                                "run; ranks time-slice the device, job time = sum of ranks")
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()

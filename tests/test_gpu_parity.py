@@ -236,7 +236,6 @@ def test_misaligned_pairs_and_segmented_pipeline(cuda, port, dt):
     """The tile pipeline at every element offset mod 16 bytes of keys,
     payloads and outputs (byte-space windows and stores: no alignment cliff),
     large enough for the persistent grid and its dynamic tail."""
-    P().set_kernel_path("auto")
     rng = np.random.default_rng(8)
     tdt = TDT[np.dtype(dt)]
     vece = 16 // np.dtype(dt).itemsize
@@ -251,6 +250,7 @@ def test_misaligned_pairs_and_segmented_pipeline(cuda, port, dt):
         v.copy_(dev(x, cuda))
         return v
 
+    P().set_kernel_path("pipe")
     for sh in [(1, 0, 0, 0, 0, 0), (0, 1, 2, 3, 1, 2), (vece - 1, 1, 0, 1, 3, 1),
                (1, vece - 1, 3, 0, 2, 3), (0, 0, 0, 0, 0, 1)]:
         va, vb = view(a, tdt, sh[0] % vece), view(b, tdt, sh[1] % vece)
@@ -263,6 +263,7 @@ def test_misaligned_pairs_and_segmented_pipeline(cuda, port, dt):
         assert P()._native.lib.comerge_cuda_last_path() == 3
         assert np.array_equal(host(ok), ek) and np.array_equal(host(ov), ev), sh
         assert np.array_equal(host(ok2), ek), sh
+    P().set_kernel_path("auto")
     if dt == np.int32:  # segmented batch, misaligned runs and output
         la, lb = rng.integers(0, 3000, 500), rng.integers(0, 3000, 500)
         sa = np.concatenate([np.sort(rng.integers(0, 99, x)) for x in la]).astype(np.int32)
