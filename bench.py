@@ -634,7 +634,7 @@ def e2e_measure(cfg, inp, steps, warmup):
     med = statistics.median(times)
     return dict(value=total / med, unit="elements/s", stat=f"median of {steps} calls",
                 h2d_bytes_per_step=int(rep.h2d_bytes), d2h_bytes_per_step=int(rep.d2h_bytes),
-                ms_per_step=1e3 * med, path=path)
+                ms_per_step=1e3 * med, path=path, calls_ms=[round(1e3 * t, 3) for t in times])
 
 
 # ------------------------------------------------------------------ main

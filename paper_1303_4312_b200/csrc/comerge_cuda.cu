@@ -335,6 +335,12 @@ int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const ui
         args.epoch = next_tail_epoch();
     }
     args.lookahead = g_tune_lookahead > 0 ? uint32_t(g_tune_lookahead) : 2u;
+    // tail units of 4 tiles but for the last 2 x grid tail tiles (single:
+    // the end balance); flags bits 15-17 override the unit (1 = round 1's
+    // one-tile claims)
+    args.tail_unit = 4u;
+    if (const uint32_t u = (uint32_t(g_tune_flags) >> 15) & 7u) args.tail_unit = u;
+    args.tail_single = 2ull * grid;
     // small inputs: co-rank the first boundaries of every CTA concurrently
     // (their random probes hit L2; on large inputs they would contend in HBM)
     args.eager_start = total * sizeof(K) <= (size_t(32) << 20) ? 1u : 0u;
@@ -722,6 +728,22 @@ host_streams& hstreams() {  // per host thread and device
     return *hs[dev];
 }
 
+// Chunks of a host-buffer merge moving `bytes` each way: ~32 MB per chunk,
+// 8 to 32 of them.  The first H2D and the last D2H run with the other
+// direction idle (a chunk each), every chunk costs ~8 copy commands and a
+// launch.  Measured e2e (tools/e2e_chunks.py): C2 (268 MB each way) 8 / 16 /
+// 32 chunks 6.39 / 6.61 / 7.39 ms; C3 (1.07 GB) 8 / 32 / 64: 24.0 / 23.6 /
+// 23.8 ms; C4 (3.2 GB) 8 / 16 / 32 / 64 / 128: 71.8 / 69.4 / 68.8 / 70.0 /
+// 72.9 ms (6.44 GB in 68.8 ms = 94 GB/s two-way, the link's measured ceiling).
+uint64_t host_chunk_count(uint64_t bytes) {
+    static const long knob = [] {
+        const char* e = std::getenv("COMERGE_HOST_CHUNKS");  // tuning knob (benchmarking)
+        return e ? std::atol(e) : 0L;
+    }();
+    if (knob > 0) return uint64_t(knob);
+    return std::min<uint64_t>(32, std::max<uint64_t>(8, (bytes + (uint64_t(16) << 20)) >> 25));
+}
+
 template <typename K, bool HAS_V>
 int merge_host_pipeline(const K* a, const uint32_t* av, uint64_t m, const K* b,
                         const uint32_t* bv, uint64_t n, K* out, uint32_t* outv, uint64_t* h2d,
@@ -733,15 +755,11 @@ int merge_host_pipeline(const K* a, const uint32_t* av, uint64_t m, const K* b,
     // shape (tools/micro/e2e_model2.cu): the same chunked copies take 6.1 ms
     // with 256-byte aligned windows and 7.2 ms with windows a few elements off.
     constexpr uint64_t G = 64;
-    static const uint64_t parts = [] {
-        const char* e = std::getenv("COMERGE_HOST_CHUNKS");  // tuning knob (benchmarking)
-        const long v = e ? std::atol(e) : 0;
-        return uint64_t(v > 0 ? v : 8);
-    }();
-    // `parts` equal chunks (weights); tried and not better on C2: 6, 12 and 16
-    // chunks, smaller first / last chunks (a chunk's H2D overlaps the previous
-    // chunk's D2H, so the bytes moved with one direction idle stay ~2x the
-    // largest chunk however the sizes ramp), see DESIGN.md section 5
+    const uint64_t parts = host_chunk_count(total * (sizeof(K) + (HAS_V ? 4 : 0)));
+    // `parts` equal chunks (weights); tried and not better: smaller first /
+    // last chunks (a chunk's H2D overlaps the previous chunk's D2H, so the
+    // bytes moved with one direction idle stay ~2x the largest chunk however
+    // the sizes ramp), see DESIGN.md section 5
     std::vector<double> w(parts, 1.0);
     if (const char* ew = std::getenv("COMERGE_HOST_WEIGHTS")) {  // tuning knob (benchmarking)
         w.clear();
@@ -924,7 +942,8 @@ int merge_segmented_host_pipeline(const K* a, const uint64_t* a_off, uint64_t m,
     host_streams& hs = hstreams();
     const uint64_t total = m + n;
     constexpr uint64_t G = 64;
-    const uint64_t parts = std::max<uint64_t>(1, std::min<uint64_t>(8, total >> 18));
+    const uint64_t parts =
+        std::max<uint64_t>(1, std::min<uint64_t>(host_chunk_count(total * sizeof(K)), total >> 18));
     std::vector<uint64_t> cuts(1, 0);
     for (uint64_t q = 1; q <= parts; ++q) {
         const uint64_t c = q == parts ? total : total * q / parts / G * G;

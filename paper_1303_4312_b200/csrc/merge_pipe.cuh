@@ -156,6 +156,13 @@ struct pipe_args {
     unsigned long long* trace;   // optional per-CTA timestamps (8 x u64 per CTA)
     uint64_t static_tiles;       // tiles [0, static_tiles) are split statically (equal shares)
     uint32_t lookahead;          // claim a tail tile when fewer than this are queued
+    // dynamic-tail anchors: the tail warps co-rank every tail_unit-th tail
+    // boundary (and each of the last tail_single) over the whole diagonal --
+    // every probe of such a search misses L2 and pulls a 128-byte line -- and
+    // the boundaries between two anchors bracketed by the first (a few
+    // lines); tail_unit = 1: every boundary over the whole diagonal
+    uint32_t tail_unit;
+    uint64_t tail_single;
     uint64_t* tail;              // dynamic tail workspace (16B aligned): {tag, count} + slots
     uint64_t epoch;              // per-launch tag validating tail state (no memset needed)
     uint32_t eager_start;        // co-rank the first tiles' boundaries concurrently (small inputs)
@@ -830,22 +837,54 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         const uint64_t epoch = scratch[38];
         // co-rank the tail boundaries q = c, c+G, ... (in passes of up to 32,
         // lane groups, full-diagonal brackets) and publish them
-        // slots 0 .. nq-1; boundary NT is trivial for a whole merge, else co-ranked too
-        const uint64_t nq = NT > NS ? NT - NS + (out_end < total ? 1 : 0) : 0;
-        for (uint64_t q0 = c; q0 < nq; q0 += 32 * uint64_t(G)) {
-            uint64_t left = (nq - q0 + G - 1) / G;
+        // slot x = boundary NS + x.  Anchors: x = 0, U, 2U, .. below nbig,
+        // then every x in [nbig, ntail) (the last tail_single tiles); boundary
+        // NT (x = ntail) is trivial for a whole merge, else an anchor too.
+        const uint64_t U = args.tail_unit ? args.tail_unit : 1;
+        const uint64_t ntail = NT > NS ? NT - NS : 0;
+        const uint64_t nsingle = args.tail_single < ntail ? args.tail_single : ntail;
+        const uint64_t nbig = ntail - nsingle;
+        const uint64_t nbu = (nbig + U - 1) / U;
+        auto anchor_x = [=](uint64_t q) {
+            return q <= nbu ? (q * U < nbig ? q * U : nbig) : nbig + (q - nbu);
+        };
+        const uint64_t nanch = ntail ? nbu + nsingle + (out_end < total ? 1 : 0) : 0;
+        auto publish = [&](uint64_t x, boundary bd) {
+            uint64_t* slot = args.tail + kTailSlots + 4 * x;
+            st_pair(slot, bd.j, bd.s);
+            st_pair(slot + 2, tail_hash(epoch, x, bd.j, bd.s), 0);
+        };
+        for (uint64_t q0 = c; q0 < nanch; q0 += 32 * uint64_t(G)) {
+            uint64_t left = (nanch - q0 + G - 1) / G;
             const int k = int(left < 32 ? left : 32);
             const int P = pow2_group(k);
             const int g = lane / P;
             const uint64_t q = q0 + uint64_t(g < k ? g : k - 1) * G;
-            const uint64_t i = diag_of(NS + q);
+            const uint64_t xa = anchor_x(q);
+            const uint64_t i = diag_of(NS + xa);
             uint64_t lo, hi;
             full_bracket(i, lo, hi);
             const boundary bd = find_boundary<K, SEG>(args, i, lo, hi, 0, P, nullptr);
-            if (lane % P == 0 && g < k) {
-                uint64_t* slot = args.tail + kTailSlots + 4 * q;
-                st_pair(slot, bd.j, bd.s);
-                st_pair(slot + 2, tail_hash(epoch, q, bd.j, bd.s), 0);
+            if (lane % P == 0 && g < k) publish(xa, bd);
+            if (U == 1 || q0 >= nbu) continue;  // no inner boundaries in this pass
+            // inner boundaries x in (anchor_x(q), anchor_x(q+1)) of the pass's
+            // anchors, 32 per round (one lane each, binary search), bracketed
+            // by their anchor: j(x) in [j(xa), j(xa) + (i(x) - i(xa))]
+            const int per = int(U - 1);
+            for (int base = 0; base < k * per; base += 32) {
+                const int idx = base + lane;
+                const int ga = idx / per < k ? idx / per : k - 1;
+                const uint64_t qa = q0 + uint64_t(ga) * G;
+                const boundary ba{__shfl_sync(0xffffffffu, bd.j, ga * P),
+                                  __shfl_sync(0xffffffffu, bd.s, ga * P)};
+                const uint64_t x0 = anchor_x(qa), x1 = qa < nbu ? anchor_x(qa + 1) : x0;
+                const uint64_t x = x0 + 1 + uint64_t(idx % per);
+                const bool valid = idx < k * per && x < x1;
+                const uint64_t ix = diag_of(NS + (valid ? x : x0));
+                uint64_t ilo = ba.j, ihi = ba.j;
+                if (valid) step_bracket(ix, diag_of(NS + x0), ba.j, ilo, ihi);
+                const boundary bi = find_boundary<K, SEG>(args, ix, ilo, ihi, ba.s, 1, nullptr);
+                if (valid) publish(x, bi);
             }
         }
         if (args.trace && lane == 0) args.trace[16 * 4096 + 4 * c + 1] = globaltimer_ns();
