@@ -20,5 +20,12 @@ for f in [int(x) for x in sys.argv[1].split(",")]:
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(); P.sort_pairs(k, v, ok, ov, workspace=ws); b.record(); torch.cuda.synchronize()
         if r >= 2: ts.append(a.elapsed_time(b))
-    print("flags", f, "sort_pairs ms", round(statistics.median(ts), 3), flush=True)
+    tk = []
+    for r in range(8):
+        flush.fill_(r)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(); P.sort(k, out=ok, workspace=ws); b.record(); torch.cuda.synchronize()
+        if r >= 2: tk.append(a.elapsed_time(b))
+    print("flags", f, "sort_pairs ms", round(statistics.median(ts), 3), "sort keys ms",
+          round(statistics.median(tk), 3), flush=True)
 N.lib.comerge_cuda_set_tuning(0, 0, 0)

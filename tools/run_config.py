@@ -48,6 +48,12 @@ def main():
         print(f"{args.config} rep {r}: {s.elapsed_time(e) * 1e3:.1f} us "
               f"(path {N.lib.comerge_cuda_last_path()})")
     if trace is not None:
+        report(trace)
+
+
+def report(trace):
+    """Per-CTA phase summary of a traced pipeline launch."""
+    if True:
         rows = trace[: 8 * 4096].view(-1, 8).cpu()
         live = rows[:, 0] > 0
         ext_raw = trace[8 * 4096: 8 * 4096 + 4 * 4096].view(-1, 4).cpu()[live]
