@@ -347,6 +347,7 @@ int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const ui
     // segmented batches: a boundary's segment search probes the (L2-resident)
     // offsets, so concurrent start-up searches are cheap there too
     if (SEG == 1 && !(g_tune_flags & 1024)) args.eager_start = 1u;
+    if (SEG == 2 && (g_tune_flags & 2)) args.eager_start = 1u;  // experiment knob
     args.flags = uint32_t(g_tune_flags);
     // scheduler look-ahead (see merge_pipe.cuh); experiment flags override:
     // bits 2-3 pass cap (1: 8, 2: 16, 3: 32), bits 4-7 look-ahead / 4,

@@ -1021,6 +1021,36 @@ def test_merge_pieces_large_range_with_dynamic_tail(cuda, port, dt):
         assert np.array_equal(host(out), expect[lo:hi]), (lo, hi)
 
 
+@pytest.mark.parametrize("unit", [1, 2, 3, 4, 7])
+def test_tail_anchor_units(cuda, port, unit):
+    """Dynamic-tail anchors (merge_pipe.cuh, pipe_args::tail_unit): every
+    unit-th tail boundary co-ranked over the whole diagonal, the ones between
+    bracketed by it, the last 2 x grid single.  Sizes where the anchored part
+    is not a multiple of the unit; keys-only int32 (duplicate-heavy), key-value
+    int32, and an output range (range merges co-rank the end boundary too)."""
+    import paper_1303_4312_b200._native as N
+    rng = np.random.default_rng(100 + unit)
+    m, n = 11_000_003, 9_500_001  # 2583 int32 tiles: tail 775 (> 2 x 296 singles)
+    a, b = _draw(rng, np.int32, m, 1 << 12), _draw(rng, np.int32, n, 1 << 12)
+    av, bv = tagged(m, n)
+    ek, ev = port.merge(a, b, av, bv)
+    da, db, dav, dbv = dev(a, cuda), dev(b, cuda), dev(av, cuda), dev(bv, cuda)
+    N.lib.comerge_cuda_set_tuning(0, unit << 15, 0)
+    try:
+        P().set_kernel_path("pipe")
+        keys = P().stable_merge(da, db)
+        ok, ov = P().merge_pairs(da, dav, db, dbv)
+        lo, hi = 1_000_001, m + n - 12_345
+        rk = P().merge_pieces([da], [db], lo, hi)
+        torch.cuda.synchronize()
+    finally:
+        N.lib.comerge_cuda_set_tuning(0, 0, 0)
+        P().set_kernel_path("auto")
+    assert np.array_equal(host(keys), ek)
+    assert np.array_equal(host(ok), ek) and np.array_equal(host(ov), ev)
+    assert np.array_equal(host(rk), ek[lo:hi])
+
+
 def test_concurrent_streams_and_host_threads(cuda, port):
     """Reentrancy (async on the caller's stream, reentrant across
     streams, no global mutable state): 4 host threads, each on its own CUDA
