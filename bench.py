@@ -67,6 +67,11 @@ CONFIGS["C2r"] = dict(kind="records", base="C2", dtype="int32", m=2**24, n=2**24
 CONFIGS["C4r"] = dict(kind="records", base="C4", dtype="uint64", m=2**27, n=2**27, width=0,
                       desc="C4 as 16-byte {uint64 key, uint32 val, pad} records (the "
                            "reference's struct + key-only less)")
+# C2 as the reference's OWN tagged<int32_t> (12 bytes: key, origin byte +
+# padding, uint32 index) merged with its tagged_key_less
+CONFIGS["C2t"] = dict(kind="records", base="C2", dtype="int32", m=2**24, n=2**24, width=16,
+                      rec=12, desc="C2 as the reference's tagged<int32_t> (12-byte {int32 key, "
+                                   "origin, uint32 index} records, tagged_key_less)")
 # diagnostic shapes (not BASELINE configs; tools/run_config.py only)
 EXTRA = {
     "X1": dict(kind="keys", dtype="int32", m=2**26, n=2**26, width=2**31,
@@ -90,7 +95,7 @@ def key_bytes(cfg):
 def elem_bytes(cfg):
     c = CONFIGS[cfg]
     if c["kind"] == "records":
-        return 2 * key_bytes(cfg)
+        return c.get("rec", 2 * key_bytes(cfg))
     return key_bytes(cfg) + (4 if c["kind"] == "pairs" else 0)
 
 
@@ -98,6 +103,8 @@ def dtype_str(cfg):
     c = CONFIGS[cfg]
     k = {"int32": "int32", "uint64": "u64"}[c["dtype"]]
     if c["kind"] == "records":
+        if c.get("rec") == 12:
+            return f"12-byte tagged<{k}> records ({k} key, origin byte, u32 index)"
         return f"{elem_bytes(cfg)}-byte records ({k} key + u32 payload)"
     return k + ("+u32 payload" if c["kind"] == "pairs" else "")
 
@@ -109,10 +116,15 @@ def count(cfg, inp):
     return inp["a"].numel() + inp["b"].numel()
 
 
-def pack_records(keys, vals):
+def pack_records(keys, vals, rec=None):
     """Device {key, val} records as a (len, 2) tensor: int32 words for 32-bit
-    keys, int64 words {key, val | pad << 32} (pad 0) for uint64 keys."""
+    keys, int64 words {key, val | pad << 32} (pad 0) for uint64 keys; rec=12:
+    the reference's tagged<int32_t> as (len, 3) int32 words {key, origin (0 for
+    A, 1 for B: the payload's top bit), index (the payload's low 31 bits)}."""
     import torch
+    if rec == 12:
+        v = vals.view(torch.int32)
+        return torch.stack([keys.view(torch.int32), (v >> 31) & 1, v & 0x7FFFFFFF], 1).contiguous()
     if keys.dtype == torch.uint64:
         return torch.stack([keys.view(torch.int64), vals.to(torch.int64)], 1).contiguous()
     return torch.stack([keys.view(torch.int32), vals.view(torch.int32)], 1).contiguous()
@@ -151,7 +163,8 @@ def make_inputs(cfg, seed=SEED, device="cuda"):
     tdt = {"int32": torch.int32, "uint64": torch.uint64}[c["dtype"]]
     if c["kind"] == "records":
         base = make_inputs(c["base"], seed, device)
-        rec = dict(a=pack_records(base["a"], base["av"]), b=pack_records(base["b"], base["bv"]),
+        rec = dict(a=pack_records(base["a"], base["av"], c.get("rec")),
+                   b=pack_records(base["b"], base["bv"], c.get("rec")),
                    m=base["a"].numel(), n=base["b"].numel())
         del base
         return rec
@@ -219,8 +232,11 @@ def alloc_outputs(cfg, inp):
     dev = inp["a"].device
     kind = {"int32": N.KEY_I32, "uint64": N.KEY_U64}[CONFIGS[cfg]["dtype"]]
     if CONFIGS[cfg]["kind"] == "records":
-        wsb = N.lib.comerge_cuda_records_workspace_bytes(inp["m"], inp["n"], kind)
-        return dict(keys=torch.empty((total, 2), dtype=inp["a"].dtype, device=dev),
+        if CONFIGS[cfg].get("rec") == 12:
+            wsb = N.lib.comerge_cuda_records12_workspace_bytes(inp["m"], inp["n"])
+        else:
+            wsb = N.lib.comerge_cuda_records_workspace_bytes(inp["m"], inp["n"], kind)
+        return dict(keys=torch.empty((total, inp["a"].shape[1]), dtype=inp["a"].dtype, device=dev),
                     ws=torch.empty(max(int(wsb), 256), dtype=torch.uint8, device=dev))
     out = dict(keys=torch.empty(total, dtype=inp["a"].dtype, device=dev))
     if CONFIGS[cfg]["kind"] == "segmented":
@@ -248,7 +264,7 @@ def run_config(cfg, inp, out=None):
                       workspace=ws)
     elif kind == "records":
         P.merge_records(inp["a"], inp["b"], out["keys"], key_dtype=CONFIGS[cfg]["dtype"],
-                        workspace=ws)
+                        workspace=ws, record_bytes=CONFIGS[cfg].get("rec"))
     else:
         P.merge_segmented(inp["a"], inp["a_off"], inp["b"], inp["b_off"], out["keys"],
                           workspace=ws)
@@ -503,6 +519,20 @@ def cpu_reference_run(cfg, h, threads):
     std::threads, each calling comerge::stable_merge (merge.hpp:52-68)."""
     from oracle.py import Ref, available_ref, Port
     kind = CONFIGS[cfg]["kind"]
+    if kind == "records" and CONFIGS[cfg].get("rec") == 12 and available_ref():
+        # the reference's own tagged<int32_t> with tagged_key_less
+        from oracle.py import KIND, tagged_dtype
+        if "a_tag" not in h:
+            for side, v in (("a", "av"), ("b", "bv")):
+                t = np.zeros(len(h[side]), tagged_dtype(KIND[np.dtype(h[side].dtype)]))
+                t["key"] = h[side]
+                t["origin"] = (h[v] >> 31).astype(np.uint8)
+                t["index"] = h[v] & np.uint32(0x7FFFFFFF)
+                h[side + "_tag"] = t
+        ref = Ref()
+        o = h.setdefault("out_tag", np.zeros(len(h["a_tag"]) + len(h["b_tag"]), h["a_tag"].dtype))
+        return ref.merge_parallel_tagged(h["a_tag"], h["b_tag"], threads, out=o)[1].wall_ns, \
+            "reference"
     if kind == "records":
         kind = "pairs"
     if available_ref():
@@ -587,11 +617,12 @@ def e2e_measure(cfg, inp, steps, warmup):
 
     if c["kind"] == "records":
         total = count(cfg, inp)
-        path = f"comerge_merge_parallel_records_{suf} (host pinned buffers)"
-        ok = torch.empty((total, 2), dtype=inp["a"].dtype).pin_memory()
+        fname = f"comerge_merge_parallel_records{'12' if c.get('rec') == 12 else ''}_{suf}"
+        path = f"{fname} (host pinned buffers)"
+        ok = torch.empty((total, inp["a"].shape[1]), dtype=inp["a"].dtype).pin_memory()
 
         def call():
-            N.check(getattr(N.lib, f"comerge_merge_parallel_records_{suf}")(
+            N.check(getattr(N.lib, fname)(
                 p(pin["a"]), inp["m"], p(pin["b"]), inp["n"], p(ok), total, 1, 0, C.byref(rep),
                 None, None))
     elif c["kind"] == "segmented":
@@ -894,7 +925,9 @@ def main():
         if legs and not args.no_e2e:
             d["e2e"] = e2e_measure(c, r["inp"], max(5, min(args.steps, 9)), 1)
         if legs and not args.no_cpu:
-            if CONFIGS[c]["kind"] == "records":  # the reference's call is this record form
+            if CONFIGS[c].get("rec") == 12:  # the reference's own tagged<int32_t> merge
+                d["cpu_baseline"] = cpu_baseline(c, make_host_inputs(CONFIGS[c]["base"]))
+            elif CONFIGS[c]["kind"] == "records":  # the reference's call is this record form
                 d["cpu_baseline"] = f"same as {CONFIGS[c]['base']} (the reference merges its " \
                                     "{key, val} structs there)"
             else:

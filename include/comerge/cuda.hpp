@@ -21,9 +21,9 @@
 // own shape -- ranges of a {key, payload} struct with a key-only comparator
 // (merge_parallel(a, b, out, workers, key_less{}); the pattern of tagged<K> /
 // tagged_key_less, oracle.hpp:22-37): any trivially copyable standard-layout
-// struct whose first member `key` is int32_t / uint32_t (8-byte struct) or
-// uint64_t (16-byte struct), the rest of the struct moving with its key byte
-// for byte.  A caller's own key-only comparator is accepted once declared
+// struct whose first member `key` is int32_t / uint32_t (8- or 12-byte struct:
+// the reference's own tagged<int32_t> is 12 bytes) or uint64_t (16-byte
+// struct), the rest of the struct moving with its key byte for byte.  A caller's own key-only comparator is accepted once declared
 // key-only by specialising comerge::cuda::is_key_less.  The SoA overload
 // merge_parallel_pairs (payload uint32_t arrays) is the other form.
 #pragma once
@@ -152,7 +152,8 @@ concept record_type =
     std::is_trivially_copyable_v<T> && std::is_standard_layout_v<T> &&
     requires(T t) { t.key; } && key_type<std::remove_cv_t<decltype(T::key)>> &&
     (offsetof(T, key) == 0) &&
-    ((sizeof(T) == 8 && sizeof(T::key) == 4) || (sizeof(T) == 16 && sizeof(T::key) == 8));
+    ((sizeof(T) == 8 && sizeof(T::key) == 4) || (sizeof(T) == 12 && sizeof(T::key) == 4) ||
+     (sizeof(T) == 16 && sizeof(T::key) == 8));
 
 template <typename R>
 concept record_range = std::ranges::contiguous_range<R> && std::ranges::sized_range<R> &&
@@ -161,8 +162,31 @@ concept record_range = std::ranges::contiguous_range<R> && std::ranges::sized_ra
 template <typename R>
 using elem_of = std::remove_cv_t<std::ranges::range_value_t<R>>;
 
-template <typename K>
+template <typename K, std::size_t S = sizeof(K) == 8 ? 16 : 8>
 struct rec_abi;
+// 12-byte records: the reference's tagged<int32_t> / tagged<uint32_t> layout
+template <>
+struct rec_abi<std::int32_t, 12> {
+    static int merge(const void* a, std::size_t m, const void* b, std::size_t n, void* out,
+                     std::size_t len, std::size_t w, int synced, comerge_merge_report* rep,
+                     std::uint64_t* bs, std::uint32_t* its) {
+        return comerge_merge_parallel_records12_i32(static_cast<const comerge_rec12_i32*>(a), m,
+                                                    static_cast<const comerge_rec12_i32*>(b), n,
+                                                    static_cast<comerge_rec12_i32*>(out), len, w,
+                                                    synced, rep, bs, its);
+    }
+};
+template <>
+struct rec_abi<std::uint32_t, 12> {
+    static int merge(const void* a, std::size_t m, const void* b, std::size_t n, void* out,
+                     std::size_t len, std::size_t w, int synced, comerge_merge_report* rep,
+                     std::uint64_t* bs, std::uint32_t* its) {
+        return comerge_merge_parallel_records12_u32(static_cast<const comerge_rec12_u32*>(a), m,
+                                                    static_cast<const comerge_rec12_u32*>(b), n,
+                                                    static_cast<comerge_rec12_u32*>(out), len, w,
+                                                    synced, rep, bs, its);
+    }
+};
 template <>
 struct rec_abi<std::int32_t> {
     static int merge(const void* a, std::size_t m, const void* b, std::size_t n, void* out,
@@ -380,7 +404,7 @@ merge_report run_merge_records(const A& a, const B& b, Out& out, std::size_t wor
     comerge_merge_report rep{};
     std::vector<std::uint64_t> bs(workers ? workers : 1);
     std::vector<std::uint32_t> its(2 * (workers ? workers : 1));
-    check(rec_abi<K>::merge(std::ranges::data(a), std::ranges::size(a), std::ranges::data(b),
+    check(rec_abi<K, sizeof(T)>::merge(std::ranges::data(a), std::ranges::size(a), std::ranges::data(b),
                             std::ranges::size(b), std::ranges::data(out), std::ranges::size(out),
                             workers, synced ? 1 : 0, &rep, bs.data(), its.data()));
     merge_report r = to_report(rep);

@@ -162,6 +162,22 @@ int comerge_cuda_merge_records_u64(const comerge_rec_u64* a, size_t m, const com
                                    size_t n, comerge_rec_u64* out, void* ws, size_t ws_bytes,
                                    comerge_stream_t stream);
 
+/* 12-byte records {32-bit key, 8 payload bytes}: the layout of the
+ * reference's own tagged<int32_t> / tagged<uint32_t> (key, origin byte + 3
+ * padding bytes, uint32 index; oracle.hpp:22-27), so a caller's
+ * std::vector<tagged<int32_t>> is merged in place of
+ * comerge::merge_parallel(a, b, out, workers, tagged_key_less{}).  4-byte
+ * aligned arrays.  Workspace from comerge_cuda_records12_workspace_bytes. */
+typedef struct comerge_rec12_i32 { int32_t key; uint32_t w[2]; } comerge_rec12_i32;
+typedef struct comerge_rec12_u32 { uint32_t key; uint32_t w[2]; } comerge_rec12_u32;
+size_t comerge_cuda_records12_workspace_bytes(size_t m, size_t n);
+int comerge_cuda_merge_records12_i32(const comerge_rec12_i32* a, size_t m,
+                                     const comerge_rec12_i32* b, size_t n, comerge_rec12_i32* out,
+                                     void* ws, size_t ws_bytes, comerge_stream_t stream);
+int comerge_cuda_merge_records12_u32(const comerge_rec12_u32* a, size_t m,
+                                     const comerge_rec12_u32* b, size_t n, comerge_rec12_u32* out,
+                                     void* ws, size_t ws_bytes, comerge_stream_t stream);
+
 /* Segmented batch: pair s merges a[a_off[s], a_off[s+1]) with
  * b[b_off[s], b_off[s+1]) into out[a_off[s]+b_off[s], ...).  a_off / b_off
  * hold nseg+1 nondecreasing offsets (device memory) with a_off[0] =
@@ -289,6 +305,16 @@ int comerge_merge_parallel_records_u64(const comerge_rec_u64* a, size_t m,
                                        size_t out_len, size_t workers, int synced,
                                        comerge_merge_report* report, uint64_t* block_sizes,
                                        uint32_t* corank_iterations);
+int comerge_merge_parallel_records12_i32(const comerge_rec12_i32* a, size_t m,
+                                         const comerge_rec12_i32* b, size_t n,
+                                         comerge_rec12_i32* out, size_t out_len, size_t workers,
+                                         int synced, comerge_merge_report* report,
+                                         uint64_t* block_sizes, uint32_t* corank_iterations);
+int comerge_merge_parallel_records12_u32(const comerge_rec12_u32* a, size_t m,
+                                         const comerge_rec12_u32* b, size_t n,
+                                         comerge_rec12_u32* out, size_t out_len, size_t workers,
+                                         int synced, comerge_merge_report* report,
+                                         uint64_t* block_sizes, uint32_t* corank_iterations);
 
 /* Segmented batch with HOST (or device) buffers -- the reference's C5
  * baseline is a loop of comerge::stable_merge over independent pairs

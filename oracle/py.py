@@ -164,6 +164,15 @@ class RefReport(C.Structure):
                 ("has_comparisons", C.c_int32), ("pad", C.c_int32)]
 
 
+def tagged_dtype(kind: int):
+    """numpy mirror of the reference's comerge::tagged<K> (oracle.hpp:22-27):
+    key, origin byte (+ padding), uint32 index."""
+    ks = 8 if DTYPE[kind] == np.uint64 else 4
+    return np.dtype({"names": ["key", "origin", "index"],
+                     "formats": [DTYPE[kind], np.uint8, np.uint32],
+                     "offsets": [0, ks, ks + 4], "itemsize": ks + 8})
+
+
 def kv_dtype(kind: int):
     """numpy mirror of ref_shim.cpp's kv_i32 / kv_u32 / kv_u64 structs."""
     return np.dtype([("key", DTYPE[kind]), ("val", np.uint32)], align=True)
@@ -190,6 +199,11 @@ class Ref:
                                               C.c_size_t, C.c_size_t, C.c_int, C.c_int,
                                               C.POINTER(RefReport), _p, _p]
         lib.ref_plan.argtypes = [C.c_int, _p, C.c_size_t, _p, C.c_size_t, C.c_size_t, _p]
+        lib.ref_tagged_size.argtypes = [C.c_int]
+        lib.ref_tagged_size.restype = C.c_size_t
+        lib.ref_merge_parallel_tagged.argtypes = [C.c_int, _p, C.c_size_t, _p, C.c_size_t, _p,
+                                                  C.c_size_t, C.c_size_t, C.c_int,
+                                                  C.POINTER(RefReport)]
         lib.ref_merge_segmented.argtypes = [C.c_int, _p, _p, _p, _p, C.c_size_t, _p, C.c_int,
                                             C.POINTER(_u64)]
         lib.ref_oracle_merge_tagged.argtypes = [_p, C.c_size_t, _p, C.c_size_t, _p, _p, _p]
@@ -199,6 +213,7 @@ class Ref:
         assert lib.ref_report_size() == C.sizeof(RefReport)
         for k in (0, 1, 2):
             assert lib.ref_kv_size(k) == kv_dtype(k).itemsize
+            assert lib.ref_tagged_size(k) == tagged_dtype(k).itemsize
         self.lib = lib
 
     def _check(self, rc):
@@ -239,6 +254,18 @@ class Ref:
                                                 int(synced), int(count), C.byref(rep), ptr(bs),
                                                 ptr(its)))
         return out, rep, bs, its
+
+    def merge_parallel_tagged(self, a, b, workers, synced=False, out=None):
+        """comerge::merge_parallel over the reference's tagged<K> with
+        tagged_key_less; a / b: numpy arrays of tagged_dtype(kind)."""
+        kind = KIND[np.dtype(a.dtype["key"])]
+        if out is None:
+            out = np.empty(len(a) + len(b), dtype=a.dtype)
+        rep = RefReport()
+        self._check(self.lib.ref_merge_parallel_tagged(kind, ptr(a), len(a), ptr(b), len(b),
+                                                       ptr(out), len(out), workers, int(synced),
+                                                       C.byref(rep)))
+        return out, rep
 
     def merge_parallel_kv(self, a_aos, b_aos, workers, simulated=False, synced=False,
                           out=None):

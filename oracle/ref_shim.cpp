@@ -276,6 +276,32 @@ int ref_merge_segmented(int kind, const void* a, const std::uint64_t* a_off, con
     });
 }
 
+// merge_parallel over the reference's OWN tagged<K> with its tagged_key_less
+// (oracle.hpp:22-37; parallel.hpp:304-317): 12-byte records for 32-bit keys,
+// 16-byte for uint64 (see ref_tagged_size)
+std::size_t ref_tagged_size(int kind) {
+    return kind == K_U64 ? sizeof(comerge::tagged<std::uint64_t>)
+                         : kind == K_U32 ? sizeof(comerge::tagged<std::uint32_t>)
+                                         : sizeof(comerge::tagged<std::int32_t>);
+}
+
+int ref_merge_parallel_tagged(int kind, const void* a, std::size_t m, const void* b,
+                              std::size_t n, void* out, std::size_t out_len, std::size_t workers,
+                              int synced, ref_report* rep) {
+    return dispatch_key(kind, [&](auto tag) {
+        using T = comerge::tagged<decltype(tag)>;
+        return guarded([&] {
+            const std::span<const T> av(static_cast<const T*>(a), m);
+            const std::span<const T> bv(static_cast<const T*>(b), n);
+            std::span<T> ov(static_cast<T*>(out), out_len);
+            const comerge::merge_report r =
+                synced ? comerge::merge_parallel_synced(av, bv, ov, workers, comerge::tagged_key_less{})
+                       : comerge::merge_parallel(av, bv, ov, workers, comerge::tagged_key_less{});
+            fill_report<T>(r, rep, nullptr, nullptr);
+        });
+    });
+}
+
 // oracle_merge_tagged over uint64 keys: origin 0 = a, 1 = b
 int ref_oracle_merge_tagged(const std::uint64_t* a, std::size_t m, const std::uint64_t* b,
                             std::size_t n, std::uint64_t* keys, std::uint8_t* origin,

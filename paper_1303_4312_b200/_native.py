@@ -78,6 +78,13 @@ def _load():
                                                                       _sz, _p]
         getattr(lib, f"comerge_merge_parallel_records_{suf}").argtypes = [
             _p, _sz, _p, _sz, _p, _sz, _sz, _i, C.POINTER(MergeReport), _p, _p]
+    lib.comerge_cuda_records12_workspace_bytes.argtypes = [_sz, _sz]
+    lib.comerge_cuda_records12_workspace_bytes.restype = _sz
+    for suf in ("i32", "u32"):
+        getattr(lib, f"comerge_cuda_merge_records12_{suf}").argtypes = [_p, _sz, _p, _sz, _p, _p,
+                                                                        _sz, _p]
+        getattr(lib, f"comerge_merge_parallel_records12_{suf}").argtypes = [
+            _p, _sz, _p, _sz, _p, _sz, _sz, _i, C.POINTER(MergeReport), _p, _p]
     lib.comerge_cuda_sort_workspace_bytes.argtypes = [_sz, _i]
     lib.comerge_cuda_sort_workspace_bytes.restype = _sz
     lib.comerge_cuda_sort_pairs_workspace_bytes.argtypes = [_sz, _i]

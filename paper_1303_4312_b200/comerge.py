@@ -365,11 +365,19 @@ _REC_SUFFIX = {"int32": "i32", "uint32": "u32", "uint64": "u64"}
 _REC_SIZE = {"i32": 8, "u32": 8, "u64": 16}
 
 
-def record_dtype(key_dtype):
+def record_dtype(key_dtype, record_bytes=None):
     """numpy dtype of one key-value record (comerge_rec_* in
     include/comerge_cuda.h): the key at offset 0, a uint32 `val`, and for
-    uint64 keys a uint32 `pad` (the C layout of {uint64_t key; uint32_t val;})."""
+    uint64 keys a uint32 `pad` (the C layout of {uint64_t key; uint32_t val;}).
+    record_bytes=12 (32-bit keys): the reference's tagged<int32_t> layout
+    (comerge_rec12_*: key, `origin` byte + 3 padding bytes, uint32 `index`)."""
     name = _dtype_name_of(key_dtype)
+    if record_bytes == 12:
+        if name not in ("int32", "uint32"):
+            raise TypeError("records: 12-byte records have 32-bit keys")
+        return np.dtype({"names": ["key", "origin", "index"],
+                         "formats": [np.dtype(name), np.uint8, np.uint32],
+                         "offsets": [0, 4, 8], "itemsize": 12})
     if name == "uint64":
         return np.dtype({"names": ["key", "val", "pad"], "formats": [np.uint64, np.uint32, np.uint32],
                          "offsets": [0, 8, 12], "itemsize": 16})
@@ -392,27 +400,43 @@ def _rec_count(x, size):
     return nbytes // size
 
 
-def records_workspace_bytes(m: int, n: int, key_dtype) -> int:
+def records_workspace_bytes(m: int, n: int, key_dtype, record_bytes=None) -> int:
     suf = _REC_SUFFIX[_dtype_name_of(key_dtype)]
+    if record_bytes == 12:
+        return int(N.lib.comerge_cuda_records12_workspace_bytes(m, n))
     return int(N.lib.comerge_cuda_records_workspace_bytes(m, n, _KIND[suf]))
 
 
-def merge_records(a, b, out=None, key_dtype=None, workers: int = 1, workspace=None):
+def _rec_abi(suf, size):
+    """(device, host) entry-point names of suf's records of `size` bytes."""
+    if size == 12:
+        if suf == "u64":
+            raise TypeError("records: 12-byte records have 32-bit keys")
+        return f"comerge_cuda_merge_records12_{suf}", f"comerge_merge_parallel_records12_{suf}"
+    if size != _REC_SIZE[suf]:
+        raise TypeError(f"records: {suf} keys take {_REC_SIZE[suf]}-byte (or 12-byte) records")
+    return f"comerge_cuda_merge_records_{suf}", f"comerge_merge_parallel_records_{suf}"
+
+
+def merge_records(a, b, out=None, key_dtype=None, workers: int = 1, workspace=None,
+                  record_bytes=None):
     """Stable merge of key-value records by key alone -- the reference's own
     key-value call shape: merge_parallel<T>(a, b, out, workers, key_less) over
     {key, val} structs (tagged<K> / tagged_key_less, oracle.hpp:22-37;
     parallel.hpp:304-317).  Ties keep A first, then input order; every record
     is copied whole (payload and padding bytes).
 
-    Host: numpy structured arrays of record_dtype(key) (synchronous; returns
-    (out, MergeReport)).  Device: CUDA tensors of any dtype holding whole
-    records (e.g. int64 of shape (n, 2) for uint64-key records), `key_dtype`
-    given (asynchronous on the current stream; returns out)."""
+    Host: numpy structured arrays of record_dtype(key[, 12]) (synchronous;
+    returns (out, MergeReport)).  Device: CUDA tensors of any dtype holding
+    whole records (e.g. int64 of shape (n, 2) for uint64-key records),
+    `key_dtype` given, `record_bytes` 12 for the tagged<int32_t> layout
+    (asynchronous on the current stream; returns out)."""
     if _is_torch(a) and a.is_cuda:
         if key_dtype is None:
             raise TypeError("merge_records: key_dtype is required for device tensors")
         suf = _REC_SUFFIX[_dtype_name_of(key_dtype)]
-        size = _REC_SIZE[suf]
+        size = record_bytes or _REC_SIZE[suf]
+        dev_fn, _ = _rec_abi(suf, size)
         m, n = _rec_count(a, size), _rec_count(b, size)
         if out is None:
             out = torch.empty((m + n) * size // a.element_size(), dtype=a.dtype, device=a.device)
@@ -420,12 +444,13 @@ def merge_records(a, b, out=None, key_dtype=None, workers: int = 1, workspace=No
             raise ValueError("merge_records: output length must equal |a| + |b|")
         wsp, wsb = _ws(workspace)
         with _on(a):
-            N.check(getattr(N.lib, f"comerge_cuda_merge_records_{suf}")(
-                _ptr(a), m, _ptr(b), n, _ptr(out), wsp, wsb, _stream(a)))
+            N.check(getattr(N.lib, dev_fn)(_ptr(a), m, _ptr(b), n, _ptr(out), wsp, wsb,
+                                           _stream(a)))
         return out
     kd = a.dtype["key"] if a.dtype.names else key_dtype
     suf = _REC_SUFFIX[_dtype_name_of(kd)]
-    size = _REC_SIZE[suf]
+    size = record_bytes or a.dtype.itemsize
+    _, host_fn = _rec_abi(suf, size)
     if a.dtype.itemsize != size or b.dtype != a.dtype:
         raise TypeError(f"merge_records: a and b must be {size}-byte records of one dtype")
     m, n = len(a), len(b)
@@ -436,7 +461,7 @@ def merge_records(a, b, out=None, key_dtype=None, workers: int = 1, workspace=No
     rep = N.MergeReport()
     bs = np.zeros(workers, np.uint64)
     its = np.zeros(2 * workers, np.uint32)
-    N.check(getattr(N.lib, f"comerge_merge_parallel_records_{suf}")(
+    N.check(getattr(N.lib, host_fn)(
         _ptr(a), m, _ptr(b), n, _ptr(out), len(out), workers, 0, C.byref(rep),
         C.c_void_p(bs.ctypes.data), C.c_void_p(its.ctypes.data)))
     return out, MergeReport(m=rep.m, n=rep.n, workers=rep.workers, wall_ns=rep.wall_ns,

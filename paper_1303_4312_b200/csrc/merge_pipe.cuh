@@ -88,10 +88,12 @@ struct pipe_cfg<uint64_t, true> {
 };
 
 // key-value records (records.cuh): 8-byte records as the 32-bit key-value
-// tile (3840 outputs), 16-byte records 1792 outputs, 3 stages of ~29 KB
+// tile (3840 outputs), 12-byte records 2816 outputs (odd VT: 33-word thread
+// stride, conflict-free staging), 16-byte records 1792 outputs; 3 stages of
+// 29-34 KB
 template <typename KT, int S, int A>
 struct pipe_cfg<rec<KT, S, A>, false> {
-    static constexpr int NC = 256, VT = S == 8 ? 15 : 7, NST = 3;
+    static constexpr int NC = 256, VT = S == 8 ? 15 : (S == 12 ? 11 : 7), NST = 3;
 };
 
 // SEG: 0 plain merge, 1 segmented batch (explicit offsets), 2 merge pass

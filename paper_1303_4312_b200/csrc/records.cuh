@@ -6,8 +6,9 @@
 // A record is S bytes: the key (int32 / uint32 / uint64) at offset 0 and
 // S - sizeof(key) bytes of payload that travel with it untouched (padding
 // included, so a record is copied byte for byte).  S = 8 ({32-bit key,
-// uint32 val}) or 16 ({uint64 key, uint32 val, 4 bytes padding}: the
-// reference's struct layout).  A is the alignment every record position has in
+// uint32 val}), 12 ({32-bit key, 8 bytes}: the reference's tagged<int32_t>)
+// or 16 ({uint64 key, uint32 val, 4 bytes padding}: the reference's struct
+// layout, and its tagged<uint64_t>).  A is the alignment every record position has in
 // global and shared memory for a launch (the arrays' common alignment), used
 // for vector shared-memory accesses: the pipeline keeps windows at their
 // address offset modulo 16, so a record's shared position has the alignment of
@@ -130,6 +131,32 @@ struct smem_io<rec<uint64_t, 16, A>> {
                          : "memory");
             asm volatile("st.shared.b64 [%0], %1;" ::"r"(addr + 8), "l"(v) : "memory");
         }
+    }
+};
+
+// 12-byte records {32-bit key, 8 payload bytes} -- the reference's own
+// tagged<int32_t> / tagged<uint32_t> (key, origin byte + 3 padding bytes,
+// uint32 index; oracle.hpp:22-27): three 32-bit accesses (a 12-byte record
+// position is 4-byte aligned in general)
+template <typename KT, int A>
+struct smem_io<rec<KT, 12, A>> {
+    using R = rec<KT, 12, A>;
+    static __device__ __forceinline__ R ld(uint32_t addr) {
+        uint32_t k, v0, v1;
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(k) : "r"(addr));
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v0) : "r"(addr + 4));
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v1) : "r"(addr + 8));
+        R r;
+        r.key = static_cast<KT>(k);
+        r.rest[0] = v0;
+        r.rest[1] = v1;
+        return r;
+    }
+    static __device__ __forceinline__ void st(uint32_t addr, const R& r) {
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(static_cast<uint32_t>(r.key))
+                     : "memory");
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr + 4), "r"(r.rest[0]) : "memory");
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr + 8), "r"(r.rest[1]) : "memory");
     }
 };
 

@@ -260,6 +260,43 @@ static void records() {
             CHECK(out == expect);
             CHECK(rep.block_sizes.size() == workers);
         }
+        // the reference's tagged<int32_t> / tagged<uint32_t>: 12-byte records,
+        // host vectors and (offset) device views
+        static_assert(sizeof(tagged<std::int32_t>) == 12 && sizeof(tagged<std::uint32_t>) == 12);
+        {
+            std::vector<tagged<std::int32_t>> ia(m), ib(n);
+            for (std::size_t i = 0; i < m; ++i)
+                ia[i] = {std::int32_t(ka[i]) - 3, origin::from_a, std::uint32_t(i)};
+            for (std::size_t i = 0; i < n; ++i)
+                ib[i] = {std::int32_t(kb[i]) - 3, origin::from_b, std::uint32_t(i)};
+            const auto iexpect = naive_merge_by_key(ia, ib);
+            for (std::size_t workers : {1, 7}) {
+                std::vector<tagged<std::int32_t>> out(m + n);
+                cm::merge_parallel(ia, ib, out, workers, tagged_key_less{});
+                CHECK(out == iexpect);
+            }
+            std::vector<tagged<std::uint32_t>> ua(m), ub(n);
+            for (std::size_t i = 0; i < m; ++i)
+                ua[i] = {std::uint32_t(ka[i]), origin::from_a, std::uint32_t(i)};
+            for (std::size_t i = 0; i < n; ++i)
+                ub[i] = {std::uint32_t(kb[i]), origin::from_b, std::uint32_t(i)};
+            using U = tagged<std::uint32_t>;
+            U *ua_d = nullptr, *ub_d = nullptr, *uo_d = nullptr;
+            cudaMalloc(&ua_d, (m + 1) * sizeof(U));
+            cudaMalloc(&ub_d, (n + 3) * sizeof(U));
+            cudaMalloc(&uo_d, (m + n + 2) * sizeof(U));
+            cudaMemcpy(ua_d + 1, ua.data(), m * sizeof(U), cudaMemcpyHostToDevice);
+            cudaMemcpy(ub_d + 3, ub.data(), n * sizeof(U), cudaMemcpyHostToDevice);
+            cm::device_span<const U> sa{ua_d + 1, m}, sb{ub_d + 3, n};
+            cm::device_span<U> so{uo_d + 2, m + n};
+            cm::stable_merge(sa, sb, so, tagged_key_less{});
+            std::vector<U> back(m + n);
+            cudaMemcpy(back.data(), uo_d + 2, (m + n) * sizeof(U), cudaMemcpyDeviceToHost);
+            CHECK(back == naive_merge_by_key(ua, ub));
+            cudaFree(ua_d);
+            cudaFree(ub_d);
+            cudaFree(uo_d);
+        }
         // 8-byte records with 32-bit keys, on the device
         std::vector<cm::record<std::int32_t>> ra(m), rb(n);
         for (std::size_t i = 0; i < m; ++i) ra[i] = {std::int32_t(ka[i]) - 7, std::uint32_t(i)};

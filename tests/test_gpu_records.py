@@ -159,3 +159,98 @@ def test_records_c2_c4_shapes_full_size(cuda):
         check(got, a, b)
         del a, b, got
         torch.cuda.empty_cache()
+
+
+# ---- 12-byte records: the reference's OWN tagged<int32_t> / tagged<uint32_t>
+# (oracle.hpp:22-27: key, origin byte + 3 padding bytes, uint32 index),
+# merged by comerge::merge_parallel(..., tagged_key_less{}) in oracle/_ref.
+
+T_REC12 = 256 * 11  # pipeline tile of 12-byte records
+
+
+def tagged(keys, origin):
+    """Records in the reference's tagged<K> layout; the padding bytes carry a
+    pattern of the index (they must travel with their record)."""
+    from oracle.py import KIND, tagged_dtype
+    r = np.zeros(len(keys), tagged_dtype(KIND[np.dtype(keys.dtype)]))
+    r["key"] = keys
+    r["origin"] = origin
+    r["index"] = np.arange(len(keys), dtype=np.uint32)
+    raw = r.view(np.uint8).reshape(len(keys), 12)
+    raw[:, 5:8] = (r["index"][:, None] >> np.array([0, 8, 16], np.uint32)).astype(np.uint8) ^ 0xA5
+    return r
+
+
+def check_tagged(got, a, b):
+    """Byte for byte against comerge::merge_parallel over tagged<K> with
+    tagged_key_less (the reference, hardware_concurrency workers)."""
+    from oracle.py import Ref
+    ref = Ref()
+    expect, rep = ref.merge_parallel_tagged(a, b, max(1, ref.hardware_concurrency()))
+    assert rep.m == len(a) and rep.n == len(b)
+    assert got.tobytes() == expect.tobytes()
+
+
+def device_merge12(a, b, cuda, offs=(0, 0, 0)):
+    kd = a["key"].dtype
+    ta, tb = on_device(a, cuda, offs[0]), on_device(b, cuda, offs[1])
+    obuf = torch.full(((len(a) + len(b)) * 12 + offs[2] + 64,), 0x77, dtype=torch.uint8,
+                      device=cuda)
+    out = obuf[offs[2]:offs[2] + (len(a) + len(b)) * 12]
+    P().merge_records(ta, tb, out, key_dtype=kd, record_bytes=12)
+    torch.cuda.synchronize()
+    h = obuf.cpu().numpy()
+    assert (h[:offs[2]] == 0x77).all() and (h[offs[2] + len(out):] == 0x77).all()
+    return out.cpu().numpy().view(a.dtype)
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.uint32])
+def test_tagged12_device_against_reference(cuda, dt):
+    """Every device path (small-merge kernel, tile pipeline) over tile-boundary,
+    empty, ragged and duplicate-heavy shapes."""
+    rng = np.random.default_rng(1212 + (dt == np.uint32))
+    T = T_REC12
+    shapes = [(0, 0), (0, 1), (1, 0), (T - 1, 0), (0, T + 1), (T, T), (T - 1, 1), (1, T - 1),
+              (2 * T + 3, 5), (5, 3 * T - 2), (3, 50000), (50000, 3), (70001, 69999),
+              (1 << 20, (1 << 20) + 7), (3_000_001, 2_999_999)]
+    shapes += [(int(rng.integers(0, 20000)), int(rng.integers(0, 20000))) for _ in range(6)]
+    for idx, (m, n) in enumerate(shapes):
+        alphabet = [0, 1, 2, 16, 1000][idx % 5]
+        a = tagged(_keys(rng, dt, m, alphabet), 0)
+        b = tagged(_keys(rng, dt, n, alphabet), 1)
+        check_tagged(device_merge12(a, b, cuda), a, b)
+
+
+def test_tagged12_any_record_offset(cuda):
+    """12-byte record positions are 4-byte aligned in general: arrays at byte
+    offsets 0 / 4 / 8 / 12 of an allocation, inputs and output."""
+    rng = np.random.default_rng(5)
+    for m, n in [(100_003, 77_777), (5000, 3), (1_000_000, 1_000_001)]:
+        a = tagged(_keys(rng, np.int32, m, 40), 0)
+        b = tagged(_keys(rng, np.int32, n, 40), 1)
+        for offs in [(0, 0, 0), (4, 8, 12), (12, 4, 8), (8, 12, 4)]:
+            check_tagged(device_merge12(a, b, cuda, offs), a, b)
+
+
+def test_tagged12_host_buffers(cuda):
+    """Host arrays of the reference's tagged<int32_t>: small ones staged,
+    >= 2^20 records through the chunked H2D / merge / D2H pipeline."""
+    rng = np.random.default_rng(12)
+    for m, n, alphabet in [(1000, 999, 7), (1_500_000, 2_100_003, 1000), (3_000_001, 17, 0)]:
+        a = tagged(_keys(rng, np.int32, m, alphabet), 0)
+        b = tagged(_keys(rng, np.int32, n, alphabet), 1)
+        out, rep = P().merge_records(a, b, workers=7)
+        check_tagged(out, a, b)
+        if m + n >= 1 << 20:
+            assert rep.h2d_bytes == (m + n) * 12 == rep.d2h_bytes
+
+
+def test_tagged12_c2_full_size(cuda):
+    """C2 in the reference's tagged<int32_t> form at full size, byte for byte
+    against the reference."""
+    import bench
+    inp = bench.make_inputs("C2", seed=5, device=cuda)
+    a = tagged(inp["a"].cpu().numpy(), 0)
+    b = tagged(inp["b"].cpu().numpy(), 1)
+    del inp
+    check_tagged(device_merge12(a, b, cuda), a, b)
