@@ -62,7 +62,7 @@ P_T = {np.dtype(np.int32): torch.int32, np.dtype(np.uint32): torch.uint32,
 
 
 def one(rng):
-    kinds = ["keys", "pairs", "seg", "sort", "sortp", "pieces", "host", "hostp"]
+    kinds = ["keys", "pairs", "seg", "sort", "sortp", "pieces", "host", "hostp", "rec", "hostrec"]
     kind = kinds[int(rng.integers(0, len(kinds)))]
     dt = [np.int32, np.uint32, np.uint64][int(rng.integers(0, 3))]
     if kind == "seg" and dt == np.uint64:
@@ -122,6 +122,31 @@ def one(rng):
         out = np.empty(m + n, dt)
         P.merge_parallel(a, b, out, int(rng.integers(1, 40)))
         assert np.array_equal(out, port.merge(a, b)), tag
+    elif kind in ("rec", "hostrec"):  # records: 8 / 12 / 16 bytes, merged by key
+        size_b = 16 if dt == np.uint64 else (12 if rng.random() < 0.5 else 8)
+        rd = P.record_dtype(dt, 12 if size_b == 12 else None)
+        vname = "index" if size_b == 12 else "val"
+        ra, rb = np.zeros(m, rd), np.zeros(n, rd)
+        ra["key"], rb["key"] = a, b
+        ra[vname] = np.arange(m, dtype=np.uint32)
+        rb[vname] = np.arange(n, dtype=np.uint32) | np.uint32(1 << 31)
+        ek, ev = port.merge(a, b, ra[vname].copy(), rb[vname].copy())
+        if kind == "hostrec":
+            out, _ = P.merge_records(ra, rb, workers=int(rng.integers(1, 40)))
+        else:  # device, at a random 4-byte offset (8-byte for 16-byte records)
+            step = 8 if size_b == 16 else 4
+            def dview(r):
+                raw = r.view(np.uint8)
+                off = step * int(rng.integers(0, 4))
+                t = torch.zeros(len(raw) + off + 16, dtype=torch.uint8, device=dev)
+                t[off:off + len(raw)] = torch.from_numpy(raw.copy()).to(dev)
+                return t[off:off + len(raw)]
+            o = dview(np.zeros(m + n, rd))
+            P.merge_records(dview(ra), dview(rb), o, key_dtype=dt,
+                            record_bytes=12 if size_b == 12 else None)
+            out = o.cpu().numpy().view(rd)
+        assert np.array_equal(out["key"], ek) and np.array_equal(out[vname], ev), \
+            tag + f" record {size_b} B"
     else:  # host buffers: key-value (misaligned host views sometimes)
         sh = int(rng.integers(0, 3))
         av = np.arange(m, dtype=np.uint32)
@@ -140,8 +165,13 @@ def main():
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     rng = np.random.default_rng(seed)
     t0, counts = time.time(), {}
+    import paper_1303_4312_b200._native as N
     while time.time() - t0 < budget:
+        # sometimes another dynamic-tail anchor unit (pipe_args::tail_unit)
+        unit = int(rng.integers(1, 8)) if rng.random() < 0.3 else 0
+        N.lib.comerge_cuda_set_tuning(0, unit << 15, 0)
         k = one(rng)
+        N.lib.comerge_cuda_set_tuning(0, 0, 0)
         counts[k] = counts.get(k, 0) + 1
     print("fuzz: OK", sum(counts.values()), "rounds", counts, flush=True)
 
