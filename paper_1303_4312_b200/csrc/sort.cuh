@@ -2,9 +2,10 @@
 // "GPU merge sort built on the segmented kernel").
 //
 //   1. block_sort_kernel: every CTA sorts one run of R = NT*VT elements in
-//      shared memory -- VT elements per thread by odd-even transposition in
-//      registers (swap only on strictly-less, so equal keys keep their
-//      order), then log2(NT) rounds of pairwise merges of the sorted lists,
+//      shared memory -- VT elements per thread by a sorting network in
+//      registers (keys only; the key-value variant uses odd-even
+//      transposition, swapping only on strictly-less, so equal keys keep
+//      their order), then log2(NT) rounds of pairwise merges of the sorted lists,
 //      each thread taking VT outputs at its merge-path split (the Lemma-1
 //      split of corank.hpp:93-94, ties to the left list as merge.hpp:22-31).
 //   2. log2(n/R) merge passes of the tile pipeline in merge-pass mode
@@ -29,6 +30,27 @@ struct sort_cfg {
     static constexpr int R = NT * VT;  // base run (a power of two)
 };
 
+// Batcher's odd-even merge sort network over the VT registers of a thread
+// (keys only: equal keys are indistinguishable, so the network need not be
+// stable): 63 compare-exchanges for 16 keys, 19 for 8, against 120 / 28 for
+// odd-even transposition; min / max of 32-bit keys are one instruction each.
+template <typename K, int VT>
+__device__ __forceinline__ void network_sort(K (&k)[VT]) {
+#pragma unroll
+    for (int p = 1; p < VT; p <<= 1)
+#pragma unroll
+        for (int q = p; q >= 1; q >>= 1)
+#pragma unroll
+            for (int j = q % p; j + q < VT; j += 2 * q)
+#pragma unroll
+                for (int i = 0; i < q && i + j + q < VT; ++i)
+                    if ((i + j) / (2 * p) == (i + j + q) / (2 * p)) {
+                        const K x = k[i + j], y = k[i + j + q];
+                        k[i + j] = y < x ? y : x;
+                        k[i + j + q] = y < x ? x : y;
+                    }
+}
+
 // Shared-memory index with one pad word per 32 elements: thread t's VT
 // consecutive elements (t*VT + v) then fall in distinct banks across a warp
 // (without it VT = 16 is a 16-way bank conflict on every staging access).
@@ -50,17 +72,7 @@ __global__ void __launch_bounds__(sort_cfg<K>::NT)
     K k[VT];
 #pragma unroll
     for (int v = 0; v < VT; ++v) k[v] = s[spad(t * VT + v)];
-#pragma unroll
-    for (int pass = 0; pass < VT; ++pass) {
-#pragma unroll
-        for (int v = pass & 1; v + 1 < VT; v += 2) {
-            if (k[v + 1] < k[v]) {
-                const K x = k[v];
-                k[v] = k[v + 1];
-                k[v + 1] = x;
-            }
-        }
-    }
+    network_sort<K, VT>(k);
     for (int w = VT; w < R; w *= 2) {
         __syncthreads();  // previous round's reads are done
 #pragma unroll
