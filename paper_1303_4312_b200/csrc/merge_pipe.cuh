@@ -1425,12 +1425,20 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
         // element x of the tile at stage + o_shift + x * sizeof(K) (store_window)
         const uint32_t ko = smem_addr(stage) + o_shift + uint32_t(tid * VT) * uint32_t(sizeof(K));
         const uint32_t vo = smem_addr(svb) + ov_shift + uint32_t(tid * VT) * 4u;
+        if (cnt == VT) {  // every thread but a partial tile's last: no per-store test
 #pragma unroll
-        for (int v = 0; v < VT; ++v)
-            if (v < cnt) {
+            for (int v = 0; v < VT; ++v) {
                 smem_io<K>::st(ko + uint32_t(v) * uint32_t(sizeof(K)), keys[v]);
                 if constexpr (HAS_V) smem_io<uint32_t>::st(vo + uint32_t(v) * 4u, src[v]);
             }
+        } else {
+#pragma unroll
+            for (int v = 0; v < VT; ++v)
+                if (v < cnt) {
+                    smem_io<K>::st(ko + uint32_t(v) * uint32_t(sizeof(K)), keys[v]);
+                    if constexpr (HAS_V) smem_io<uint32_t>::st(vo + uint32_t(v) * 4u, src[v]);
+                }
+        }
         fence_proxy_async_smem();
         named_bar_sync(1, NC);
         const unsigned long long p3 = args.trace && tid == 0 ? globaltimer_ns() : 0;
