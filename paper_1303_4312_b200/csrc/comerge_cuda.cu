@@ -743,19 +743,20 @@ host_streams& hstreams() {  // per host thread and device
 }
 
 // Chunks of a host-buffer merge moving `bytes` each way: ~32 MB per chunk,
-// 8 to 32 of them.  The first H2D and the last D2H run with the other
+// 2 to 32 of them.  The first H2D and the last D2H run with the other
 // direction idle (a chunk each), every chunk costs ~8 copy commands and a
-// launch.  Measured e2e (tools/e2e_chunks.py): C2 (268 MB each way) 8 / 16 /
-// 32 chunks 6.39 / 6.61 / 7.39 ms; C3 (1.07 GB) 8 / 32 / 64: 24.0 / 23.6 /
-// 23.8 ms; C4 (3.2 GB) 8 / 16 / 32 / 64 / 128: 71.8 / 69.4 / 68.8 / 70.0 /
-// 72.9 ms (6.44 GB in 68.8 ms = 94 GB/s two-way, the link's measured ceiling).
+// launch.  Measured e2e (tools/e2e_chunks.py): C1 (8.4 MB each way) 2 / 4 / 8
+// chunks 0.33 / 0.35 / 0.38 ms; C2 (268 MB) 4 / 8 / 16 / 32 chunks 6.76 /
+// 6.39 / 6.61 / 7.39 ms; C3 (1.07 GB) 8 / 32 / 64: 24.0 / 23.6 / 23.8 ms; C4
+// (3.2 GB) 8 / 16 / 32 / 64 / 128: 71.8 / 69.4 / 68.8 / 70.0 / 72.9 ms
+// (6.44 GB in 68.8 ms = 94 GB/s two-way, the link's measured ceiling).
 uint64_t host_chunk_count(uint64_t bytes) {
     static const long knob = [] {
         const char* e = std::getenv("COMERGE_HOST_CHUNKS");  // tuning knob (benchmarking)
         return e ? std::atol(e) : 0L;
     }();
     if (knob > 0) return uint64_t(knob);
-    return std::min<uint64_t>(32, std::max<uint64_t>(8, (bytes + (uint64_t(16) << 20)) >> 25));
+    return std::min<uint64_t>(32, std::max<uint64_t>(2, (bytes + (uint64_t(16) << 20)) >> 25));
 }
 
 template <typename K, bool HAS_V>
