@@ -273,7 +273,7 @@ template <typename K, bool HAS_V, int SEG>
 int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const uint32_t* bv,
                 uint64_t n, K* out, uint32_t* outv, const uint64_t* aoff, const uint64_t* boff,
                 uint64_t nseg, void* ws, size_t ws_bytes, cudaStream_t s, uint64_t run_len = 0,
-                const pipe_pieces* pieces = nullptr) {
+                const pipe_pieces* pieces = nullptr, bool pdl = false) {
     using PL = pipe_layout<K, HAS_V, SEG>;
     const uint64_t total = m + n;
     const uint64_t out_base = pieces ? pieces->out_base : 0;
@@ -369,7 +369,25 @@ int launch_pipe(const K* a, const uint32_t* av, uint64_t m, const K* b, const ui
     if (g_tune_flags & 512) args.store_evict_first = 0;
     g_last_path = SEG == 3 ? 7 : (SEG == 2 ? 6 : (SEG ? 5 : 3));
     mark_before(s);
-    merge_pipe_kernel<K, HAS_V, SEG><<<grid, PL::kThreads, PL::kSmem, s>>>(args);
+    if (pdl) {
+        // programmatic dependent launch: the grid may be scheduled while the
+        // previous kernel on the stream drains; the kernel's first act is
+        // griddepcontrol.wait (merge_pipe.cuh), so it reads nothing early
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(PL::kThreads);
+        cfg.dynamicSmemBytes = PL::kSmem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, merge_pipe_kernel<K, HAS_V, SEG>, args);
+        if (e != cudaSuccess) return cuda_fail(e, "comerge: pipeline merge launch");
+    } else {
+        merge_pipe_kernel<K, HAS_V, SEG><<<grid, PL::kThreads, PL::kSmem, s>>>(args);
+    }
     mark_after(s);
     return check_launch("comerge: pipeline merge launch");
 }
@@ -1538,6 +1556,11 @@ size_t sort_pairs_ws_bytes(size_t n) {
     return 2 * buf + tail;
 }
 
+// Merge passes launch with programmatic dependent launch (flags bit 24: off,
+// an A/B knob): each pass's grid is scheduled while the previous kernel
+// drains instead of after it.
+inline bool sort_pdl() { return !(g_tune_flags & 16777216); }
+
 // Stable key-value merge sort: as sort_device, the payload moving with its key.
 template <typename K>
 int sort_pairs_device(const K* keys, const uint32_t* vals, size_t n, K* out, uint32_t* out_v,
@@ -1583,7 +1606,8 @@ int sort_pairs_device(const K* keys, const uint32_t* vals, size_t n, K* out, uin
         const uint64_t full = n / (2 * L), rem = n % (2 * L);
         const uint64_t ma = full * L + (rem < L ? rem : L), mb = n - ma;
         if (int rc = launch_pipe<K, true, 2>(ck, cv, ma, ck, cv, mb, dk, dv, nullptr, nullptr,
-                                             div_up(n, 2 * L), tail, tail_bytes, s, L))
+                                             div_up(n, 2 * L), tail, tail_bytes, s, L, nullptr,
+                                             sort_pdl()))
             return rc;
         ck = dk;
         cv = dv;
@@ -1633,7 +1657,8 @@ int sort_device(const K* keys, size_t n, K* out, void* ws, size_t ws_bytes, cuda
         const uint64_t ma = full * L + (rem < L ? rem : L), mb = n - ma;
         const uint64_t nseg = div_up(n, 2 * L);
         if (int rc = launch_pipe<K, false, 2>(cur, nullptr, ma, cur, nullptr, mb, dst, nullptr,
-                                                 nullptr, nullptr, nseg, tail, tail_bytes, s, L))
+                                                 nullptr, nullptr, nseg, tail, tail_bytes, s, L,
+                                                 nullptr, sort_pdl()))
             return rc;
         cur = dst;
     }

@@ -717,6 +717,8 @@ __global__ void __launch_bounds__(pipe_layout<K, HAS_V>::kThreads, pipe_min_bloc
     constexpr bool SEGM = L::kSeg;
 
     extern __shared__ __align__(128) unsigned char smem[];
+    pdl_wait();     // inputs written by a preceding grid (sort passes) are visible
+    pdl_trigger();  // the next pass may be scheduled as SMs free up
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::oBars);
     uint64_t* empty = full + NST;
     uint64_t* staged = empty + NST;  // consumers -> store warp: tile written to the stage

@@ -69,6 +69,16 @@ __device__ __forceinline__ void mbar_wait_sleepy(uint64_t* bar, uint32_t parity,
     } while (!ok);
 }
 
+// Programmatic dependent launch (sort passes launched back to back): a
+// dependent grid's CTAs may start while this grid drains; they wait here
+// until every prerequisite grid has completed and its memory is visible
+// (a no-op for a grid launched without the attribute).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// ... and this grid lets its dependents be scheduled (they still wait above).
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // 1-D TMA bulk copy global -> shared, completing `bytes` on `bar`.
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
                                             uint64_t* bar, uint64_t policy) {

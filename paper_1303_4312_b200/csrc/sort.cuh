@@ -20,6 +20,7 @@
 #include <limits>
 
 #include "corank.cuh"
+#include "ptx.cuh"
 
 namespace comerge_b200 {
 
@@ -62,6 +63,7 @@ __global__ void __launch_bounds__(sort_cfg<K>::NT)
     constexpr int NT = sort_cfg<K>::NT, VT = sort_cfg<K>::VT, R = sort_cfg<K>::R;
     // + slack: a finished list may be read one past its end (never used)
     __shared__ K s[R + R / 32 + 4];
+    pdl_trigger();  // the first merge pass may be scheduled (it waits for this grid)
     const uint64_t base = uint64_t(blockIdx.x) * R;
     const int cnt = n - base < uint64_t(R) ? int(n - base) : R;
     const int t = threadIdx.x;
@@ -127,6 +129,7 @@ __global__ void __launch_bounds__(sort_pairs_cfg<K>::NT)
                   R = sort_pairs_cfg<K>::R;
     __shared__ K s[R + R / 32 + 4];
     __shared__ uint32_t sv[R + R / 32 + 4];
+    pdl_trigger();
     const uint64_t base = uint64_t(blockIdx.x) * R;
     const int cnt = n - base < uint64_t(R) ? int(n - base) : R;
     const int t = threadIdx.x;
