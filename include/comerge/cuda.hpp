@@ -31,6 +31,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <functional>
+#include <new>
 #include <optional>
 #include <ranges>
 #include <span>
@@ -369,6 +370,31 @@ merge_report merge_parallel_synced(const A& a, const B& b, Out&& out, std::size_
                                    std::less<> = {}, merge_options opts = {}) {
     return detail::run_merge_parallel(a, b, out, workers, opts, true);
 }
+
+/// std::allocator replacement handing out page-locked host memory
+/// (comerge_cuda_host_alloc): host-buffer merges of vectors allocated with it
+/// copy at PCIe rate (pageable storage is staged by the driver, ~7x slower on
+/// C4).  std::vector<T, comerge::cuda::pinned_allocator<T>> is a contiguous
+/// range every overload here accepts.
+template <typename T>
+struct pinned_allocator {
+    using value_type = T;
+    pinned_allocator() noexcept = default;
+    template <typename U>
+    pinned_allocator(const pinned_allocator<U>&) noexcept {}
+    T* allocate(std::size_t n) {
+        if (n > std::size_t(-1) / sizeof(T)) throw std::bad_array_new_length();
+        void* p = nullptr;
+        if (comerge_cuda_host_alloc(n * sizeof(T), &p) != COMERGE_OK || (n && !p))
+            throw std::bad_alloc();
+        return static_cast<T*>(p);
+    }
+    void deallocate(T* p, std::size_t) noexcept { comerge_cuda_host_free(p); }
+    template <typename U>
+    friend bool operator==(const pinned_allocator&, const pinned_allocator<U>&) noexcept {
+        return true;
+    }
+};
 
 /// A key-value record (the shape of the reference's tagged<K>, oracle.hpp:22-37).
 template <typename K>

@@ -54,6 +54,14 @@ const char* comerge_cuda_last_error(void);
 /* ABI version (major*10000 + minor*100 + patch). */
 int comerge_cuda_abi_version(void);
 
+/* Page-locked host memory for the host-buffer entry points.  The host
+ * pipeline's copies run at PCIe rate only from page-locked buffers (measured
+ * on C4: 69 ms pinned, 467 ms from pageable std::vector storage, whose copies
+ * the driver stages synchronously); comerge::cuda::pinned_allocator<T> wraps
+ * these for std::vector.  Returns COMERGE_OK or COMERGE_E_CUDA. */
+int comerge_cuda_host_alloc(size_t bytes, void** ptr);
+int comerge_cuda_host_free(void* ptr);
+
 /* Instrumentation (bench / profiling): when set on the calling thread, every
  * comerge_cuda_merge_* call records `before` on its stream right before the
  * dominant merge kernel and `after` right after it, so a caller can time that

@@ -1689,6 +1689,24 @@ void comerge_cuda_set_kernel_events(void* before, void* after) {
 }
 int comerge_cuda_abi_version(void) { return 10000; }
 
+int comerge_cuda_host_alloc(size_t bytes, void** ptr) {
+    if (!ptr) return fail(COMERGE_E_INVALID, "host_alloc: null result pointer");
+    *ptr = nullptr;
+    if (bytes == 0) return COMERGE_OK;
+    const cudaError_t e = cudaHostAlloc(ptr, bytes, cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+        *ptr = nullptr;
+        return cuda_fail(e, "comerge: page-locked host allocation");
+    }
+    return COMERGE_OK;
+}
+
+int comerge_cuda_host_free(void* ptr) {
+    if (!ptr) return COMERGE_OK;
+    const cudaError_t e = cudaFreeHost(ptr);
+    return e == cudaSuccess ? COMERGE_OK : cuda_fail(e, "comerge: page-locked host free");
+}
+
 size_t comerge_cuda_merge_workspace_bytes(size_t m, size_t n, int key_kind, int) {
     return with_slack(key_kind == COMERGE_KEY_U64 ? merge_ws_bytes<uint64_t>(m, n)
                                                   : merge_ws_bytes<uint32_t>(m, n));

@@ -327,8 +327,34 @@ static void records() {
         [&] { cm::merge_parallel(x, y, bad, 2, cm::key_less{}); }, "output length must equal"));
 }
 
+// host-buffer merges of vectors in page-locked memory (pinned_allocator)
+static void pinned_vectors() {
+    std::mt19937_64 rng(5);
+    const std::size_t m = 1500001, n = 1200003;  // >= 2^20: the chunked host pipeline
+    std::vector<std::uint64_t> ka(m), kb(n);
+    for (auto& x : ka) x = rng();
+    for (auto& x : kb) x = rng();
+    std::sort(ka.begin(), ka.end());
+    std::sort(kb.begin(), kb.end());
+    std::vector<std::uint64_t, cm::pinned_allocator<std::uint64_t>> pa(ka.begin(), ka.end()),
+        pb(kb.begin(), kb.end()), out(m + n);
+    cm::merge_parallel(pa, pb, out, 8);
+    std::vector<std::uint64_t> expect(m + n);
+    std::merge(ka.begin(), ka.end(), kb.begin(), kb.end(), expect.begin());
+    CHECK(std::equal(out.begin(), out.end(), expect.begin()));
+    std::vector<tagged<std::int32_t>, cm::pinned_allocator<tagged<std::int32_t>>> ta(m), tb(n),
+        to(m + n);
+    for (std::size_t i = 0; i < m; ++i) ta[i] = {std::int32_t(ka[i] >> 40), origin::from_a, std::uint32_t(i)};
+    for (std::size_t i = 0; i < n; ++i) tb[i] = {std::int32_t(kb[i] >> 40), origin::from_b, std::uint32_t(i)};
+    cm::merge_parallel(ta, tb, to, 8, tagged_key_less{});
+    const auto texpect = naive_merge_by_key(std::vector<tagged<std::int32_t>>(ta.begin(), ta.end()),
+                                            std::vector<tagged<std::int32_t>>(tb.begin(), tb.end()));
+    CHECK(std::equal(to.begin(), to.end(), texpect.begin()));
+}
+
 int main() {
     kats();
+    pinned_vectors();
     comparisons();
     records();
     sweep<std::int32_t>(1);
