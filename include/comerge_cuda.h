@@ -95,11 +95,18 @@ void comerge_cuda_set_host_mode(int mode);
  * to device_buffer[12*4096 + 4c ..] and scheduler tail counters to
  * device_buffer[16*4096 + 4c ..].  NULL disables. */
 void comerge_cuda_set_trace(unsigned long long* device_buffer);
-/* Tuning knobs of the tile pipeline (benchmarking only; 0 = default): the
- * statically assigned share of tiles in percent (default 70; the rest is the
- * dynamic tail), experiment flags (bit 0: co-rank the start-up boundaries one
- * after the other), and the claim look-ahead (queued tiles below which the next
- * tail tile is claimed, default 2). */
+/* Tuning knobs of the tile pipeline (benchmarking only, per host thread;
+ * 0 = default): the statically assigned share of tiles in percent (default
+ * 70; the rest is the dynamic tail), experiment flags, and the claim
+ * look-ahead (queued tiles below which the next tail tile is claimed,
+ * default 2).  Flags: bit 0 co-rank the start-up boundaries one after the
+ * other; bits 2-3 scheduler pass cap (1: 8, 2: 16, 3: 32); bits 4-7
+ * scheduler look-ahead / 4; bit 8 / 9 output stores evict-first on / off;
+ * bit 10 no concurrent start-up searches for segmented batches; bit 12 no L2
+ * pull of small inputs; bit 13 no L2 pull of segment offsets; bit 14 the
+ * small-merge kernel's searches to the end (no superset windows); bits 15-17
+ * dynamic-tail anchor unit (1-7, default 4); bit 24 merge passes without
+ * programmatic dependent launch. */
 void comerge_cuda_set_tuning(int static_pct, int flags, int lookahead);
 
 /* ------------------------------------------------------------ workspace */
