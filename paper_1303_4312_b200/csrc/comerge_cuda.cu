@@ -1222,6 +1222,26 @@ int merge_segmented_host_pipeline(const K* a, const uint64_t* a_off, uint64_t m,
     };
     h2d_copy(dAoff, a_off, (nseg + 1) * 8);
     h2d_copy(dBoff, b_off, (nseg + 1) * 8);
+    // pageable key arrays through page-locked slots, as merge_host_pipeline
+    const bool pg_a = m && !is_pinned_host(a), pg_b = n && !is_pinned_host(b);
+    const bool pg_o = !is_pinned_host(out);
+    const size_t sin = (chunk + 4 * G) * sizeof(K) + 2 * 256, sout = round256(chunk * sizeof(K));
+    unsigned char* pst = nullptr;
+    if (pg_a || pg_b || pg_o) {
+        pst = static_cast<unsigned char*>(pinned_stage(3 * round256(sin + sout)));
+        if (!pst) rc = fail(COMERGE_E_CUDA, "comerge: page-locked staging allocation");
+    }
+    auto slot_in = [&](int sl) { return pst + size_t(sl) * round256(sin + sout); };
+    auto copy_out = [&](uint64_t cc) {
+        if (!pg_o) return;
+        const cudaError_t ce = cudaEventSynchronize(hs.out_done[cc % 3]);
+        if (ce != cudaSuccess) {
+            if (!rc) rc = cuda_fail(ce, "comerge: host pipeline device->host copy");
+            return;
+        }
+        copy_pool::get().copy(out + cuts[cc], slot_in(int(cc % 3)) + sin,
+                              (cuts[cc + 1] - cuts[cc]) * sizeof(K));
+    };
     std::vector<uint64_t> js(nchunks + 1), ss(nchunks + 1);
     js[0] = 0;
     ss[0] = 0;
@@ -1243,8 +1263,29 @@ int merge_segmented_host_pipeline(const K* a, const uint64_t* a_off, uint64_t m,
         const uint64_t sa = j0 / G * G, ea = std::min(m, div_up(j1, G) * G);
         const uint64_t sb = k0 / G * G, eb = std::min(n, div_up(k1, G) * G);
         if (c >= 3) cudaStreamWaitEvent(hs.h2d, hs.out_done[sl], 0);
-        h2d_copy(dA, a + sa, (ea - sa) * sizeof(K));
-        h2d_copy(dB, b + sb, (eb - sb) * sizeof(K));
+        const void* srcA = a + sa;
+        const void* srcB = b + sb;
+        if (pg_a || pg_b) {
+            if (c >= 3) {  // the slot's previous chunk has been copied to the device
+                const cudaError_t ce = cudaEventSynchronize(hs.in_done[sl]);
+                if (ce != cudaSuccess) {
+                    rc = cuda_fail(ce, "comerge: host pipeline host->device copy");
+                    break;
+                }
+            }
+            unsigned char* in = slot_in(sl);
+            if (pg_a && ea > sa) {
+                copy_pool::get().copy(in, srcA, (ea - sa) * sizeof(K));
+                srcA = in;
+            }
+            if (pg_b && eb > sb) {
+                unsigned char* inb = in + round256((ea - sa) * sizeof(K));
+                copy_pool::get().copy(inb, srcB, (eb - sb) * sizeof(K));
+                srcB = inb;
+            }
+        }
+        h2d_copy(dA, srcA, (ea - sa) * sizeof(K));
+        h2d_copy(dB, srcB, (eb - sb) * sizeof(K));
         *h2d += (i1 - i0) * sizeof(K);
         cudaEventRecord(hs.in_done[sl], hs.h2d);
         if (rc) break;
@@ -1269,11 +1310,14 @@ int merge_segmented_host_pipeline(const K* a, const uint64_t* a_off, uint64_t m,
         cudaEventRecord(hs.merged[sl], hs.comp);
         cudaStreamWaitEvent(hs.d2h, hs.merged[sl], 0);
         const uint64_t h = std::min(i1, i0 + (j1 - j0 + G / 2) / G * G) - i0;
-        d2h_copy(out + i0, dO, h * sizeof(K));
-        d2h_copy(out + i0 + h, dO + h, (i1 - i0 - h) * sizeof(K));
+        K* dstO = pg_o ? reinterpret_cast<K*>(slot_in(sl) + sin) : out + i0;
+        d2h_copy(dstO, dO, h * sizeof(K));
+        d2h_copy(dstO + h, dO + h, (i1 - i0 - h) * sizeof(K));
         *d2h += (i1 - i0) * sizeof(K);
         cudaEventRecord(hs.out_done[sl], hs.d2h);
+        if (c >= 1 && !rc) copy_out(c - 1);
     }
+    if (!rc && nchunks) copy_out(nchunks - 1);
     cudaEventRecord(hs.t1, hs.comp);
     cudaEventRecord(hs.in_done[0], hs.d2h);
     cudaStreamWaitEvent(hs.comp, hs.in_done[0], 0);

@@ -22,6 +22,8 @@ for cfg in sys.argv[1:]:
     for kind in ("pageable", "pinned"):
         h = {k: (v.cpu().numpy() if kind == "pageable" else v.cpu().pin_memory())
              for k, v in inp.items()}
+        if "a_off" in h and kind == "pinned":  # offsets: host arrays either way
+            h["a_off"], h["b_off"] = inp["a_off"].cpu().numpy(), inp["b_off"].cpu().numpy()
         total = len(h["a"]) + len(h["b"])
         mk = (lambda n, dt: np.empty(n, dt)) if kind == "pageable" else \
             (lambda n, dt: torch.empty(n, dtype={np.int32: torch.int32, np.uint64: torch.uint64,
@@ -29,7 +31,12 @@ for cfg in sys.argv[1:]:
         kdt = np.uint64 if c["dtype"] == "uint64" else np.int32
         ok = mk(total, kdt)
         rep = N.MergeReport()
-        if c["kind"] == "pairs":
+        if c["kind"] == "segmented":
+            fn = getattr(N.lib, f"comerge_merge_segmented_host_{suf}")
+            nseg = len(h["a_off"]) - 1
+            call = lambda: N.check(fn(p(h["a"]), p(h["a_off"]), len(h["a"]), p(h["b"]),  # noqa: E731
+                                      p(h["b_off"]), len(h["b"]), nseg, p(ok), total, C.byref(rep)))
+        elif c["kind"] == "pairs":
             ov = mk(total, np.uint32)
             fn = getattr(N.lib, f"comerge_merge_parallel_pairs_{suf}")
             call = lambda: N.check(fn(p(h["a"]), p(h["av"]), len(h["a"]), p(h["b"]), p(h["bv"]),  # noqa: E731
