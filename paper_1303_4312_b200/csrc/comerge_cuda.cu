@@ -851,8 +851,10 @@ class copy_pool {
 };
 
 // Page-locked staging for pageable host buffers (per host thread and device,
-// grow-only: pinning costs ~80 ms per GB, once).
+// grow-only: pinning costs ~80 ms per GB, once; at most 4 GB -- beyond it,
+// or when pinning fails, the caller falls back to the driver's staging).
 void* pinned_stage(size_t bytes) {
+    if (bytes > (size_t(4) << 30)) return nullptr;
     struct cache {
         void* p = nullptr;
         size_t bytes = 0;
@@ -972,22 +974,20 @@ int merge_host_pipeline(const K* a, const uint32_t* av, uint64_t m, const K* b,
     // pageable arrays go through three page-locked slots (copy_pool): per
     // slot the input windows [A | B | A vals | B vals], then the chunk's
     // output [keys | vals]
-    const bool pg_a = m && !is_pinned_host(a), pg_b = n && !is_pinned_host(b);
-    const bool pg_av = HAS_V && m && !is_pinned_host(av), pg_bv = HAS_V && n && !is_pinned_host(bv);
-    const bool pg_o = !is_pinned_host(out), pg_ov = HAS_V && !is_pinned_host(outv);
-    const bool pg_out = pg_o || pg_ov;
+    bool pg_a = m && !is_pinned_host(a), pg_b = n && !is_pinned_host(b);
+    bool pg_av = HAS_V && m && !is_pinned_host(av), pg_bv = HAS_V && n && !is_pinned_host(bv);
+    bool pg_o = !is_pinned_host(out), pg_ov = HAS_V && !is_pinned_host(outv);
     const size_t sin = (chunk + 4 * G) * (sizeof(K) + (HAS_V ? 4 : 0)) + 4 * 256;
     const size_t sok = round256(chunk * sizeof(K));
     const size_t sout = sok + (HAS_V ? round256(chunk * 4) : 0);
     unsigned char* pst = nullptr;
-    if (pg_a || pg_b || pg_av || pg_bv || pg_out) {
+    if (pg_a || pg_b || pg_av || pg_bv || pg_o || pg_ov) {
         pst = static_cast<unsigned char*>(pinned_stage(3 * round256(sin + sout)));
-        if (!pst) {
-            cudaFreeAsync(buf, hs.comp);
-            cudaStreamSynchronize(hs.comp);
-            return fail(COMERGE_E_CUDA, "comerge: page-locked staging allocation");
-        }
+        // no page-locked memory to spare: the driver's own (synchronous)
+        // staging of pageable copies instead
+        if (!pst) pg_a = pg_b = pg_av = pg_bv = pg_o = pg_ov = false;
     }
+    const bool pg_out = pg_o || pg_ov;
     auto slot_in = [&](int sl) { return pst + size_t(sl) * round256(sin + sout); };
     auto copy_out = [&](uint64_t cc) {  // chunk cc's staged output -> the caller's arrays
         if (!pg_out) return;
@@ -1223,13 +1223,13 @@ int merge_segmented_host_pipeline(const K* a, const uint64_t* a_off, uint64_t m,
     h2d_copy(dAoff, a_off, (nseg + 1) * 8);
     h2d_copy(dBoff, b_off, (nseg + 1) * 8);
     // pageable key arrays through page-locked slots, as merge_host_pipeline
-    const bool pg_a = m && !is_pinned_host(a), pg_b = n && !is_pinned_host(b);
-    const bool pg_o = !is_pinned_host(out);
+    bool pg_a = m && !is_pinned_host(a), pg_b = n && !is_pinned_host(b);
+    bool pg_o = !is_pinned_host(out);
     const size_t sin = (chunk + 4 * G) * sizeof(K) + 2 * 256, sout = round256(chunk * sizeof(K));
     unsigned char* pst = nullptr;
     if (pg_a || pg_b || pg_o) {
         pst = static_cast<unsigned char*>(pinned_stage(3 * round256(sin + sout)));
-        if (!pst) rc = fail(COMERGE_E_CUDA, "comerge: page-locked staging allocation");
+        if (!pst) pg_a = pg_b = pg_o = false;  // the driver's own staging instead
     }
     auto slot_in = [&](int sl) { return pst + size_t(sl) * round256(sin + sout); };
     auto copy_out = [&](uint64_t cc) {
