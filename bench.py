@@ -843,7 +843,16 @@ def run_split(args, dist, rank, world, device, peak, flush):
     pbv = piece(full["bv"], n) if "bv" in full else None
     del full
     torch.cuda.empty_cache()
-    dm = DistributedMerge(pa, pb, a_vals=pav, b_vals=pbv)
+    try:  # CUDA IPC / peer access between the ranks' GPUs
+        dm, err = DistributedMerge(pa, pb, a_vals=pav, b_vals=pbv), None
+    except Exception as e:  # noqa: BLE001 -- every rank must learn of any rank's failure
+        dm, err = None, repr(e)
+    if allreduce_time(dist, [0.0 if err is None else 1.0], device)[0] > 0:
+        if dm is not None:
+            dm.close()
+        print(f"bench.py rank {rank}: split setup failed ({err or 'on a peer rank'}); "
+              "falling back to replicas", file=sys.stderr, flush=True)
+        return False
 
     class Ctx:
         def barrier(self):
@@ -906,11 +915,13 @@ def main():
     torch.cuda.set_device(device)
     peak, peak_src = peak_hbm()
     flush = L2Flush(device)
+    split_failed = False
     if world > 1 and not args.replicas:
-        run_split(args, dist, rank, world, device, peak, flush)
-        dist.barrier()
-        dist.destroy_process_group()
-        return
+        if run_split(args, dist, rank, world, device, peak, flush) is not False:
+            dist.barrier()
+            dist.destroy_process_group()
+            return
+        split_failed = True
 
     class Ctx:
         def barrier(self):
@@ -974,6 +985,8 @@ def main():
             configs=per_config, sorts=sorts)
         if world > 1:
             line["scaling_note"] = "replicas: an independent instance per GPU (seed + rank)"
+            if split_failed:
+                line["scaling_note"] += "; the split of one merge could not set up peer access"
             if shared_devices(dist):
                 line["note"] = (f"{world} ranks on {torch.cuda.device_count()} GPU(s): a functional "
                                 "run; ranks time-slice the device, job time = sum of ranks")
