@@ -500,6 +500,18 @@ def test_host_buffers_pipelined(cuda, port):
         ok, ov = np.empty_like(ek), np.empty_like(ev)
         P().merge_pairs(a, av, b, bv, ok, ov)
         assert np.array_equal(ok, ek) and np.array_equal(ov, ev)
+        # mixed page-locked and pageable arrays: only the pageable ones go
+        # through the page-locked staging slots
+        pav = torch.from_numpy(av).pin_memory()
+        pbv = torch.from_numpy(bv).pin_memory()
+        pov = torch.zeros(m + n, dtype=torch.uint32).pin_memory()
+        ok2 = np.zeros_like(ek)
+        P().merge_pairs(pa.numpy(), av, b, pbv.numpy(), ok2, pov.numpy())
+        assert np.array_equal(ok2, ek) and np.array_equal(pov.numpy(), ev)
+        po.zero_()
+        ov2 = np.zeros_like(ev)
+        P().merge_pairs(a, pav.numpy(), pb.numpy(), bv, po.numpy(), ov2)
+        assert np.array_equal(po.numpy(), ek) and np.array_equal(ov2, ev)
 
 
 def test_host_pipeline_aligned_windows(cuda, port):
