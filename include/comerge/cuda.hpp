@@ -163,65 +163,6 @@ concept record_range = std::ranges::contiguous_range<R> && std::ranges::sized_ra
 template <typename R>
 using elem_of = std::remove_cv_t<std::ranges::range_value_t<R>>;
 
-template <typename K, std::size_t S = sizeof(K) == 8 ? 16 : 8>
-struct rec_abi;
-// 12-byte records: the reference's tagged<int32_t> / tagged<uint32_t> layout
-template <>
-struct rec_abi<std::int32_t, 12> {
-    static int merge(const void* a, std::size_t m, const void* b, std::size_t n, void* out,
-                     std::size_t len, std::size_t w, int synced, comerge_merge_report* rep,
-                     std::uint64_t* bs, std::uint32_t* its) {
-        return comerge_merge_parallel_records12_i32(static_cast<const comerge_rec12_i32*>(a), m,
-                                                    static_cast<const comerge_rec12_i32*>(b), n,
-                                                    static_cast<comerge_rec12_i32*>(out), len, w,
-                                                    synced, rep, bs, its);
-    }
-};
-template <>
-struct rec_abi<std::uint32_t, 12> {
-    static int merge(const void* a, std::size_t m, const void* b, std::size_t n, void* out,
-                     std::size_t len, std::size_t w, int synced, comerge_merge_report* rep,
-                     std::uint64_t* bs, std::uint32_t* its) {
-        return comerge_merge_parallel_records12_u32(static_cast<const comerge_rec12_u32*>(a), m,
-                                                    static_cast<const comerge_rec12_u32*>(b), n,
-                                                    static_cast<comerge_rec12_u32*>(out), len, w,
-                                                    synced, rep, bs, its);
-    }
-};
-template <>
-struct rec_abi<std::int32_t> {
-    static int merge(const void* a, std::size_t m, const void* b, std::size_t n, void* out,
-                     std::size_t len, std::size_t w, int synced, comerge_merge_report* rep,
-                     std::uint64_t* bs, std::uint32_t* its) {
-        return comerge_merge_parallel_records_i32(static_cast<const comerge_rec_i32*>(a), m,
-                                                  static_cast<const comerge_rec_i32*>(b), n,
-                                                  static_cast<comerge_rec_i32*>(out), len, w,
-                                                  synced, rep, bs, its);
-    }
-};
-template <>
-struct rec_abi<std::uint32_t> {
-    static int merge(const void* a, std::size_t m, const void* b, std::size_t n, void* out,
-                     std::size_t len, std::size_t w, int synced, comerge_merge_report* rep,
-                     std::uint64_t* bs, std::uint32_t* its) {
-        return comerge_merge_parallel_records_u32(static_cast<const comerge_rec_u32*>(a), m,
-                                                  static_cast<const comerge_rec_u32*>(b), n,
-                                                  static_cast<comerge_rec_u32*>(out), len, w,
-                                                  synced, rep, bs, its);
-    }
-};
-template <>
-struct rec_abi<std::uint64_t> {
-    static int merge(const void* a, std::size_t m, const void* b, std::size_t n, void* out,
-                     std::size_t len, std::size_t w, int synced, comerge_merge_report* rep,
-                     std::uint64_t* bs, std::uint32_t* its) {
-        return comerge_merge_parallel_records_u64(static_cast<const comerge_rec_u64*>(a), m,
-                                                  static_cast<const comerge_rec_u64*>(b), n,
-                                                  static_cast<comerge_rec_u64*>(out), len, w,
-                                                  synced, rep, bs, its);
-    }
-};
-
 template <typename K>
 struct abi;
 
@@ -422,20 +363,52 @@ template <>
 struct is_key_less<key_less> : std::true_type {};
 
 namespace detail {
+// generic record entry points by key type (record size passed at run time)
+template <typename K>
+struct rec_generic;
+#define COMERGE_CUDA_REC_GENERIC(K, SUF)                                                        \
+    template <>                                                                                 \
+    struct rec_generic<K> {                                                                     \
+        static int merge_ex(const void* a, std::size_t m, const void* b, std::size_t n,        \
+                            void* out, std::size_t len, std::size_t rb, std::size_t w,          \
+                            const comerge_merge_options* o, comerge_merge_report* rep,         \
+                            std::uint64_t* bs, std::uint32_t* its, std::uint64_t* cmp) {        \
+            return comerge_merge_parallel_records_ex_##SUF(a, m, b, n, out, len, rb, w, o, rep, \
+                                                           bs, its, cmp);                       \
+        }                                                                                       \
+        static int co_rank(std::uint64_t t, const void* a, std::size_t m, const void* b,       \
+                           std::size_t n, std::size_t rb, std::uint64_t* j, std::uint64_t* k,   \
+                           std::uint32_t* it, std::uint32_t* cmp) {                             \
+            return comerge_co_rank_records_##SUF(t, a, m, b, n, rb, j, k, it, cmp);             \
+        }                                                                                       \
+        static int plan(const void* a, std::size_t m, const void* b, std::size_t n,            \
+                        std::size_t rb, std::size_t w, std::uint64_t* blocks) {                 \
+            return comerge_plan_records_##SUF(a, m, b, n, rb, w, blocks);                       \
+        }                                                                                       \
+    };
+COMERGE_CUDA_REC_GENERIC(std::int32_t, i32)
+COMERGE_CUDA_REC_GENERIC(std::uint32_t, u32)
+COMERGE_CUDA_REC_GENERIC(std::uint64_t, u64)
+#undef COMERGE_CUDA_REC_GENERIC
+
 template <typename A, typename B, typename Out>
 merge_report run_merge_records(const A& a, const B& b, Out& out, std::size_t workers,
-                               bool synced) {
+                               bool synced, merge_options opts = {}) {
     using T = elem_of<A>;
     using K = std::remove_cv_t<decltype(T::key)>;
     comerge_merge_report rep{};
+    const comerge_merge_options o{synced ? 1 : 0, opts.count_comparisons ? 1 : 0};
     std::vector<std::uint64_t> bs(workers ? workers : 1);
     std::vector<std::uint32_t> its(2 * (workers ? workers : 1));
-    check(rec_abi<K, sizeof(T)>::merge(std::ranges::data(a), std::ranges::size(a), std::ranges::data(b),
-                            std::ranges::size(b), std::ranges::data(out), std::ranges::size(out),
-                            workers, synced ? 1 : 0, &rep, bs.data(), its.data()));
+    std::uint64_t cmp = 0;
+    check(rec_generic<K>::merge_ex(std::ranges::data(a), std::ranges::size(a),
+                                   std::ranges::data(b), std::ranges::size(b),
+                                   std::ranges::data(out), std::ranges::size(out), sizeof(T),
+                                   workers, &o, &rep, bs.data(), its.data(), &cmp));
     merge_report r = to_report(rep);
     r.block_sizes.assign(bs.begin(), bs.begin() + workers);
-    r.corank_iterations.assign(its.begin(), its.begin() + 2 * workers);
+    r.corank_iterations.assign(its.begin(), its.begin() + (synced ? workers : 2 * workers));
+    if (opts.count_comparisons) r.comparisons = cmp;
     return r;
 }
 }  // namespace detail
@@ -449,8 +422,47 @@ template <detail::record_range A, detail::record_range B, std::ranges::contiguou
              std::same_as<detail::elem_of<A>, std::ranges::range_value_t<Out>> &&
              is_key_less<Less>::value
 merge_report merge_parallel(const A& a, const B& b, Out&& out, std::size_t workers, Less,
-                            merge_options = {}) {
-    return detail::run_merge_records(a, b, out, workers, false);
+                            merge_options opts = {}) {
+    return detail::run_merge_records(a, b, out, workers, false, opts);
+}
+
+/// comerge::merge_parallel_synced over records (parallel.hpp:323-336).
+template <detail::record_range A, detail::record_range B, std::ranges::contiguous_range Out,
+          typename Less>
+    requires std::same_as<detail::elem_of<A>, detail::elem_of<B>> &&
+             std::same_as<detail::elem_of<A>, std::ranges::range_value_t<Out>> &&
+             is_key_less<Less>::value
+merge_report merge_parallel_synced(const A& a, const B& b, Out&& out, std::size_t workers, Less,
+                                   merge_options opts = {}) {
+    return detail::run_merge_records(a, b, out, workers, true, opts);
+}
+
+/// comerge::co_rank over records with a key-only comparator (corank.hpp:128-133;
+/// the comparator known-answer test of corank_test.cpp:205-214).
+template <detail::record_range A, detail::record_range B, typename Less>
+    requires std::same_as<detail::elem_of<A>, detail::elem_of<B>> && is_key_less<Less>::value
+co_ranks co_rank(rank_t target, const A& a, const B& b, Less, co_rank_stats* stats = nullptr) {
+    using T = detail::elem_of<A>;
+    using K = std::remove_cv_t<decltype(T::key)>;
+    std::uint64_t j = 0, k = 0;
+    std::uint32_t it = 0, cmp = 0;
+    detail::check(detail::rec_generic<K>::co_rank(target, std::ranges::data(a),
+                                                  std::ranges::size(a), std::ranges::data(b),
+                                                  std::ranges::size(b), sizeof(T), &j, &k, &it,
+                                                  &cmp));
+    if (stats) *stats = {it, cmp};
+    return {static_cast<std::size_t>(j), static_cast<std::size_t>(k)};
+}
+
+/// comerge::co_rank_counted over records (corank.hpp:138-147).
+template <detail::record_range A, detail::record_range B, typename Less>
+    requires std::same_as<detail::elem_of<A>, detail::elem_of<B>> && is_key_less<Less>::value
+co_ranks co_rank_counted(rank_t target, const A& a, const B& b, Less less,
+                         comparison_counter& counter) {
+    co_rank_stats st;
+    const co_ranks r = co_rank(target, a, b, less, &st);
+    counter.count += st.comparisons;
+    return r;
 }
 
 /// comerge::stable_merge over records (merge.hpp:52-68).
@@ -501,6 +513,29 @@ merge_plan plan(const A& a, const B& b, std::size_t workers, std::less<> = {}) {
     detail::check(detail::abi<K>::plan(std::ranges::data(a), std::ranges::size(a),
                                        std::ranges::data(b), std::ranges::size(b), workers,
                                        raw.data()));
+    merge_plan p;
+    p.workers = workers;
+    for (std::size_t r = 0; r < workers; ++r) {
+        const std::uint64_t* o = raw.data() + 7 * r;
+        p.blocks.push_back({static_cast<std::size_t>(o[0]), static_cast<rank_t>(o[1]),
+                            static_cast<rank_t>(o[2]), static_cast<std::size_t>(o[3]),
+                            static_cast<std::size_t>(o[4]), static_cast<std::size_t>(o[5]),
+                            static_cast<std::size_t>(o[6])});
+    }
+    return p;
+}
+
+/// comerge::plan over records with a key-only comparator (parallel.hpp:94-115).
+template <detail::record_range A, detail::record_range B, typename Less>
+    requires std::same_as<detail::elem_of<A>, detail::elem_of<B>> && is_key_less<Less>::value
+merge_plan plan(const A& a, const B& b, std::size_t workers, Less) {
+    using T = detail::elem_of<A>;
+    using K = std::remove_cv_t<decltype(T::key)>;
+    if (workers == 0) throw std::invalid_argument("plan: worker count must be positive");
+    std::vector<std::uint64_t> raw(7 * workers);
+    detail::check(detail::rec_generic<K>::plan(std::ranges::data(a), std::ranges::size(a),
+                                               std::ranges::data(b), std::ranges::size(b),
+                                               sizeof(T), workers, raw.data()));
     merge_plan p;
     p.workers = workers;
     for (std::size_t r = 0; r < workers; ++r) {

@@ -455,6 +455,65 @@ int comerge_co_rank_u64(uint64_t target, const uint64_t* a, size_t m, const uint
                         size_t n, uint64_t* j, uint64_t* k, uint32_t* iterations,
                         uint32_t* comparisons);
 
+/* The same templates instantiated with a record type and a key-only less
+ * (the reference's tagged<K> / tagged_key_less, oracle.hpp:22-37; the
+ * comparator known-answer test of corank_test.cpp:205-214): arrays of
+ * `record_bytes`-byte records with the key at offset 0 -- 8 or 12 bytes for
+ * _i32 / _u32, 16 for _u64 (COMERGE_E_INVALID otherwise) -- host or device
+ * pointers.  Only keys are compared, so j, k, iterations, comparisons and the
+ * plan equal those of the records' key arrays.
+ *   comerge_co_rank_records_*         co_rank / co_rank_counted  corank.hpp:128-147
+ *   comerge_plan_records_*            plan                       parallel.hpp:94-115
+ *   comerge_cuda_co_rank_batch_records_*  batched, device arrays, async
+ *   comerge_merge_parallel_records_ex_*   merge_parallel / _synced with
+ *       merge_options (count_comparisons) and every report field,
+ *       parallel.hpp:304-336 */
+int comerge_co_rank_records_i32(uint64_t target, const void* a, size_t m, const void* b,
+                                size_t n, size_t record_bytes, uint64_t* j, uint64_t* k,
+                                uint32_t* iterations, uint32_t* comparisons);
+int comerge_plan_records_i32(const void* a, size_t m, const void* b, size_t n,
+                             size_t record_bytes, size_t workers, uint64_t* blocks);
+int comerge_cuda_co_rank_batch_records_i32(const uint64_t* ranks, size_t count, const void* a,
+                                           size_t m, const void* b, size_t n,
+                                           size_t record_bytes, uint64_t* out_j,
+                                           uint32_t* out_iterations, uint32_t* out_comparisons,
+                                           comerge_stream_t stream);
+int comerge_merge_parallel_records_ex_i32(const void* a, size_t m, const void* b, size_t n,
+                                          void* out, size_t out_len, size_t record_bytes,
+                                          size_t workers, const comerge_merge_options* opts,
+                                          comerge_merge_report* report, uint64_t* block_sizes,
+                                          uint32_t* corank_iterations, uint64_t* comparisons);
+int comerge_co_rank_records_u32(uint64_t target, const void* a, size_t m, const void* b,
+                                size_t n, size_t record_bytes, uint64_t* j, uint64_t* k,
+                                uint32_t* iterations, uint32_t* comparisons);
+int comerge_plan_records_u32(const void* a, size_t m, const void* b, size_t n,
+                             size_t record_bytes, size_t workers, uint64_t* blocks);
+int comerge_cuda_co_rank_batch_records_u32(const uint64_t* ranks, size_t count, const void* a,
+                                           size_t m, const void* b, size_t n,
+                                           size_t record_bytes, uint64_t* out_j,
+                                           uint32_t* out_iterations, uint32_t* out_comparisons,
+                                           comerge_stream_t stream);
+int comerge_merge_parallel_records_ex_u32(const void* a, size_t m, const void* b, size_t n,
+                                          void* out, size_t out_len, size_t record_bytes,
+                                          size_t workers, const comerge_merge_options* opts,
+                                          comerge_merge_report* report, uint64_t* block_sizes,
+                                          uint32_t* corank_iterations, uint64_t* comparisons);
+int comerge_co_rank_records_u64(uint64_t target, const void* a, size_t m, const void* b,
+                                size_t n, size_t record_bytes, uint64_t* j, uint64_t* k,
+                                uint32_t* iterations, uint32_t* comparisons);
+int comerge_plan_records_u64(const void* a, size_t m, const void* b, size_t n,
+                             size_t record_bytes, size_t workers, uint64_t* blocks);
+int comerge_cuda_co_rank_batch_records_u64(const uint64_t* ranks, size_t count, const void* a,
+                                           size_t m, const void* b, size_t n,
+                                           size_t record_bytes, uint64_t* out_j,
+                                           uint32_t* out_iterations, uint32_t* out_comparisons,
+                                           comerge_stream_t stream);
+int comerge_merge_parallel_records_ex_u64(const void* a, size_t m, const void* b, size_t n,
+                                          void* out, size_t out_len, size_t record_bytes,
+                                          size_t workers, const comerge_merge_options* opts,
+                                          comerge_merge_report* report, uint64_t* block_sizes,
+                                          uint32_t* corank_iterations, uint64_t* comparisons);
+
 /* comerge::partition_output(total, workers, r) (parallel.hpp:60-67). */
 int comerge_partition_output(uint64_t total, uint64_t workers, uint64_t r, uint64_t* out);
 

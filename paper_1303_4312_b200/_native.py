@@ -78,6 +78,16 @@ def _load():
                                                                       _sz, _p]
         getattr(lib, f"comerge_merge_parallel_records_{suf}").argtypes = [
             _p, _sz, _p, _sz, _p, _sz, _sz, _i, C.POINTER(MergeReport), _p, _p]
+        # records by run-time size: co_rank / plan / batched co-rank / full report
+        getattr(lib, f"comerge_co_rank_records_{suf}").argtypes = [
+            _u64, _p, _sz, _p, _sz, _sz, C.POINTER(_u64), C.POINTER(_u64),
+            C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
+        getattr(lib, f"comerge_plan_records_{suf}").argtypes = [_p, _sz, _p, _sz, _sz, _sz, _p]
+        getattr(lib, f"comerge_cuda_co_rank_batch_records_{suf}").argtypes = [
+            _p, _sz, _p, _sz, _p, _sz, _sz, _p, _p, _p, _p]
+        getattr(lib, f"comerge_merge_parallel_records_ex_{suf}").argtypes = [
+            _p, _sz, _p, _sz, _p, _sz, _sz, _sz, C.POINTER(MergeOptions),
+            C.POINTER(MergeReport), _p, _p, C.POINTER(_u64)]
     lib.comerge_cuda_records12_workspace_bytes.argtypes = [_sz, _sz]
     lib.comerge_cuda_records12_workspace_bytes.restype = _sz
     for suf in ("i32", "u32"):

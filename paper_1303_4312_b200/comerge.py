@@ -470,6 +470,101 @@ def merge_records(a, b, out=None, key_dtype=None, workers: int = 1, workspace=No
                             tiles=rep.tiles)
 
 
+def _rec_info(x, key_dtype, record_bytes):
+    """(suffix, record size, record count) of a record array: a numpy
+    structured array of record_dtype(), or any buffer of whole records with
+    `key_dtype` (and `record_bytes` when not the default size) given."""
+    if not _is_torch(x) and x.dtype.names:
+        kd, size = x.dtype["key"], record_bytes or x.dtype.itemsize
+        if x.dtype.itemsize != size:
+            raise TypeError(f"records: the array holds {x.dtype.itemsize}-byte records, not {size}")
+    else:
+        if key_dtype is None:
+            raise TypeError("records: key_dtype is required for unstructured buffers")
+        kd = key_dtype
+        size = record_bytes or _REC_SIZE[_REC_SUFFIX[_dtype_name_of(kd)]]
+    return _REC_SUFFIX[_dtype_name_of(kd)], size, _rec_count(x, size)
+
+
+def co_rank_records(target: int, a, b, key_dtype=None, record_bytes=None,
+                    stats: Optional[CoRankStats] = None):
+    """comerge::co_rank over records with a key-only less (corank.hpp:128-133
+    instantiated as in corank_test.cpp:205-214): the split, iterations and
+    comparisons of the records' key arrays.  Host or device buffers."""
+    suf, size, m = _rec_info(a, key_dtype, record_bytes)
+    n = _rec_info(b, key_dtype, record_bytes)[2]
+    if target < 0:
+        raise IndexError("co_rank: rank out of range (exceeds m+n)")
+    j, k, it, cmp = C.c_uint64(), C.c_uint64(), C.c_uint32(), C.c_uint32()
+    with _on(a):
+        N.check(getattr(N.lib, f"comerge_co_rank_records_{suf}")(
+            int(target), _ptr(a), m, _ptr(b), n, size, C.byref(j), C.byref(k), C.byref(it),
+            C.byref(cmp)))
+    if stats is not None:
+        stats.iterations, stats.comparisons = it.value, cmp.value
+    return (j.value, k.value)
+
+
+def co_rank_batch_records(ranks, a, b, key_dtype, record_bytes=None, with_stats: bool = False):
+    """Device batch of co-ranks over record arrays (see co_rank_batch)."""
+    suf, size, m = _rec_info(a, key_dtype, record_bytes)
+    n = _rec_info(b, key_dtype, record_bytes)[2]
+    q = int(ranks.numel())
+    j = torch.empty(q, dtype=torch.uint64, device=a.device)
+    it = torch.empty(q, dtype=torch.uint32, device=a.device) if with_stats else None
+    cmp = torch.empty(q, dtype=torch.uint32, device=a.device) if with_stats else None
+    with _on(a):
+        N.check(getattr(N.lib, f"comerge_cuda_co_rank_batch_records_{suf}")(
+            _ptr(ranks), q, _ptr(a), m, _ptr(b), n, size, _ptr(j), _ptr(it), _ptr(cmp),
+            _stream(a)))
+    return (j, it, cmp) if with_stats else j
+
+
+def plan_records(a, b, workers: int, key_dtype=None, record_bytes=None):
+    """comerge::plan over records with a key-only less (parallel.hpp:94-115)."""
+    if workers <= 0:
+        raise ValueError("plan: worker count must be positive")
+    suf, size, m = _rec_info(a, key_dtype, record_bytes)
+    n = _rec_info(b, key_dtype, record_bytes)[2]
+    raw = np.zeros(7 * workers, np.uint64)
+    if _is_torch(a) and a.is_cuda:
+        torch.cuda.current_stream(a.device).synchronize()
+    with _on(a):
+        N.check(getattr(N.lib, f"comerge_plan_records_{suf}")(
+            _ptr(a), m, _ptr(b), n, size, workers, C.c_void_p(raw.ctypes.data)))
+    return [BlockAssignment(*(int(x) for x in raw[7 * r:7 * r + 7])) for r in range(workers)]
+
+
+def merge_parallel_records(a, b, out, workers: int, key_dtype=None, record_bytes=None,
+                           opts: Optional[MergeOptions] = None, synced: bool = False):
+    """comerge::merge_parallel / merge_parallel_synced over records with a
+    key-only less and the full report (merge_options::count_comparisons
+    included; parallel.hpp:304-336).  Synchronous; host or device buffers."""
+    suf, size, m = _rec_info(a, key_dtype, record_bytes)
+    n = _rec_info(b, key_dtype, record_bytes)[2]
+    out_len = _rec_info(out, key_dtype, record_bytes)[2]
+    if workers < 0:
+        raise ValueError("merge_parallel: worker count must be positive")
+    count = bool(opts is not None and opts.count_comparisons)
+    rep = N.MergeReport()
+    bs = np.zeros(max(workers, 1), np.uint64)
+    its = np.zeros(2 * max(workers, 1), np.uint32)
+    cmp = C.c_uint64(0)
+    mo = N.MergeOptions(int(synced), int(count))
+    if _is_torch(out) and out.is_cuda:
+        torch.cuda.current_stream(out.device).synchronize()
+    with _on(out if _is_torch(out) and out.is_cuda else a):
+        N.check(getattr(N.lib, f"comerge_merge_parallel_records_ex_{suf}")(
+            _ptr(a), m, _ptr(b), n, _ptr(out), out_len, size, workers, C.byref(mo), C.byref(rep),
+            C.c_void_p(bs.ctypes.data), C.c_void_p(its.ctypes.data), C.byref(cmp)))
+    return MergeReport(
+        m=rep.m, n=rep.n, workers=rep.workers, wall_ns=rep.wall_ns,
+        block_sizes=[int(x) for x in bs[:workers]],
+        corank_iterations=[int(x) for x in its[:(workers if synced else 2 * workers)]],
+        comparisons=int(cmp.value) if count else None,
+        e2e_ns=rep.e2e_ns, h2d_bytes=rep.h2d_bytes, d2h_bytes=rep.d2h_bytes, tiles=rep.tiles)
+
+
 def merge_segmented(a, a_off, b, b_off, out=None, workspace=None, report=False):
     """Merge every pair s (a[a_off[s]:a_off[s+1]], b[b_off[s]:b_off[s+1]]) into
     out[a_off[s]+b_off[s]:...]: device tensors in one asynchronous launch;

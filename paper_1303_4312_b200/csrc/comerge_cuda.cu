@@ -1745,7 +1745,7 @@ template <typename KT, int S>
 int merge_parallel_records_sync(const void* a, size_t m, const void* b, size_t n, void* out,
                                 size_t out_len, size_t workers, int synced,
                                 comerge_merge_report* rep, uint64_t* block_sizes,
-                                uint32_t* corank_iterations) {
+                                uint32_t* corank_iterations, uint64_t* comparisons = nullptr) {
     const int A = records_align_class<KT, S>(a, m, b, n, out);
     if (A == 0)
         return fail(COMERGE_E_INVALID, "merge_parallel: arrays must be aligned to their record type");
@@ -1754,7 +1754,8 @@ int merge_parallel_records_sync(const void* a, size_t m, const void* b, size_t n
         return merge_parallel_sync<R, false>(static_cast<const R*>(a), nullptr, m,
                                              static_cast<const R*>(b), nullptr, n,
                                              static_cast<R*>(out), nullptr, out_len, workers,
-                                             synced, rep, block_sizes, corank_iterations);
+                                             synced, rep, block_sizes, corank_iterations,
+                                             comparisons);
     };
     if constexpr (S == 16) {
         return A >= 16 ? run(rec<KT, 16, 16>{}) : run(rec<KT, 16, 8>{});
@@ -1762,6 +1763,86 @@ int merge_parallel_records_sync(const void* a, size_t m, const void* b, size_t n
         return run(rec<KT, 12, 4>{});
     } else {
         return A >= 8 ? run(rec<KT, 8, 8>{}) : run(rec<KT, 8, 4>{});
+    }
+}
+
+// The reference's generic co_rank / plan / full-report merge_parallel over
+// records with a key-only less (corank.hpp:128-147 and parallel.hpp:94-115,
+// :304-336 instantiated with tagged<K> / tagged_key_less, oracle.hpp:22-37;
+// the comparator KAT of corank_test.cpp:205-214).  The record size arrives at
+// run time: 8 or 12 bytes with a 32-bit key, 16 with a 64-bit one.  Co-ranks
+// only read keys, so the narrowest-alignment instantiation serves every view.
+template <typename KT, typename Fn>
+int with_record_type(const char* who, size_t record_bytes, const void* a, size_t m, const void* b,
+                     size_t n, Fn&& fn) {
+    constexpr uintptr_t nat = sizeof(KT) - 1;  // the record struct's own alignment
+    if ((m && (reinterpret_cast<uintptr_t>(a) & nat)) || (n && (reinterpret_cast<uintptr_t>(b) & nat)))
+        return fail(COMERGE_E_INVALID, std::string(who) + ": arrays must be aligned to their record type");
+    if constexpr (sizeof(KT) == 8) {
+        if (record_bytes == 16) return fn(rec<KT, 16, 8>{});
+        return fail(COMERGE_E_INVALID, std::string(who) + ": records with a 64-bit key are 16 bytes");
+    } else {
+        if (record_bytes == 8) return fn(rec<KT, 8, 4>{});
+        if (record_bytes == 12) return fn(rec<KT, 12, 4>{});
+        return fail(COMERGE_E_INVALID, std::string(who) + ": records with a 32-bit key are 8 or 12 bytes");
+    }
+}
+
+template <typename KT>
+int co_rank_records_sync(uint64_t target, const void* a, size_t m, const void* b, size_t n,
+                         size_t record_bytes, uint64_t* j, uint64_t* k, uint32_t* iterations,
+                         uint32_t* comparisons) {
+    return with_record_type<KT>("co_rank", record_bytes, a, m, b, n, [&](auto tag) {
+        using R = decltype(tag);
+        return co_rank_sync<R>(target, static_cast<const R*>(a), m, static_cast<const R*>(b), n, j,
+                               k, iterations, comparisons);
+    });
+}
+
+template <typename KT>
+int plan_records_sync(const void* a, size_t m, const void* b, size_t n, size_t record_bytes,
+                      size_t workers, uint64_t* blocks) {
+    return with_record_type<KT>("plan", record_bytes, a, m, b, n, [&](auto tag) {
+        using R = decltype(tag);
+        return plan_sync<R>(static_cast<const R*>(a), m, static_cast<const R*>(b), n, workers,
+                            blocks);
+    });
+}
+
+template <typename KT>
+int co_rank_batch_records_device(const uint64_t* ranks, size_t count, const void* a, size_t m,
+                                 const void* b, size_t n, size_t record_bytes, uint64_t* out_j,
+                                 uint32_t* out_it, uint32_t* out_cmp, cudaStream_t s) {
+    return with_record_type<KT>("co_rank", record_bytes, a, m, b, n, [&](auto tag) {
+        using R = decltype(tag);
+        return co_rank_batch_device<R>(ranks, count, static_cast<const R*>(a), m,
+                                       static_cast<const R*>(b), n, out_j, out_it, out_cmp, s);
+    });
+}
+
+template <typename KT>
+int merge_parallel_records_ex(const void* a, size_t m, const void* b, size_t n, void* out,
+                              size_t out_len, size_t record_bytes, size_t workers,
+                              const comerge_merge_options* opts, comerge_merge_report* rep,
+                              uint64_t* block_sizes, uint32_t* corank_iterations,
+                              uint64_t* comparisons) {
+    const int synced = opts ? opts->synced : 0;
+    if (opts && opts->count_comparisons && !comparisons)
+        return fail(COMERGE_E_INVALID, "merge_parallel: count_comparisons needs an output");
+    uint64_t* cmp = opts && opts->count_comparisons ? comparisons : nullptr;
+    if constexpr (sizeof(KT) == 8) {
+        if (record_bytes == 16)
+            return merge_parallel_records_sync<KT, 16>(a, m, b, n, out, out_len, workers, synced,
+                                                       rep, block_sizes, corank_iterations, cmp);
+        return fail(COMERGE_E_INVALID, "merge_parallel: records with a 64-bit key are 16 bytes");
+    } else {
+        if (record_bytes == 8)
+            return merge_parallel_records_sync<KT, 8>(a, m, b, n, out, out_len, workers, synced,
+                                                      rep, block_sizes, corank_iterations, cmp);
+        if (record_bytes == 12)
+            return merge_parallel_records_sync<KT, 12>(a, m, b, n, out, out_len, workers, synced,
+                                                       rep, block_sizes, corank_iterations, cmp);
+        return fail(COMERGE_E_INVALID, "merge_parallel: records with a 32-bit key are 8 or 12 bytes");
     }
 }
 
@@ -2143,6 +2224,38 @@ size_t comerge_cuda_records12_workspace_bytes(size_t m, size_t n) {
 
 COMERGE_RECORDS12(i32, int32_t)
 COMERGE_RECORDS12(u32, uint32_t)
+
+#define COMERGE_RECORDS_GENERIC(SUF, KT)                                                         \
+    int comerge_co_rank_records_##SUF(uint64_t target, const void* a, size_t m, const void* b,   \
+                                      size_t n, size_t record_bytes, uint64_t* j, uint64_t* k,   \
+                                      uint32_t* iterations, uint32_t* comparisons) {             \
+        return co_rank_records_sync<KT>(target, a, m, b, n, record_bytes, j, k, iterations,      \
+                                        comparisons);                                            \
+    }                                                                                            \
+    int comerge_plan_records_##SUF(const void* a, size_t m, const void* b, size_t n,             \
+                                   size_t record_bytes, size_t workers, uint64_t* blocks) {      \
+        return plan_records_sync<KT>(a, m, b, n, record_bytes, workers, blocks);                 \
+    }                                                                                            \
+    int comerge_cuda_co_rank_batch_records_##SUF(                                                \
+        const uint64_t* ranks, size_t count, const void* a, size_t m, const void* b, size_t n,   \
+        size_t record_bytes, uint64_t* out_j, uint32_t* out_it, uint32_t* out_cmp,               \
+        comerge_stream_t stream) {                                                               \
+        return co_rank_batch_records_device<KT>(ranks, count, a, m, b, n, record_bytes, out_j,   \
+                                                out_it, out_cmp, stream);                        \
+    }                                                                                            \
+    int comerge_merge_parallel_records_ex_##SUF(                                                 \
+        const void* a, size_t m, const void* b, size_t n, void* out, size_t out_len,             \
+        size_t record_bytes, size_t workers, const comerge_merge_options* opts,                  \
+        comerge_merge_report* report, uint64_t* block_sizes, uint32_t* corank_iterations,        \
+        uint64_t* comparisons) {                                                                 \
+        return merge_parallel_records_ex<KT>(a, m, b, n, out, out_len, record_bytes, workers,    \
+                                             opts, report, block_sizes, corank_iterations,       \
+                                             comparisons);                                       \
+    }
+
+COMERGE_RECORDS_GENERIC(i32, int32_t)
+COMERGE_RECORDS_GENERIC(u32, uint32_t)
+COMERGE_RECORDS_GENERIC(u64, uint64_t)
 
 static_assert(sizeof(comerge_rec_i32) == sizeof(rec<int32_t, 8, 8>) &&
                   sizeof(comerge_rec_u64) == sizeof(rec<uint64_t, 16, 16>) &&

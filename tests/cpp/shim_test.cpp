@@ -327,6 +327,82 @@ static void records() {
         [&] { cm::merge_parallel(x, y, bad, 2, cm::key_less{}); }, "output length must equal"));
 }
 
+// co_rank / co_rank_counted / plan / merge_parallel_synced / count_comparisons
+// over records with a key-only comparator: everything equals the same call on
+// the records' key arrays (only keys are compared).
+static void records_api() {
+    // corank_test.cpp:205-214: ordering on the first component only, ties stay
+    // a-before-b ({int, char} as an 8-byte record with the key first)
+    struct pr {
+        std::int32_t key;
+        char tag;
+    };
+    static_assert(sizeof(pr) == 8);
+    const std::vector<pr> pa{{1, 'x'}, {2, 'y'}}, pb{{1, 'z'}, {2, 'w'}};
+    CHECK((cm::co_rank(1, pa, pb, cm::key_less{}) == cm::co_ranks{1, 0}));
+    CHECK((cm::co_rank(2, pa, pb, cm::key_less{}) == cm::co_ranks{1, 1}));
+    CHECK((cm::co_rank(3, pa, pb, cm::key_less{}) == cm::co_ranks{2, 1}));
+    CHECK(throws_with<std::out_of_range>([&] { cm::co_rank(5, pa, pb, cm::key_less{}); },
+                                         "rank out of range"));
+    std::mt19937_64 rng(21);
+    const std::size_t m = 3001, n = 1777;
+    keys ka(m), kb(n);
+    for (auto& x : ka) x = rng() % 40;
+    for (auto& x : kb) x = rng() % 40;
+    std::sort(ka.begin(), ka.end());
+    std::sort(kb.begin(), kb.end());
+    auto check_shape = [&](auto tag, auto keys_tag) {
+        using T = decltype(tag);
+        using K = decltype(keys_tag);
+        std::vector<T> ta(m), tb(n);
+        std::vector<K> xa(m), xb(n);
+        for (std::size_t i = 0; i < m; ++i) {
+            xa[i] = K(ka[i]);
+            ta[i] = {K(ka[i]), origin::from_a, std::uint32_t(i)};
+        }
+        for (std::size_t i = 0; i < n; ++i) {
+            xb[i] = K(kb[i]);
+            tb[i] = {K(kb[i]), origin::from_b, std::uint32_t(i)};
+        }
+        for (std::size_t i : {std::size_t{0}, std::size_t{1}, m, (m + n) / 2, m + n - 1, m + n}) {
+            cm::co_rank_stats sr, sk;
+            CHECK((cm::co_rank(i, ta, tb, tagged_key_less{}, &sr) == cm::co_rank(i, xa, xb, {}, &sk)));
+            CHECK(sr.iterations == sk.iterations && sr.comparisons == sk.comparisons);
+            cm::comparison_counter cr, ck;
+            cm::co_rank_counted(i, ta, tb, tagged_key_less{}, cr);
+            cm::co_rank_counted(i, xa, xb, {}, ck);
+            CHECK(cr.count == ck.count);
+        }
+        for (std::size_t w : {std::size_t{1}, std::size_t{5}, std::size_t{64}}) {
+            const auto pr_ = cm::plan(ta, tb, w, tagged_key_less{});
+            const auto pk = cm::plan(xa, xb, w);
+            CHECK(pr_.workers == w && pr_.blocks == pk.blocks);
+            cm::merge_options opts;
+            opts.count_comparisons = true;
+            std::vector<T> out(m + n);
+            std::vector<K> kout(m + n);
+            const auto expect = naive_merge_by_key(ta, tb);
+            for (bool synced : {false, true}) {
+                const auto rr = synced ? cm::merge_parallel_synced(ta, tb, out, w, tagged_key_less{}, opts)
+                                       : cm::merge_parallel(ta, tb, out, w, tagged_key_less{}, opts);
+                const auto rk = synced ? cm::merge_parallel_synced(xa, xb, kout, w, {}, opts)
+                                       : cm::merge_parallel(xa, xb, kout, w, {}, opts);
+                CHECK(out == expect);
+                CHECK(rr.comparisons.has_value() && rr.comparisons == rk.comparisons);
+                CHECK(rr.block_sizes == rk.block_sizes);
+                CHECK(rr.corank_iterations == rk.corank_iterations);
+                CHECK(rr.corank_iterations.size() == (synced ? w : 2 * w));
+            }
+            CHECK(!cm::merge_parallel(ta, tb, out, w, tagged_key_less{}).comparisons.has_value());
+        }
+        CHECK(throws_with<std::invalid_argument>([&] { cm::plan(ta, tb, 0, tagged_key_less{}); },
+                                                 "worker count must be positive"));
+    };
+    check_shape(tagged<std::uint64_t>{}, std::uint64_t{});
+    check_shape(tagged<std::int32_t>{}, std::int32_t{});
+    check_shape(tagged<std::uint32_t>{}, std::uint32_t{});
+}
+
 // host-buffer merges of vectors in page-locked memory (pinned_allocator)
 static void pinned_vectors() {
     std::mt19937_64 rng(5);
@@ -357,6 +433,7 @@ int main() {
     pinned_vectors();
     comparisons();
     records();
+    records_api();
     sweep<std::int32_t>(1);
     sweep<std::uint32_t>(2);
     sweep<std::uint64_t>(3);

@@ -254,3 +254,101 @@ def test_tagged12_c2_full_size(cuda):
     b = tagged(inp["b"].cpu().numpy(), 1)
     del inp
     check_tagged(device_merge12(a, b, cuda), a, b)
+
+
+# ---- the rest of the reference's generic API over records with a key-only
+# less: co_rank / co_rank_counted (corank.hpp:128-147), plan
+# (parallel.hpp:94-115), merge_parallel / merge_parallel_synced with
+# merge_options::count_comparisons (parallel.hpp:304-336).  Only keys are
+# compared, so every number equals the reference's on the records' key arrays.
+
+def _record_cases(rng):
+    for dt, size in [(np.int32, 8), (np.uint32, 8), (np.int32, 12), (np.uint32, 12),
+                     (np.uint64, 16)]:
+        for m, n, alphabet in [(0, 0, 3), (0, 9, 3), (7, 0, 3), (2, 2, 1), (1000, 777, 5),
+                               (20_000, 30_001, 0)]:
+            ka, kb = _keys(rng, dt, m, alphabet), _keys(rng, dt, n, alphabet)
+            if size == 12:
+                yield ka, kb, tagged(ka, 0), tagged(kb, 1)
+            else:
+                yield ka, kb, records(ka, 0), records(kb, 1 << 31)
+
+
+def test_records_co_rank_and_plan_match_reference(cuda):
+    from oracle.py import Ref
+    ref = Ref()
+    rng = np.random.default_rng(99)
+    for ka, kb, a, b in _record_cases(rng):
+        total, size, kd = len(ka) + len(kb), a.dtype.itemsize, ka.dtype
+        ranks = sorted({0, total, total // 2, min(total, 1), max(total, 1) - 1,
+                        *(int(x) for x in rng.integers(0, total + 1, 6))})
+        ta, tb = on_device(a, cuda, 0), on_device(b, cuda, 0)
+        for i in ranks:
+            want, wstats = ref.co_rank(i, ka, kb, stats=True)
+            st = P().CoRankStats()
+            assert P().co_rank_records(i, a, b, stats=st) == want           # host arrays
+            assert (st.iterations, st.comparisons) == wstats
+            st = P().CoRankStats()
+            assert P().co_rank_records(i, ta, tb, key_dtype=kd, record_bytes=size,
+                                       stats=st) == want                     # device views
+            assert (st.iterations, st.comparisons) == wstats
+        with pytest.raises(IndexError, match="rank out of range"):
+            P().co_rank_records(total + 1, a, b)
+        # batched, on the device
+        r = torch.tensor(ranks, dtype=torch.int64, device=cuda).view(torch.uint64)
+        j, it, cmp = P().co_rank_batch_records(r, ta, tb, kd, size, with_stats=True)
+        torch.cuda.synchronize()
+        wants = [ref.co_rank(i, ka, kb, stats=True) for i in ranks]
+        assert j.view(torch.int64).tolist() == [w[0][0] for w in wants]
+        assert it.view(torch.int32).tolist() == [w[1][0] for w in wants]
+        assert cmp.view(torch.int32).tolist() == [w[1][1] for w in wants]
+        for workers in (1, 3, 16):
+            got = [blk.as_tuple() for blk in P().plan_records(a, b, workers)]
+            assert got == [tuple(int(x) for x in row) for row in ref.plan(ka, kb, workers)]
+            assert got == [blk.as_tuple() for blk in
+                           P().plan_records(ta, tb, workers, key_dtype=kd, record_bytes=size)]
+    with pytest.raises(ValueError, match="worker count must be positive"):
+        P().plan_records(a, b, 0)
+    with pytest.raises(ValueError, match="8 or 12 bytes"):
+        P().co_rank_records(0, np.zeros(32, np.uint8), np.zeros(32, np.uint8),
+                            key_dtype=np.int32, record_bytes=16)
+
+
+def test_records_full_report_matches_reference(cuda):
+    """block sizes, co-rank iterations and count_comparisons totals of the
+    record merges = the reference's merge_parallel on the key arrays, both
+    modes; the merged records byte for byte (host staging, the chunked host
+    pipeline and device buffers)."""
+    from oracle.py import Ref
+    ref = Ref()
+    rng = np.random.default_rng(123)
+    opts = P().MergeOptions(count_comparisons=True)
+    cases = list(_record_cases(rng))
+    dt = np.int32  # one case through the chunked host pipeline (>= 2^20 records)
+    ka, kb = _keys(rng, dt, 1_300_000, 50), _keys(rng, dt, 900_001, 50)
+    cases.append((ka, kb, tagged(ka, 0), tagged(kb, 1)))
+    for ka, kb, a, b in cases:
+        size, kd = a.dtype.itemsize, ka.dtype
+        for workers in (1, 5, 33):
+            for synced in (False, True):
+                _, rrep, rbs, rits = ref.merge_parallel(ka, kb, workers, synced=synced, count=True)
+                nit = workers if synced else 2 * workers
+                out = np.zeros(len(a) + len(b), a.dtype)
+                rep = P().merge_parallel_records(a, b, out, workers, opts=opts, synced=synced)
+                if size == 12:
+                    check_tagged(out, a, b)
+                else:
+                    check(out, a, b)
+                assert rep.block_sizes == [int(x) for x in rbs[:workers]]
+                assert rep.corank_iterations == [int(x) for x in rits[:nit]]
+                assert rep.comparisons == int(rrep.comparisons)
+                if len(a) + len(b) > 100_000:
+                    continue
+                ta, tb = on_device(a, cuda, 0), on_device(b, cuda, 0)
+                to = torch.zeros((len(a) + len(b)) * size, dtype=torch.uint8, device=cuda)
+                drep = P().merge_parallel_records(ta, tb, to, workers, key_dtype=kd,
+                                                  record_bytes=size, opts=opts, synced=synced)
+                assert to.cpu().numpy().tobytes() == out.tobytes()
+                assert (drep.block_sizes, drep.corank_iterations, drep.comparisons) == \
+                    (rep.block_sizes, rep.corank_iterations, rep.comparisons)
+        assert P().merge_parallel_records(a, b, out, 2).comparisons is None
