@@ -82,6 +82,8 @@ EXTRA = {
                desc="diagnostic: segmented batch of 2^20 small pairs, m_s,n_s in [1,64]"),
     "X4": dict(kind="segmented", dtype="int32", nseg=2**21, maxlen=16, width=2**20,
                desc="diagnostic: segmented batch of 2^21 tiny pairs, m_s,n_s in [1,16]"),
+    "X5": dict(kind="keys", dtype="uint64", m=2**26, n=2**26, width=0,
+               desc="diagnostic: uint64 keys only (the reference's key_t), m=n=2^26, full range"),
 }
 HEADLINE = "C4"
 SEED = 5

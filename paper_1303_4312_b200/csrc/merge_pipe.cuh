@@ -76,10 +76,16 @@ struct pipe_cfg<int32_t, true> {
 };
 template <>
 struct pipe_cfg<uint32_t, true> : pipe_cfg<int32_t, true> {};
-// 64-bit keys only: tile 2816, 4 stages of ~23 KB.
+// 64-bit keys only (the reference's key_t): tile 3840, 3 stages of ~31 KB
+// (2^26 + 2^26 uniform keys: VT 11 x 4 stages 365 us, 13 x 4 346, 15 x 3 341,
+// 17 x 3 343 -- fewer, larger tiles amortise the per-tile barriers and probes).
+#ifndef PIPE_K64_VT
+#define PIPE_K64_VT 15
+#define PIPE_K64_NST 3
+#endif
 template <>
 struct pipe_cfg<uint64_t, false> {
-    static constexpr int NC = 256, VT = 11, NST = 4;
+    static constexpr int NC = 256, VT = PIPE_K64_VT, NST = PIPE_K64_NST;
 };
 // 64-bit keys + payload: tile 2816, 3 stages of ~34 KB.
 template <>

@@ -188,7 +188,8 @@ def _draw(rng, dt, size, alphabet):
 
 
 # tile sizes of the pipeline (keys-only) and tile kernels: shapes straddle both
-TILES = {np.int32: 256 * 31, np.uint32: 256 * 15, np.uint64: 256 * 11}
+TILES = {np.int32: 256 * 31, np.uint32: 256 * 31, np.uint64: 256 * 15}
+PAIR_TILES = {np.int32: 256 * 15, np.uint32: 256 * 15, np.uint64: 256 * 11}
 
 
 @pytest.mark.parametrize("dt", [np.int32, np.uint32, np.uint64])
@@ -197,6 +198,8 @@ def test_random_sweep_keys_and_pairs(cuda, path, port, dt):
     T = TILES[dt]
     shapes = [(0, 0), (0, 1), (1, 0), (T - 1, 0), (0, T + 1), (T, T), (T - 1, 1), (1, T - 1),
               (2 * T + 3, 5), (5, 3 * T - 2), (3, 50000), (50000, 3), (70001, 69999)]
+    T2 = PAIR_TILES[dt]  # the key-value tile
+    shapes += [(T2 - 1, 0), (0, T2 + 1), (T2, T2), (T2 - 1, 1), (2 * T2 + 3, 5), (5, 3 * T2 - 2)]
     shapes += [(int(rng.integers(0, 20000)), int(rng.integers(0, 20000))) for _ in range(12)]
     for idx, (m, n) in enumerate(shapes):
         alphabet = [0, 1, 2, 16, 1000][idx % 5]

@@ -19,10 +19,11 @@ def main():
     import bench
     bench.CONFIGS.update(bench.EXTRA)
     dev = torch.device("cuda:0")
+    flush = bench.L2Flush(dev)
     for cfg in args.configs.split(","):
         r, st = [], []
         for _ in range(args.rounds):
-            t = bench.time_config(cfg, args.steps, 3, dev)
+            t = bench.time_config(cfg, args.steps, 3, dev, flush)
             r.append(statistics.mean(t["kern_ms"]) * 1e3)
             st.append(statistics.mean(t["step_ms"]) * 1e3)
         print(f"{args.name:8s} {cfg:4s} kernel us {min(r):8.1f}  step us {min(st):8.1f}  "
