@@ -1,13 +1,15 @@
 // sort.cuh -- stable merge sort built on the merge path (SURVEY.md §8f row 1:
 // "GPU merge sort built on the segmented kernel").
 //
-//   1. block_sort_kernel: every CTA sorts one run of R = NT*VT elements in
-//      shared memory -- VT elements per thread by a sorting network in
+//   1. block_sort_kernel: every CTA sorts one run of R elements in shared
+//      memory -- VT (odd) elements per thread by a sorting network in
 //      registers (keys only; the key-value variant uses odd-even
 //      transposition, swapping only on strictly-less, so equal keys keep
-//      their order), then log2(NT) rounds of pairwise merges of the sorted lists,
-//      each thread taking VT outputs at its merge-path split (the Lemma-1
-//      split of corank.hpp:93-94, ties to the left list as merge.hpp:22-31).
+//      their order), then rounds of pairwise merges of the sorted lists
+//      (the first five inside one warp: warp barriers only), each thread
+//      taking VT outputs at its merge-path split (the Lemma-1 split of
+//      corank.hpp:93-94, ties to the left list as merge.hpp:22-31) with the
+//      pipeline consumers' serial merge (merge_serial.cuh).
 //   2. log2(n/R) merge passes of the tile pipeline in merge-pass mode
 //      (merge_pipe.cuh, pipe_args::run_len): pass p merges runs 2s and 2s+1
 //      of length R*2^p as one segmented batch with implicit offsets.
@@ -20,21 +22,33 @@
 #include <limits>
 
 #include "corank.cuh"
+#include "merge_serial.cuh"
 #include "ptx.cuh"
 
 namespace comerge_b200 {
 
+// Base runs of R elements (a power of two: the merge passes' run arithmetic
+// is shifts) sorted by NA = ceil(R / VT) threads of VT elements each, VT ODD:
+// thread t's elements sit at s[t*VT + v], an odd word stride, so the staging
+// accesses of a warp are bank-conflict free without padding and the rounds
+// can run the pipeline consumers' lean serial merge on plain shared addresses
+// (merge_serial.cuh, ~12 instructions per output).  The last slots (R .. NA*VT)
+// hold padding keys.
 template <typename K>
 struct sort_cfg {
-    static constexpr int NT = 512;
-    static constexpr int VT = sizeof(K) == 8 ? 8 : 16;
-    static constexpr int R = NT * VT;  // base run (a power of two)
+    static constexpr int VT = sizeof(K) == 8 ? 9 : 17;
+    static constexpr int R = sizeof(K) == 8 ? 4096 : 8192;  // base run (a power of two)
+    static constexpr int NA = (R + VT - 1) / VT;            // threads holding elements
+    static constexpr int NT = (NA + 31) / 32 * 32;          // 512 / 480
+    static constexpr int S = NA * VT;                       // slots incl. padding
+    static_assert(NA <= NT && (R & (R - 1)) == 0, "block sort shape");
 };
 
 // Batcher's odd-even merge sort network over the VT registers of a thread
 // (keys only: equal keys are indistinguishable, so the network need not be
-// stable): 63 compare-exchanges for 16 keys, 19 for 8, against 120 / 28 for
-// odd-even transposition; min / max of 32-bit keys are one instruction each.
+// stable; any VT -- checked by the 0-1 principle for 8, 9, 16, 17): 85
+// compare-exchanges for 17 keys, 28 for 9, against 136 / 36 for odd-even
+// transposition; min / max of 32-bit keys are one instruction each.
 template <typename K, int VT>
 __device__ __forceinline__ void network_sort(K (&k)[VT]) {
 #pragma unroll
@@ -52,105 +66,15 @@ __device__ __forceinline__ void network_sort(K (&k)[VT]) {
                     }
 }
 
-// Shared-memory index with one pad word per 32 elements: thread t's VT
-// consecutive elements (t*VT + v) then fall in distinct banks across a warp
-// (without it VT = 16 is a 16-way bank conflict on every staging access).
-__device__ __forceinline__ int spad(int i) { return i + (i >> 5); }
-
-template <typename K>
-__global__ void __launch_bounds__(sort_cfg<K>::NT)
-    block_sort_kernel(const K* __restrict__ in, K* __restrict__ out, uint64_t n) {
-    constexpr int NT = sort_cfg<K>::NT, VT = sort_cfg<K>::VT, R = sort_cfg<K>::R;
-    // + slack: a finished list may be read one past its end (never used)
-    __shared__ K s[R + R / 32 + 4];
-    pdl_trigger();  // the first merge pass may be scheduled (it waits for this grid)
-    const uint64_t base = uint64_t(blockIdx.x) * R;
-    const int cnt = n - base < uint64_t(R) ? int(n - base) : R;
-    const int t = threadIdx.x;
-    // padding sorts last and, being last in input order, stays behind real maxima
-    const K pad = std::numeric_limits<K>::max();
-    for (int x = t; x < R; x += NT) s[spad(x)] = x < cnt ? in[base + x] : pad;
-    __syncthreads();
-    K k[VT];
-#pragma unroll
-    for (int v = 0; v < VT; ++v) k[v] = s[spad(t * VT + v)];
-    network_sort<K, VT>(k);
-    for (int w = VT; w < R; w *= 2) {
-        __syncthreads();  // previous round's reads are done
-#pragma unroll
-        for (int v = 0; v < VT; ++v) s[spad(t * VT + v)] = k[v];
-        __syncthreads();
-        const int d = t * VT;
-        const int a0 = d / (2 * w) * (2 * w), b0 = a0 + w;  // list starts
-        const int diag = d - a0;
-        int lo = diag > w ? diag - w : 0, hi = diag < w ? diag : w;
-        while (lo < hi) {  // Lemma-1 split (ties to the left list)
-            const int mid = (lo + hi + 1) >> 1;
-            if (s[spad(b0 + diag - mid)] < s[spad(a0 + mid - 1)])
-                hi = mid - 1;
-            else
-                lo = mid;
-        }
-        int ia = lo, ib = diag - lo;
-        K ka = s[spad(a0 + ia)], kb = s[spad(b0 + ib)];
-#pragma unroll
-        for (int v = 0; v < VT; ++v) {  // branch-free: one shared load per output
-            const bool take_b = ib < w && (ia >= w || kb < ka);
-            k[v] = take_b ? kb : ka;
-            ia += take_b ? 0 : 1;
-            ib += take_b ? 1 : 0;
-            const K nx = s[spad(take_b ? b0 + ib : a0 + ia)];
-            ka = take_b ? ka : nx;
-            kb = take_b ? nx : kb;
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int v = 0; v < VT; ++v) s[spad(t * VT + v)] = k[v];
-    __syncthreads();
-    for (int x = t; x < cnt; x += NT) out[base + x] = s[spad(x)];
-}
-
-// Key-value variant: the uint32 payload moves with its key (VT = 8, runs of
-// 4096 pairs, 2048 for 64-bit keys; keys and payloads in two padded shared
-// arrays within the 48 KB static limit).
-template <typename K>
-struct sort_pairs_cfg {
-    static constexpr int NT = sizeof(K) == 8 ? 256 : 512;
-    static constexpr int VT = 8;
-    static constexpr int R = NT * VT;
-};
-
-template <typename K>
-__global__ void __launch_bounds__(sort_pairs_cfg<K>::NT)
-    block_sort_pairs_kernel(const K* __restrict__ in, const uint32_t* __restrict__ in_v,
-                            K* __restrict__ out, uint32_t* __restrict__ out_v, uint64_t n) {
-    constexpr int NT = sort_pairs_cfg<K>::NT, VT = sort_pairs_cfg<K>::VT,
-                  R = sort_pairs_cfg<K>::R;
-    __shared__ K s[R + R / 32 + 4];
-    __shared__ uint32_t sv[R + R / 32 + 4];
-    pdl_trigger();
-    const uint64_t base = uint64_t(blockIdx.x) * R;
-    const int cnt = n - base < uint64_t(R) ? int(n - base) : R;
-    const int t = threadIdx.x;
-    const K pad = std::numeric_limits<K>::max();
-    for (int x = t; x < R; x += NT) {
-        s[spad(x)] = x < cnt ? in[base + x] : pad;
-        sv[spad(x)] = x < cnt ? in_v[base + x] : 0u;
-    }
-    __syncthreads();
-    K k[VT];
-    uint32_t p[VT];
-#pragma unroll
-    for (int v = 0; v < VT; ++v) {
-        k[v] = s[spad(t * VT + v)];
-        p[v] = sv[spad(t * VT + v)];
-    }
+// Stable variant for key-value pairs: odd-even transposition, swapping only
+// on strictly-less, so equal keys keep their order.
+template <typename K, int VT>
+__device__ __forceinline__ void transposition_sort(K (&k)[VT], uint32_t (&p)[VT]) {
 #pragma unroll
     for (int pass = 0; pass < VT; ++pass) {
 #pragma unroll
         for (int v = pass & 1; v + 1 < VT; v += 2) {
-            if (k[v + 1] < k[v]) {  // strict: equal keys keep their order
+            if (k[v + 1] < k[v]) {
                 const K x = k[v];
                 k[v] = k[v + 1];
                 k[v + 1] = x;
@@ -160,50 +84,153 @@ __global__ void __launch_bounds__(sort_pairs_cfg<K>::NT)
             }
         }
     }
-    for (int w = VT; w < R; w *= 2) {
-        __syncthreads();
+}
+
+// One merge round of the block sort: sorted lists of W slots are merged in
+// pairs (the last list of the array may be short or missing); thread t takes
+// the VT outputs from its merge-path split (the Lemma-1 split of
+// corank.hpp:93-94, ties to the left list as merge.hpp:22-31).  Rounds whose
+// list pairs lie inside one warp's 32*VT slots synchronise the warp only.
+template <typename K, int VT, int S, int W, bool HAS_V>
+__device__ __forceinline__ void block_sort_round(K* s, uint32_t* sv, int t, bool active,
+                                                 K (&k)[VT], uint32_t (&p)[VT]) {
+    constexpr bool kWarpLocal = 2 * W <= 32 * VT;
+    if constexpr (kWarpLocal) __syncwarp(); else __syncthreads();  // previous reads are done
+    if (active) {
 #pragma unroll
         for (int v = 0; v < VT; ++v) {
-            s[spad(t * VT + v)] = k[v];
-            sv[spad(t * VT + v)] = p[v];
+            s[t * VT + v] = k[v];
+            if constexpr (HAS_V) sv[t * VT + v] = p[v];
         }
-        __syncthreads();
-        const int d = t * VT;
-        const int a0 = d / (2 * w) * (2 * w), b0 = a0 + w;
-        const int diag = d - a0;
-        int lo = diag > w ? diag - w : 0, hi = diag < w ? diag : w;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (s[spad(b0 + diag - mid)] < s[spad(a0 + mid - 1)])
-                hi = mid - 1;
-            else
-                lo = mid;
-        }
-        int ia = lo, ib = diag - lo;
-        K ka = s[spad(a0 + ia)], kb = s[spad(b0 + ib)];
+    }
+    if constexpr (kWarpLocal) __syncwarp(); else __syncthreads();
+    if (!active) return;
+    const int d = t * VT;
+    const int a0 = d / (2 * W) * (2 * W);
+    const int la = S - a0 < W ? S - a0 : W;
+    const int b0 = a0 + la;
+    const int lb = S - b0 < W ? S - b0 : W;
+    uint32_t src[VT];
+    // Lemma-1 split of the thread's diagonal (the data-dependent search of
+    // merge_serial.cuh; a branch-free fixed-trip form -- 8 instead of 13
+    // instructions per iteration -- measured 2^26 int32 keys 1.860 instead of
+    // 1.805 ms: threads near a list pair's ends have narrow brackets)
+    const int diag = d - a0;
+    const K* sA = s + a0;
+    const K* sB = s + b0;
+    const int j = smem_split<K>(sA, la, sB, lb, diag);
+    const uint32_t pa0 = smem_addr(sA), pb0 = smem_addr(sB);
+    constexpr uint32_t SZ = sizeof(K);
+    serial_merge<K, VT, HAS_V, false>(pa0 + uint32_t(j) * SZ, pa0 + uint32_t(la) * SZ,
+                                      pb0 + uint32_t(diag - j) * SZ, pb0 + uint32_t(lb) * SZ, 0,
+                                      0, VT, k, src);
+    if constexpr (HAS_V) {
+        const uint32_t base = smem_addr(s);
+        constexpr int SH = sizeof(K) == 8 ? 3 : 2;
 #pragma unroll
-        for (int v = 0; v < VT; ++v) {
-            const bool take_b = ib < w && (ia >= w || kb < ka);
-            k[v] = take_b ? kb : ka;
-            p[v] = sv[spad(take_b ? b0 + ib : a0 + ia)];
-            ia += take_b ? 0 : 1;
-            ib += take_b ? 1 : 0;
-            const K nx = s[spad(take_b ? b0 + ib : a0 + ia)];
-            ka = take_b ? ka : nx;
-            kb = take_b ? nx : kb;
+        for (int v = 0; v < VT; ++v) p[v] = sv[(src[v] - base) >> SH];
+    }
+}
+
+template <typename K, int VT, int S, int W, bool HAS_V>
+__device__ __forceinline__ void block_sort_rounds(K* s, uint32_t* sv, int t, bool active,
+                                                  K (&k)[VT], uint32_t (&p)[VT]) {
+    if constexpr (W < S) {
+        block_sort_round<K, VT, S, W, HAS_V>(s, sv, t, active, k, p);
+        block_sort_rounds<K, VT, S, 2 * W, HAS_V>(s, sv, t, active, k, p);
+    }
+}
+
+// Shared body of the keys and key-value block sorts (CFG: NT, VT, R, NA, S).
+template <typename K, typename CFG, bool HAS_V>
+__device__ __forceinline__ void block_sort_body(K* s, uint32_t* sv, const K* __restrict__ in,
+                                                const uint32_t* __restrict__ in_v,
+                                                K* __restrict__ out, uint32_t* __restrict__ out_v,
+                                                uint64_t n) {
+    constexpr int NT = CFG::NT, VT = CFG::VT, R = CFG::R, NA = CFG::NA, S = CFG::S;
+    pdl_trigger();  // the first merge pass may be scheduled (it waits for this grid)
+    const uint64_t base = uint64_t(blockIdx.x) * R;
+    const int cnt = n - base < uint64_t(R) ? int(n - base) : R;
+    const int t = threadIdx.x;
+    // padding sorts last and, being last in input order, stays behind real maxima
+    const K pad = std::numeric_limits<K>::max();
+    {  // coalesced loads, all in flight before the first shared store
+        constexpr int kIters = (S + 4 + NT - 1) / NT;  // + the merge's look-ahead slack
+        K lk[kIters];
+        uint32_t lv[kIters];
+#pragma unroll
+        for (int i = 0; i < kIters; ++i) {
+            const int x = t + i * NT;
+            lk[i] = x < cnt ? in[base + x] : pad;
+            if constexpr (HAS_V) lv[i] = x < cnt ? in_v[base + x] : 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < kIters; ++i) {
+            const int x = t + i * NT;
+            if (x < S + 4) {
+                s[x] = lk[i];
+                if constexpr (HAS_V) sv[x] = lv[i];
+            }
         }
     }
     __syncthreads();
+    const bool active = t < NA;
+    K k[VT];
+    uint32_t p[VT];
+    if (active) {
 #pragma unroll
-    for (int v = 0; v < VT; ++v) {
-        s[spad(t * VT + v)] = k[v];
-        sv[spad(t * VT + v)] = p[v];
+        for (int v = 0; v < VT; ++v) {
+            k[v] = s[t * VT + v];
+            if constexpr (HAS_V) p[v] = sv[t * VT + v];
+        }
+        if constexpr (HAS_V)
+            transposition_sort<K, VT>(k, p);
+        else
+            network_sort<K, VT>(k);
+    }
+    block_sort_rounds<K, VT, S, VT, HAS_V>(s, sv, t, active, k, p);
+    __syncthreads();
+    if (active) {
+#pragma unroll
+        for (int v = 0; v < VT; ++v) {
+            s[t * VT + v] = k[v];
+            if constexpr (HAS_V) sv[t * VT + v] = p[v];
+        }
     }
     __syncthreads();
     for (int x = t; x < cnt; x += NT) {
-        out[base + x] = s[spad(x)];
-        out_v[base + x] = sv[spad(x)];
+        out[base + x] = s[x];
+        if constexpr (HAS_V) out_v[base + x] = sv[x];
     }
+}
+
+template <typename K>
+__global__ void __launch_bounds__(sort_cfg<K>::NT)
+    block_sort_kernel(const K* __restrict__ in, K* __restrict__ out, uint64_t n) {
+    __shared__ __align__(16) K s[sort_cfg<K>::S + 4];
+    block_sort_body<K, sort_cfg<K>, false>(s, nullptr, in, nullptr, out, nullptr, n);
+}
+
+// Key-value variant: the uint32 payload moves with its key (runs of 4096
+// pairs, 2048 for 64-bit keys; keys and payloads in two shared arrays within
+// the 48 KB static limit).
+template <typename K>
+struct sort_pairs_cfg {
+    static constexpr int VT = 9;
+    static constexpr int R = sizeof(K) == 8 ? 2048 : 4096;
+    static constexpr int NA = (R + VT - 1) / VT;
+    static constexpr int NT = (NA + 31) / 32 * 32;  // 480 / 256
+    static constexpr int S = NA * VT;
+    static_assert(NA <= NT && (R & (R - 1)) == 0, "block sort shape");
+};
+
+template <typename K>
+__global__ void __launch_bounds__(sort_pairs_cfg<K>::NT)
+    block_sort_pairs_kernel(const K* __restrict__ in, const uint32_t* __restrict__ in_v,
+                            K* __restrict__ out, uint32_t* __restrict__ out_v, uint64_t n) {
+    __shared__ __align__(16) K s[sort_pairs_cfg<K>::S + 4];
+    __shared__ uint32_t sv[sort_pairs_cfg<K>::S + 4];
+    block_sort_body<K, sort_pairs_cfg<K>, true>(s, sv, in, in_v, out, out_v, n);
 }
 
 }  // namespace comerge_b200
