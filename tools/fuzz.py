@@ -62,7 +62,8 @@ P_T = {np.dtype(np.int32): torch.int32, np.dtype(np.uint32): torch.uint32,
 
 
 def one(rng):
-    kinds = ["keys", "pairs", "seg", "sort", "sortp", "pieces", "host", "hostp", "rec", "hostrec"]
+    kinds = ["keys", "pairs", "seg", "sort", "sortp", "pieces", "host", "hostp", "rec", "hostrec",
+             "recapi"]
     kind = kinds[int(rng.integers(0, len(kinds)))]
     dt = [np.int32, np.uint32, np.uint64][int(rng.integers(0, 3))]
     if kind == "seg" and dt == np.uint64:
@@ -122,6 +123,31 @@ def one(rng):
         out = np.empty(m + n, dt)
         P.merge_parallel(a, b, out, int(rng.integers(1, 40)))
         assert np.array_equal(out, port.merge(a, b)), tag
+    elif kind == "recapi":  # co_rank / plan / full report over records = the key arrays'
+        m, n = min(m, 200_000), min(n, 200_000)
+        a, b = a[:m], b[:n]
+        size_b = 16 if dt == np.uint64 else (12 if rng.random() < 0.5 else 8)
+        rd = P.record_dtype(dt, 12 if size_b == 12 else None)
+        ra, rb = np.zeros(m, rd), np.zeros(n, rd)
+        ra["key"], rb["key"] = a, b
+        for i in {0, m + n, int(rng.integers(0, m + n + 1)), int(rng.integers(0, m + n + 1))}:
+            st = P.CoRankStats()
+            got = P.co_rank_records(i, ra, rb, stats=st)
+            assert (got, (st.iterations, st.comparisons)) == port.co_rank(i, a, b, stats=True), tag
+        w = int(rng.integers(1, 40))
+        synced = bool(rng.integers(0, 2))
+        bs, its, cmp = port.merge_report(a, b, w, synced)
+        out = np.zeros(m + n, rd)
+        rep = P.merge_parallel_records(ra, rb, out, w, synced=synced,
+                                       opts=P.MergeOptions(count_comparisons=True))
+        assert np.array_equal(out["key"], port.merge(a, b)), tag
+        assert rep.block_sizes == [int(x) for x in bs[:w]], tag
+        assert rep.corank_iterations == [int(x) for x in its], tag
+        assert rep.comparisons == cmp, tag
+        pl = P.plan_records(ra, rb, w)
+        assert [x.out_end - x.out_begin for x in pl] == rep.block_sizes, tag
+        assert all(x.a_end - x.a_begin + x.b_end - x.b_begin == x.out_end - x.out_begin
+                   for x in pl), tag
     elif kind in ("rec", "hostrec"):  # records: 8 / 12 / 16 bytes, merged by key
         size_b = 16 if dt == np.uint64 else (12 if rng.random() < 0.5 else 8)
         rd = P.record_dtype(dt, 12 if size_b == 12 else None)
