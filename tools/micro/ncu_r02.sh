@@ -1,7 +1,7 @@
 # round-2 ncu evidence: one `ncu --set full` capture of the merge kernel per
 # config (after warm-up launches), exported on the box as raw / source CSV
 # pages (reports are large), then the launch list of the bench command
-for c in C1 C2 C3 C4 C5 C2r C4r; do
+for c in C1 C2 C3 C4 C5 C2r C2t C4r X5; do
   timeout 600 ncu --set full --import-source on --clock-control none \
     -k regex:'merge_(pipe|small)_kernel' --launch-skip 3 -c 1 -o gpurun_out/r02_$c -f \
     python tools/run_config.py $c --reps 4 > gpurun_out/r02_ncu_$c.log 2>&1
