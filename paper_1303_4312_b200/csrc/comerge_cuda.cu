@@ -1875,6 +1875,27 @@ size_t sort_pairs_ws_bytes(size_t n) {
 inline bool sort_pdl() { return !(g_tune_flags & 16777216); }
 
 // Stable key-value merge sort: as sort_device, the payload moving with its key.
+// block sorts: dynamic shared memory, opted in once per device
+template <typename K, bool SMALL>
+void launch_block_sort_pairs(const K* in, const uint32_t* in_v, K* out, uint32_t* out_v,
+                             uint64_t n, cudaStream_t s) {
+    using C = sort_pairs_cfg<K, SMALL>;
+    static std::once_flag once[kMaxDevices];
+    std::call_once(once[current_device()], [] {
+        cudaFuncSetAttribute(block_sort_pairs_kernel<K, SMALL>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem));
+    });
+    block_sort_pairs_kernel<K, SMALL><<<unsigned(div_up(n, C::R)), C::NT, C::kSmem, s>>>(
+        in, in_v, out, out_v, n);
+}
+
+// Base run of a sort of n elements: the full-size run, or half of it (twice the
+// CTAs) while the input is under one full-size run per SM.
+template <typename CFG_BIG, typename CFG_SMALL>
+bool sort_small_runs(uint64_t n) {
+    return n < uint64_t(CFG_BIG::R) * uint64_t(sm_count());
+}
+
 template <typename K>
 int sort_pairs_device(const K* keys, const uint32_t* vals, size_t n, K* out, uint32_t* out_v,
                       void* ws, size_t ws_bytes, cudaStream_t s) {
@@ -1886,13 +1907,18 @@ int sort_pairs_device(const K* keys, const uint32_t* vals, size_t n, K* out, uin
         (vals != out_v && overlaps(vals, n * 4, out_v, n * 4)) ||
         overlaps(out, n * sizeof(K), out_v, n * 4))
         return fail(COMERGE_E_INVALID, "sort_pairs: outputs must not partially overlap the inputs or each other");
-    constexpr uint64_t R = sort_pairs_cfg<K>::R;
-    const uint64_t nblocks = div_up(n, R);
+    const bool small = sort_small_runs<sort_pairs_cfg<K, false>, sort_pairs_cfg<K, true>>(n);
+    const uint64_t R = small ? sort_pairs_cfg<K, true>::R : sort_pairs_cfg<K, false>::R;
+    auto block_sort = [&](K* ok, uint32_t* ov) {
+        if (small)
+            launch_block_sort_pairs<K, true>(keys, vals, ok, ov, n, s);
+        else
+            launch_block_sort_pairs<K, false>(keys, vals, ok, ov, n, s);
+    };
     uint32_t passes = 0;
     while ((R << passes) < n) ++passes;
     if (passes == 0) {
-        block_sort_pairs_kernel<K><<<unsigned(nblocks), sort_pairs_cfg<K>::NT, 0, s>>>(
-            keys, vals, out, out_v, n);
+        block_sort(out, out_v);
         return check_launch("comerge: block sort launch");
     }
     scratch sc;
@@ -1909,8 +1935,7 @@ int sort_pairs_device(const K* keys, const uint32_t* vals, size_t n, K* out, uin
     uint32_t* bv[2] = {direct ? out_v : tv[1], tv[0]};
     K* ck = bk[passes & 1];
     uint32_t* cv = bv[passes & 1];
-    block_sort_pairs_kernel<K><<<unsigned(nblocks), sort_pairs_cfg<K>::NT, 0, s>>>(keys, vals, ck,
-                                                                                  cv, n);
+    block_sort(ck, cv);
     if (int rc = check_launch("comerge: block sort launch")) return rc;
     uint64_t L = R;
     for (uint32_t p = 0; p < passes; ++p, L *= 2) {
@@ -1933,6 +1958,17 @@ int sort_pairs_device(const K* keys, const uint32_t* vals, size_t n, K* out, uin
     return COMERGE_OK;
 }
 
+template <typename K, bool SMALL>
+void launch_block_sort(const K* in, K* out, uint64_t n, cudaStream_t s) {
+    using C = sort_cfg<K, SMALL>;
+    static std::once_flag once[kMaxDevices];
+    std::call_once(once[current_device()], [] {
+        cudaFuncSetAttribute(block_sort_kernel<K, SMALL>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::kSmem));
+    });
+    block_sort_kernel<K, SMALL><<<unsigned(div_up(n, C::R)), C::NT, C::kSmem, s>>>(in, out, n);
+}
+
 template <typename K>
 int sort_device(const K* keys, size_t n, K* out, void* ws, size_t ws_bytes, cudaStream_t s) {
     if (n && (!keys || !out)) return fail(COMERGE_E_INVALID, "sort: null pointer");
@@ -1940,12 +1976,18 @@ int sort_device(const K* keys, size_t n, K* out, void* ws, size_t ws_bytes, cuda
     if (n > (size_t(1) << 40)) return fail(COMERGE_E_LENGTH, "sort: more than 2^40 elements");
     if (keys != out && overlaps(keys, n * sizeof(K), out, n * sizeof(K)))
         return fail(COMERGE_E_INVALID, "sort: output must not partially overlap the input");
-    constexpr uint64_t R = sort_cfg<K>::R;
-    const uint64_t nblocks = div_up(n, R);
+    const bool small = sort_small_runs<sort_cfg<K, false>, sort_cfg<K, true>>(n);
+    const uint64_t R = small ? sort_cfg<K, true>::R : sort_cfg<K, false>::R;
+    auto block_sort = [&](K* dst) {
+        if (small)
+            launch_block_sort<K, true>(keys, dst, n, s);
+        else
+            launch_block_sort<K, false>(keys, dst, n, s);
+    };
     uint32_t passes = 0;
     while ((R << passes) < n) ++passes;
     if (passes == 0) {
-        block_sort_kernel<K><<<unsigned(nblocks), sort_cfg<K>::NT, 0, s>>>(keys, out, n);
+        block_sort(out);
         return check_launch("comerge: block sort launch");
     }
     scratch sc;
@@ -1961,7 +2003,7 @@ int sort_device(const K* keys, size_t n, K* out, void* ws, size_t ws_bytes, cuda
     const bool direct = aligned16(out);
     K* bufs[2] = {direct ? out : t1, t0};  // bufs[x]: the result of a stage with passes-left parity x
     K* cur = bufs[passes & 1];
-    block_sort_kernel<K><<<unsigned(nblocks), sort_cfg<K>::NT, 0, s>>>(keys, cur, n);
+    block_sort(cur);
     if (int rc = check_launch("comerge: block sort launch")) return rc;
     uint64_t L = R;
     for (uint32_t p = 0; p < passes; ++p, L *= 2) {

@@ -27,6 +27,39 @@
 
 namespace comerge_b200 {
 
+// elements per thread of the block sorts (odd: see sort_cfg) and base runs.
+// Measured on 2^26 keys (ms; R = 8192 / 4096 / 4096 unless noted): 32-bit keys
+// VT 17: 1.804, 21: 1.762, 25: 1.723, 29: 1.709, 33: 1.671, 41: 1.704, 49:
+// 1.723, 65: 1.755; R = 16384 with VT 33: 1.664, VT 65: 1.626 (R = 32768:
+// 1.699).  64-bit keys VT 9: 3.609, 13: 3.451, 17: 3.354, 25: 3.359, 33: 3.285;
+// R = 8192 with VT 33: 3.147 (VT 17: 3.333, VT 65: 3.541).  32-bit pairs VT 9:
+// 3.477, 13: 3.401, 17: 3.337, 21: 3.408, 33: 3.437; R = 8192 with VT 17:
+// 3.289, VT 33: 3.267 (VT 65: 3.879).  More keys per thread amortise the split
+// search of every round and leave fewer block-wide rounds (5 warp-local rounds
+// + log2(warps)); a power-of-two warp count keeps the last round full.
+#ifndef SORT_VT32
+#define SORT_VT32 65
+#endif
+#ifndef SORT_VT64
+#define SORT_VT64 33
+#endif
+#ifndef SORTP_VT
+#define SORTP_VT 33
+#endif
+// base runs (powers of two): 32-bit keys, 64-bit keys, 32-bit pairs, 64-bit pairs
+#ifndef SORT_R32
+#define SORT_R32 16384
+#endif
+#ifndef SORT_R64
+#define SORT_R64 8192
+#endif
+#ifndef SORTP_R32
+#define SORTP_R32 8192
+#endif
+#ifndef SORTP_R64
+#define SORTP_R64 4096
+#endif
+
 // Base runs of R elements (a power of two: the merge passes' run arithmetic
 // is shifts) sorted by NA = ceil(R / VT) threads of VT elements each, VT ODD:
 // thread t's elements sit at s[t*VT + v], an odd word stride, so the staging
@@ -34,14 +67,19 @@ namespace comerge_b200 {
 // can run the pipeline consumers' lean serial merge on plain shared addresses
 // (merge_serial.cuh, ~12 instructions per output).  The last slots (R .. NA*VT)
 // hold padding keys.
-template <typename K>
+// SMALL: half the run with half the keys per thread -- twice the CTAs -- for
+// inputs of fewer than one full-size run per SM (the host chooses).
+template <typename K, bool SMALL = false>
 struct sort_cfg {
-    static constexpr int VT = sizeof(K) == 8 ? 9 : 17;
-    static constexpr int R = sizeof(K) == 8 ? 4096 : 8192;  // base run (a power of two)
+    static constexpr int VTB = sizeof(K) == 8 ? SORT_VT64 : SORT_VT32;
+    static constexpr int RB = sizeof(K) == 8 ? SORT_R64 : SORT_R32;
+    static constexpr int VT = SMALL ? (VTB + 1) / 2 : VTB;
+    static constexpr int R = SMALL ? RB / 2 : RB;           // base run (a power of two)
     static constexpr int NA = (R + VT - 1) / VT;            // threads holding elements
-    static constexpr int NT = (NA + 31) / 32 * 32;          // 512 / 480
+    static constexpr int NT = (NA + 31) / 32 * 32;
     static constexpr int S = NA * VT;                       // slots incl. padding
-    static_assert(NA <= NT && (R & (R - 1)) == 0, "block sort shape");
+    static constexpr size_t kSmem = size_t(S + 4) * sizeof(K);  // dynamic shared memory
+    static_assert(NA <= NT && (R & (R - 1)) == 0 && VT % 2 == 1, "block sort shape");
 };
 
 // Batcher's odd-even merge sort network over the VT registers of a thread
@@ -204,33 +242,38 @@ __device__ __forceinline__ void block_sort_body(K* s, uint32_t* sv, const K* __r
     }
 }
 
-template <typename K>
-__global__ void __launch_bounds__(sort_cfg<K>::NT)
+template <typename K, bool SMALL>
+__global__ void __launch_bounds__(sort_cfg<K, SMALL>::NT)
     block_sort_kernel(const K* __restrict__ in, K* __restrict__ out, uint64_t n) {
-    __shared__ __align__(16) K s[sort_cfg<K>::S + 4];
-    block_sort_body<K, sort_cfg<K>, false>(s, nullptr, in, nullptr, out, nullptr, n);
+    extern __shared__ __align__(16) unsigned char bs_smem[];
+    block_sort_body<K, sort_cfg<K, SMALL>, false>(reinterpret_cast<K*>(bs_smem), nullptr, in,
+                                                  nullptr, out, nullptr, n);
 }
 
-// Key-value variant: the uint32 payload moves with its key (runs of 4096
-// pairs, 2048 for 64-bit keys; keys and payloads in two shared arrays within
-// the 48 KB static limit).
-template <typename K>
+// Key-value variant: the uint32 payload moves with its key (runs of 8192
+// pairs, 4096 for 64-bit keys; keys and payloads in two shared arrays).
+template <typename K, bool SMALL = false>
 struct sort_pairs_cfg {
-    static constexpr int VT = 9;
-    static constexpr int R = sizeof(K) == 8 ? 2048 : 4096;
+    static constexpr int VT = SMALL ? (SORTP_VT + 1) / 2 : SORTP_VT;
+    static constexpr int RB = sizeof(K) == 8 ? SORTP_R64 : SORTP_R32;
+    static constexpr int R = SMALL ? RB / 2 : RB;
     static constexpr int NA = (R + VT - 1) / VT;
-    static constexpr int NT = (NA + 31) / 32 * 32;  // 480 / 256
+    static constexpr int NT = (NA + 31) / 32 * 32;
     static constexpr int S = NA * VT;
-    static_assert(NA <= NT && (R & (R - 1)) == 0, "block sort shape");
+    static constexpr size_t kKeys = (size_t(S + 4) * sizeof(K) + 15) / 16 * 16;
+    static constexpr size_t kSmem = kKeys + size_t(S + 4) * 4;  // keys, then payloads
+    static_assert(NA <= NT && (R & (R - 1)) == 0 && VT % 2 == 1, "block sort shape");
 };
 
-template <typename K>
-__global__ void __launch_bounds__(sort_pairs_cfg<K>::NT)
+template <typename K, bool SMALL>
+__global__ void __launch_bounds__(sort_pairs_cfg<K, SMALL>::NT)
     block_sort_pairs_kernel(const K* __restrict__ in, const uint32_t* __restrict__ in_v,
                             K* __restrict__ out, uint32_t* __restrict__ out_v, uint64_t n) {
-    __shared__ __align__(16) K s[sort_pairs_cfg<K>::S + 4];
-    __shared__ uint32_t sv[sort_pairs_cfg<K>::S + 4];
-    block_sort_body<K, sort_pairs_cfg<K>, true>(s, sv, in, in_v, out, out_v, n);
+    extern __shared__ __align__(16) unsigned char bs_smem[];
+    using C = sort_pairs_cfg<K, SMALL>;
+    block_sort_body<K, C, true>(reinterpret_cast<K*>(bs_smem),
+                                reinterpret_cast<uint32_t*>(bs_smem + C::kKeys), in, in_v, out,
+                                out_v, n);
 }
 
 }  // namespace comerge_b200

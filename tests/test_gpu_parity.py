@@ -574,7 +574,7 @@ def test_rank_shards_concatenate(cuda, port):
 # merge-pass mode.  Oracle: oracle_merge_sort (repeated stable_merge of
 # adjacent runs, merge.hpp:52-68), bit-exact.
 
-SORT_RUN = {np.dtype(np.int32): 8192, np.dtype(np.uint32): 8192, np.dtype(np.uint64): 4096}
+SORT_RUN = {np.dtype(np.int32): 16384, np.dtype(np.uint32): 16384, np.dtype(np.uint64): 8192}
 
 
 @pytest.mark.parametrize("dt", [np.int32, np.uint32, np.uint64])
@@ -680,7 +680,7 @@ def test_comparison_counts_large_host_pipeline(cuda, port):
 @pytest.mark.parametrize("dt", [np.int32, np.uint32, np.uint64])
 def test_sort_pairs_stability_against_oracle(cuda, port, dt):
     """Key-value sort: payload = input index, so stability is visible."""
-    R = 4096 if np.dtype(dt).itemsize == 4 else 2048
+    R = 8192 if np.dtype(dt).itemsize == 4 else 4096
     rng = np.random.default_rng(8)
     for n in (0, 1, 9, R - 1, R, R + 1, 2 * R + 3, 5 * R + 7, 100_003, 1 << 20):
         for alphabet in (2, 1000, None):
