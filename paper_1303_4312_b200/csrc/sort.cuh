@@ -67,6 +67,17 @@ namespace comerge_b200 {
 // can run the pipeline consumers' lean serial merge on plain shared addresses
 // (merge_serial.cuh, ~12 instructions per output).  The last slots (R .. NA*VT)
 // hold padding keys.
+// CTAs per SM the shared memory allows (227 KB, 1 KB reserved per CTA), as the
+// kernels' launch bound -- the register allocation must not be what lowers the
+// occupancy (64-bit keys at 86 registers fell from 3 to 2 CTAs per SM) --
+// but never forcing fewer than 64 registers per thread.
+constexpr int block_sort_min_blocks(size_t smem, int nt) {
+    const int by_smem = int(size_t(227) * 1024 / (smem + 1024));
+    const int by_regs = 1024 / nt;
+    const int b = by_smem < by_regs ? by_smem : by_regs;
+    return b < 1 ? 1 : b;
+}
+
 // SMALL: half the run with half the keys per thread -- twice the CTAs -- for
 // inputs of fewer than one full-size run per SM (the host chooses).
 template <typename K, bool SMALL = false>
@@ -79,6 +90,7 @@ struct sort_cfg {
     static constexpr int NT = (NA + 31) / 32 * 32;
     static constexpr int S = NA * VT;                       // slots incl. padding
     static constexpr size_t kSmem = size_t(S + 4) * sizeof(K);  // dynamic shared memory
+    static constexpr int kMinBlocks = block_sort_min_blocks(kSmem, NT);
     static_assert(NA <= NT && (R & (R - 1)) == 0 && VT % 2 == 1, "block sort shape");
 };
 
@@ -124,58 +136,56 @@ __device__ __forceinline__ void transposition_sort(K (&k)[VT], uint32_t (&p)[VT]
     }
 }
 
-// One merge round of the block sort: sorted lists of W slots are merged in
-// pairs (the last list of the array may be short or missing); thread t takes
-// the VT outputs from its merge-path split (the Lemma-1 split of
-// corank.hpp:93-94, ties to the left list as merge.hpp:22-31).  Rounds whose
-// list pairs lie inside one warp's 32*VT slots synchronise the warp only.
-template <typename K, int VT, int S, int W, bool HAS_V>
-__device__ __forceinline__ void block_sort_round(K* s, uint32_t* sv, int t, bool active,
-                                                 K (&k)[VT], uint32_t (&p)[VT]) {
-    constexpr bool kWarpLocal = 2 * W <= 32 * VT;
-    if constexpr (kWarpLocal) __syncwarp(); else __syncthreads();  // previous reads are done
-    if (active) {
-#pragma unroll
-        for (int v = 0; v < VT; ++v) {
-            s[t * VT + v] = k[v];
-            if constexpr (HAS_V) sv[t * VT + v] = p[v];
-        }
-    }
-    if constexpr (kWarpLocal) __syncwarp(); else __syncthreads();
-    if (!active) return;
-    const int d = t * VT;
-    const int a0 = d / (2 * W) * (2 * W);
-    const int la = S - a0 < W ? S - a0 : W;
-    const int b0 = a0 + la;
-    const int lb = S - b0 < W ? S - b0 : W;
-    uint32_t src[VT];
-    // Lemma-1 split of the thread's diagonal (the data-dependent search of
-    // merge_serial.cuh; a branch-free fixed-trip form -- 8 instead of 13
-    // instructions per iteration -- measured 2^26 int32 keys 1.860 instead of
-    // 1.805 ms: threads near a list pair's ends have narrow brackets)
-    const int diag = d - a0;
-    const K* sA = s + a0;
-    const K* sB = s + b0;
-    const int j = smem_split<K>(sA, la, sB, lb, diag);
-    const uint32_t pa0 = smem_addr(sA), pb0 = smem_addr(sB);
-    constexpr uint32_t SZ = sizeof(K);
-    serial_merge<K, VT, HAS_V, false>(pa0 + uint32_t(j) * SZ, pa0 + uint32_t(la) * SZ,
-                                      pb0 + uint32_t(diag - j) * SZ, pb0 + uint32_t(lb) * SZ, 0,
-                                      0, VT, k, src);
-    if constexpr (HAS_V) {
-        const uint32_t base = smem_addr(s);
-        constexpr int SH = sizeof(K) == 8 ? 3 : 2;
-#pragma unroll
-        for (int v = 0; v < VT; ++v) p[v] = sv[(src[v] - base) >> SH];
-    }
-}
-
-template <typename K, int VT, int S, int W, bool HAS_V>
+// The merge rounds of the block sort: round k merges sorted lists of
+// W = VT << k slots in pairs (the last list of the array may be short or
+// missing); thread t takes the VT outputs from its merge-path split (the
+// Lemma-1 split of corank.hpp:93-94, ties to the left list as
+// merge.hpp:22-31).  A list pair spans 2^(k+1) threads, so its start is a
+// shift of the thread index.  Rounds whose pairs lie inside one warp's 32*VT
+// slots (k < 5) synchronise the warp only.  One rolled loop over the rounds:
+// unrolled per round, the 8-9 copies of the VT-step merge overflowed the
+// instruction cache (ncu: 9% of the stall samples on no_instructions).
+template <typename K, int VT, int S, bool HAS_V>
 __device__ __forceinline__ void block_sort_rounds(K* s, uint32_t* sv, int t, bool active,
                                                   K (&k)[VT], uint32_t (&p)[VT]) {
-    if constexpr (W < S) {
-        block_sort_round<K, VT, S, W, HAS_V>(s, sv, t, active, k, p);
-        block_sort_rounds<K, VT, S, 2 * W, HAS_V>(s, sv, t, active, k, p);
+#pragma unroll 1
+    for (int r = 0; (VT << r) < S; ++r) {
+        const int W = VT << r;
+        const bool warp_local = r < 5;
+        if (warp_local) __syncwarp(); else __syncthreads();  // previous reads are done
+        if (active) {
+#pragma unroll
+            for (int v = 0; v < VT; ++v) {
+                s[t * VT + v] = k[v];
+                if constexpr (HAS_V) sv[t * VT + v] = p[v];
+            }
+        }
+        if (warp_local) __syncwarp(); else __syncthreads();
+        if (!active) continue;
+        const int a0 = ((t >> (r + 1)) << (r + 1)) * VT;
+        const int la = S - a0 < W ? S - a0 : W;
+        const int b0 = a0 + la;
+        const int lb = S - b0 < W ? S - b0 : W;
+        uint32_t src[VT];
+        // Lemma-1 split of the thread's diagonal (the data-dependent search of
+        // merge_serial.cuh; a branch-free fixed-trip form -- 8 instead of 13
+        // instructions per iteration -- measured 2^26 int32 keys 1.860 instead
+        // of 1.805 ms: threads near a list pair's ends have narrow brackets)
+        const int diag = t * VT - a0;
+        const K* sA = s + a0;
+        const K* sB = s + b0;
+        const int j = smem_split<K>(sA, la, sB, lb, diag);
+        const uint32_t pa0 = smem_addr(sA), pb0 = smem_addr(sB);
+        constexpr uint32_t SZ = sizeof(K);
+        serial_merge<K, VT, HAS_V, false>(pa0 + uint32_t(j) * SZ, pa0 + uint32_t(la) * SZ,
+                                          pb0 + uint32_t(diag - j) * SZ, pb0 + uint32_t(lb) * SZ,
+                                          0, 0, VT, k, src);
+        if constexpr (HAS_V) {
+            const uint32_t base = smem_addr(s);
+            constexpr int SH = sizeof(K) == 8 ? 3 : 2;
+#pragma unroll
+            for (int v = 0; v < VT; ++v) p[v] = sv[(src[v] - base) >> SH];
+        }
     }
 }
 
@@ -226,7 +236,7 @@ __device__ __forceinline__ void block_sort_body(K* s, uint32_t* sv, const K* __r
         else
             network_sort<K, VT>(k);
     }
-    block_sort_rounds<K, VT, S, VT, HAS_V>(s, sv, t, active, k, p);
+    block_sort_rounds<K, VT, S, HAS_V>(s, sv, t, active, k, p);
     __syncthreads();
     if (active) {
 #pragma unroll
@@ -243,7 +253,7 @@ __device__ __forceinline__ void block_sort_body(K* s, uint32_t* sv, const K* __r
 }
 
 template <typename K, bool SMALL>
-__global__ void __launch_bounds__(sort_cfg<K, SMALL>::NT)
+__global__ void __launch_bounds__(sort_cfg<K, SMALL>::NT, sort_cfg<K, SMALL>::kMinBlocks)
     block_sort_kernel(const K* __restrict__ in, K* __restrict__ out, uint64_t n) {
     extern __shared__ __align__(16) unsigned char bs_smem[];
     block_sort_body<K, sort_cfg<K, SMALL>, false>(reinterpret_cast<K*>(bs_smem), nullptr, in,
@@ -262,11 +272,12 @@ struct sort_pairs_cfg {
     static constexpr int S = NA * VT;
     static constexpr size_t kKeys = (size_t(S + 4) * sizeof(K) + 15) / 16 * 16;
     static constexpr size_t kSmem = kKeys + size_t(S + 4) * 4;  // keys, then payloads
+    static constexpr int kMinBlocks = block_sort_min_blocks(kSmem, NT);
     static_assert(NA <= NT && (R & (R - 1)) == 0 && VT % 2 == 1, "block sort shape");
 };
 
 template <typename K, bool SMALL>
-__global__ void __launch_bounds__(sort_pairs_cfg<K, SMALL>::NT)
+__global__ void __launch_bounds__(sort_pairs_cfg<K, SMALL>::NT, sort_pairs_cfg<K, SMALL>::kMinBlocks)
     block_sort_pairs_kernel(const K* __restrict__ in, const uint32_t* __restrict__ in_v,
                             K* __restrict__ out, uint32_t* __restrict__ out_v, uint64_t n) {
     extern __shared__ __align__(16) unsigned char bs_smem[];
