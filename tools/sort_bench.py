@@ -50,15 +50,17 @@ for n, dt, width in ((1 << 20, torch.int32, 1 << 31), (1 << 24, torch.int32, 1 <
 
 # key-value (uint32 payload) sorts
 for n, dt, width in ((1 << 24, torch.int32, 1 << 31), (1 << 26, torch.int32, 1 << 31),
-                     (1 << 26, torch.int32, 16)):
+                     (1 << 26, torch.int32, 16), (1 << 26, torch.int64, 1 << 62)):
     k = keys(n, dt, width)
     v = torch.arange(n, dtype=torch.int32, device="cuda").view(torch.uint32)
     ok, ov = torch.empty_like(k), torch.empty_like(v)
-    ws = torch.empty(P.sort_pairs_workspace_bytes(n, k.dtype), dtype=torch.uint8, device="cuda")
-    t_ours = timeit(lambda: P.sort_pairs(k, v, out_keys=ok, out_vals=ov, workspace=ws))
+    ku = k.view(torch.uint64) if dt == torch.int64 else k  # uint64 keys (values < 2^63)
+    oku = ok.view(torch.uint64) if dt == torch.int64 else ok
+    ws = torch.empty(P.sort_pairs_workspace_bytes(n, ku.dtype), dtype=torch.uint8, device="cuda")
+    t_ours = timeit(lambda: P.sort_pairs(ku, v, out_keys=oku, out_vals=ov, workspace=ws))
     t_torch = timeit(lambda: torch.sort(k, stable=True))  # values + int64 indices
     ref = torch.sort(k, stable=True)
     equal = torch.equal(ok, ref.values) and torch.equal(ov.view(torch.int32).long(), ref.indices)
-    print(f"pairs n=2^{n.bit_length() - 1} int32 width {width:>11d}: merge sort {t_ours:7.3f} ms "
+    print(f"pairs n=2^{n.bit_length() - 1} {str(ku.dtype)[6:]} width {width:>11d}: merge sort {t_ours:7.3f} ms "
           f"({n / t_ours / 1e6:6.2f} G pairs/s)  torch.sort(stable, indices) {t_torch:7.3f} ms  "
           f"equal={equal}")
