@@ -891,8 +891,11 @@ def run_split(args, dist, rank, world, device, peak, flush):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    # defaults: a 50-step timed region (~55 ms for C4) keeps one host-side hiccup
+    # of a millisecond or two (seen once: 20 steps at 1.090 instead of 1.004 ms)
+    # within a few percent of the whole-job figure
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default=HEADLINE, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--replicas", action="store_true",
