@@ -822,6 +822,46 @@ def sort_extras(device, flush, reps=5):
     return out
 
 
+def split_e2e(dm, local, dist, device, calls, total_bytes):
+    """End to end at N GPUs: every call copies each rank's input pieces from
+    pinned host memory to its GPU, waits until every rank's pieces are in place
+    (the peers read them over NVLink), runs the rank's range merge and copies
+    its output range back to pinned host memory.  Wall clock between barriers,
+    max over ranks; median of the calls after two warm-up calls."""
+    import torch
+    host = [x.cpu().pin_memory() for x in local]
+    outs = [dm.out] + ([dm.out_vals] if dm.out_vals is not None else [])
+    hout = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in outs]
+    times = []
+    for it in range(calls + 2):
+        torch.cuda.synchronize(device)
+        dist.barrier()
+        t0 = time.perf_counter()
+        for d, h in zip(local, host):
+            d.copy_(h, non_blocking=True)
+        torch.cuda.synchronize(device)
+        dist.barrier()  # every rank's pieces are resident before any rank's kernel reads them
+        dm.run()
+        for h, o in zip(hout, outs):
+            h.copy_(o, non_blocking=True)
+        torch.cuda.synchronize(device)
+        dt = time.perf_counter() - t0
+        # wall clock between barriers spans every rank's work: max over ranks
+        on_dev = dist.get_backend() == "nccl"
+        w = torch.tensor([dt], dtype=torch.float64, device=device if on_dev else "cpu")
+        dist.all_reduce(w, op=dist.ReduceOp.MAX)
+        job = float(w.cpu()[0])
+        if it >= 2:
+            times.append(job)
+    med = statistics.median(times)
+    return dict(value=dm.total / med, unit="elements/s",
+                stat=f"median of {calls} calls, max over ranks",
+                h2d_bytes_per_step=int(total_bytes), d2h_bytes_per_step=int(total_bytes),
+                ms_per_step=1e3 * med,
+                path="per rank: H2D of its pieces, range merge over peer windows "
+                     "(comerge_cuda_merge_*_pieces_*), D2H of its output range")
+
+
 def run_split(args, dist, rank, world, device, peak, flush):
     """ONE merge of the config split across the ranks (Algorithm 2 with a
     worker per GPU): rank r holds the r-th piece of A and B (cut at r/world,
@@ -865,6 +905,8 @@ def run_split(args, dist, rank, world, device, peak, flush):
                                       device)
     if shared_devices(dist):  # per-rank kernel time: the summed one over the ranks
         kern /= world
+    e2e = split_e2e(dm, [x for x in (pa, pb, pav, pbv) if x is not None], dist, device,
+                    max(3, min(args.steps, 9)), (m + n) * elem_bytes(cfg))
     dm.close()
     total = m + n
     balg = 2 * total * elem_bytes(cfg)
@@ -880,7 +922,7 @@ def run_split(args, dist, rank, world, device, peak, flush):
                           unit="GB/s", frac=balg / world / (kern * 1e-3) / 1e9 / peak,
                           traffic=None, kernel="merge_pipe_kernel (pieced range, per rank)",
                           algorithmic_bytes_per_launch=balg // world),
-            cpu_baseline=None, e2e=None, clocks=res["clocks"],
+            cpu_baseline=None, e2e=e2e, clocks=res["clocks"],
             gpu_launches=args.steps * launches_per_step(res["path"]))
         if shared_devices(dist):
             line["note"] = (f"{world} ranks on {torch.cuda.device_count()} GPU(s): a functional run "
