@@ -314,8 +314,8 @@ merge_report merge_parallel_synced(const A& a, const B& b, Out&& out, std::size_
 
 /// std::allocator replacement handing out page-locked host memory
 /// (comerge_cuda_host_alloc): host-buffer merges of vectors allocated with it
-/// copy at PCIe rate (pageable storage is staged by the driver, ~7x slower on
-/// C4).  std::vector<T, comerge::cuda::pinned_allocator<T>> is a contiguous
+/// copy at PCIe rate (pageable storage goes through the library's staging
+/// pool, ~1.9x slower on C4).  std::vector<T, comerge::cuda::pinned_allocator<T>> is a contiguous
 /// range every overload here accepts.
 template <typename T>
 struct pinned_allocator {

@@ -56,8 +56,9 @@ int comerge_cuda_abi_version(void);
 
 /* Page-locked host memory for the host-buffer entry points.  The host
  * pipeline's copies run at PCIe rate only from page-locked buffers (measured
- * on C4: 69 ms pinned, 467 ms from pageable std::vector storage, whose copies
- * the driver stages synchronously); comerge::cuda::pinned_allocator<T> wraps
+ * on C4: 69 ms pinned; from pageable std::vector storage 467 ms through the
+ * driver's synchronous staging, 132 ms through the library's staging pool);
+ * comerge::cuda::pinned_allocator<T> wraps
  * these for std::vector.  Returns COMERGE_OK or COMERGE_E_CUDA. */
 int comerge_cuda_host_alloc(size_t bytes, void** ptr);
 int comerge_cuda_host_free(void* ptr);
