@@ -3,9 +3,9 @@
 //
 //   1. block_sort_kernel: every CTA sorts one run of R elements in shared
 //      memory -- VT (odd) elements per thread by a sorting network in
-//      registers (keys only; the key-value variant uses odd-even
-//      transposition, swapping only on strictly-less, so equal keys keep
-//      their order), then rounds of pairwise merges of the sorted lists
+//      registers (the key-value variant sorts (key, position) composites,
+//      so equal keys keep their order, and gathers the payloads by position
+//      afterwards), then rounds of pairwise merges of the sorted lists
 //      (the first five inside one warp: warp barriers only), each thread
 //      taking VT outputs at its merge-path split (the Lemma-1 split of
 //      corank.hpp:93-94, ties to the left list as merge.hpp:22-31) with the
@@ -44,9 +44,6 @@ namespace comerge_b200 {
 #ifndef SORT_VT64
 #define SORT_VT64 33
 #endif
-#ifndef SORTP_TRANSPOSITION
-#define SORTP_TRANSPOSITION 0
-#endif
 #ifndef SORTP_VT
 #define SORTP_VT 33
 #endif
@@ -67,13 +64,6 @@ namespace comerge_b200 {
 #define SORTP_R64 4096
 #endif
 
-// Base runs of R elements (a power of two: the merge passes' run arithmetic
-// is shifts) sorted by NA = ceil(R / VT) threads of VT elements each, VT ODD:
-// thread t's elements sit at s[t*VT + v], an odd word stride, so the staging
-// accesses of a warp are bank-conflict free without padding and the rounds
-// can run the pipeline consumers' lean serial merge on plain shared addresses
-// (merge_serial.cuh, ~12 instructions per output).  The last slots (R .. NA*VT)
-// hold padding keys.
 // CTAs per SM the shared memory allows (227 KB, 1 KB reserved per CTA), as the
 // kernels' launch bound -- the register allocation must not be what lowers the
 // occupancy (64-bit keys at 86 registers fell from 3 to 2 CTAs per SM) --
@@ -85,6 +75,13 @@ constexpr int block_sort_min_blocks(size_t smem, int nt) {
     return b < 1 ? 1 : b;
 }
 
+// Base runs of R elements (a power of two: the merge passes' run arithmetic
+// is shifts) sorted by NA = ceil(R / VT) threads of VT elements each, VT ODD:
+// thread t's elements sit at s[t*VT + v], an odd word stride, so the staging
+// accesses of a warp are bank-conflict free without padding and the rounds
+// can run the pipeline consumers' lean serial merge on plain shared addresses
+// (merge_serial.cuh, ~12 instructions per output).  The last slots (R .. NA*VT)
+// hold padding keys.
 // SMALL: half the run with half the keys per thread -- twice the CTAs -- for
 // inputs of fewer than one full-size run per SM (the host chooses).
 template <typename K, bool SMALL = false>
@@ -103,9 +100,9 @@ struct sort_cfg {
 
 // Batcher's odd-even merge sort network over the VT registers of a thread
 // (keys only: equal keys are indistinguishable, so the network need not be
-// stable; any VT -- checked by the 0-1 principle for 8, 9, 16, 17): 85
-// compare-exchanges for 17 keys, 28 for 9, against 136 / 36 for odd-even
-// transposition; min / max of 32-bit keys are one instruction each.
+// stable; any VT: the power-of-two network with the comparators beyond VT
+// dropped, checked by the 0-1 principle for 8 .. 21): 85 compare-exchanges for
+// 17 keys, 221 for 33; min / max of 32-bit keys are one instruction each.
 template <typename K, int VT>
 __device__ __forceinline__ void network_sort(K (&k)[VT]) {
 #pragma unroll
@@ -165,26 +162,6 @@ __device__ __forceinline__ void stable_network_sort(K (&k)[VT], uint32_t (&pos)[
                             pos[i + j] = sw ? py : px;
                             pos[i + j + q] = sw ? px : py;
                         }
-    }
-}
-
-// (previous form) odd-even transposition, swapping only on strictly-less, so
-// equal keys keep their order.
-template <typename K, int VT>
-__device__ __forceinline__ void transposition_sort(K (&k)[VT], uint32_t (&p)[VT]) {
-#pragma unroll
-    for (int pass = 0; pass < VT; ++pass) {
-#pragma unroll
-        for (int v = pass & 1; v + 1 < VT; v += 2) {
-            if (k[v + 1] < k[v]) {
-                const K x = k[v];
-                k[v] = k[v + 1];
-                k[v + 1] = x;
-                const uint32_t y = p[v];
-                p[v] = p[v + 1];
-                p[v + 1] = y;
-            }
-        }
     }
 }
 
@@ -281,20 +258,13 @@ __device__ __forceinline__ void block_sort_body(K* s, uint32_t* sv, const K* __r
 #pragma unroll
         for (int v = 0; v < VT; ++v) {
             k[v] = s[t * VT + v];
-#if SORTP_TRANSPOSITION
-            if constexpr (HAS_V) p[v] = sv[t * VT + v];
-#endif
         }
         if constexpr (HAS_V) {
-#if SORTP_TRANSPOSITION
-            transposition_sort<K, VT>(k, p);
-#else
             // the payloads are still where they were loaded: gather by position
             uint32_t pos[VT];
             stable_network_sort<K, VT>(k, pos);
 #pragma unroll
             for (int v = 0; v < VT; ++v) p[v] = sv[t * VT + int(pos[v])];
-#endif
         } else {
             network_sort<K, VT>(k);
         }
