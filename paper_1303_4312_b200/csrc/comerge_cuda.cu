@@ -804,6 +804,17 @@ inline void host_copy(void* dst, const void* src, size_t bytes) {
 inline void host_copy(void* dst, const void* src, size_t bytes) { std::memcpy(dst, src, bytes); }
 #endif
 
+// Chunks between a chunk's enqueue and its drain out of the staging slot
+// (pageable outputs; 1 or 2 with three slots): 2 -- the drained chunk's D2H
+// finished during the previous iteration, so the host never waits for it, and
+// its slot is the next chunk's (lag 1 / lag 2 from pageable arrays: C2 13.3 /
+// 12.7 ms, C3 39.9 / 33.2, C4 127.6 / 114.1, C5 11.3 / 9.8).
+// COMERGE_HOST_LAG=1 restores the shorter lag (benchmarking).
+inline uint64_t host_drain_lag(uint64_t) {
+    static const char* e = std::getenv("COMERGE_HOST_LAG");
+    return e && e[0] == '1' ? 1 : 2;
+}
+
 // The calling thread plus up to hardware_concurrency - 1 workers copy 2 MB
 // pieces of one job at a time.
 class copy_pool {
@@ -1063,6 +1074,7 @@ int merge_host_pipeline(const K* a, const uint32_t* av, uint64_t m, const K* b,
         const cudaError_t ce = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, hs.d2h);
         if (ce != cudaSuccess) rc = cuda_fail(ce, "comerge: host pipeline device->host copy");
     };
+    const uint64_t lag = host_drain_lag(nchunks);
     for (uint64_t c = 0; c < nchunks && rc == COMERGE_OK; ++c) {
         const int sl = int(c % 3);
         unsigned char* base = static_cast<unsigned char*>(buf) + sl * slot_bytes;
@@ -1148,9 +1160,11 @@ int merge_host_pipeline(const K* a, const uint32_t* av, uint64_t m, const K* b,
         *d2h += (i1 - i0) * (sizeof(K) + (HAS_V ? 4 : 0));
         cudaEventRecord(hs.out_done[sl], hs.d2h);
         if (trace) cudaEventRecord(tev[4 * c + 3], hs.d2h);
-        if (c >= 1 && !rc) copy_out(c - 1);  // overlaps this chunk's copies and merge
+        // drain an earlier chunk while this chunk's copies and merge run
+        // (host_drain_lag)
+        if (c >= lag && !rc) copy_out(c - lag);
     }
-    if (!rc && nchunks) copy_out(nchunks - 1);
+    for (uint64_t q = std::min<uint64_t>(lag, nchunks); q >= 1 && !rc; --q) copy_out(nchunks - q);
     cudaEventRecord(hs.t1, hs.comp);
     cudaEventRecord(hs.in_done[0], hs.d2h);  // free the staging after the last copy-out
     cudaStreamWaitEvent(hs.comp, hs.in_done[0], 0);
@@ -1287,6 +1301,7 @@ int merge_segmented_host_pipeline(const K* a, const uint64_t* a_off, uint64_t m,
     js[0] = 0;
     ss[0] = 0;
     bool first = true;
+    const uint64_t lag = host_drain_lag(nchunks);
     for (uint64_t c = 0; c < nchunks && rc == COMERGE_OK; ++c) {
         const int sl = int(c % 3);
         unsigned char* base = slots + sl * slot_bytes;
@@ -1356,9 +1371,9 @@ int merge_segmented_host_pipeline(const K* a, const uint64_t* a_off, uint64_t m,
         d2h_copy(dstO + h, dO + h, (i1 - i0 - h) * sizeof(K));
         *d2h += (i1 - i0) * sizeof(K);
         cudaEventRecord(hs.out_done[sl], hs.d2h);
-        if (c >= 1 && !rc) copy_out(c - 1);
+        if (c >= lag && !rc) copy_out(c - lag);  // as merge_host_pipeline
     }
-    if (!rc && nchunks) copy_out(nchunks - 1);
+    for (uint64_t q = std::min<uint64_t>(lag, nchunks); q >= 1 && !rc; --q) copy_out(nchunks - q);
     cudaEventRecord(hs.t1, hs.comp);
     cudaEventRecord(hs.in_done[0], hs.d2h);
     cudaStreamWaitEvent(hs.comp, hs.in_done[0], 0);
